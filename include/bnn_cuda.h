@@ -1,0 +1,219 @@
+/* bnn_cuda.h — C ABI of the B200 (sm_100a) binarized-layer hot path.
+ *
+ * This is the drop-in boundary for the reference's operator API (namespace bnn,
+ * static lib bnncore, /root/reference/proj). Every entry point names the reference
+ * declaration it replaces. Two families:
+ *
+ *   bnn_*        device pointers, stream-ordered (enqueue only; no host sync unless
+ *                the function says so). Used by the network engine and the benchmark.
+ *   bnn_host_*   host pointers with the reference's exact semantics: H2D copy, kernel,
+ *                D2H copy, synchronous. include/bnn/*.hpp re-exposes these under the
+ *                reference C++ signatures.
+ *
+ * Conventions
+ *   - Packed bit matrices are the reference layout (tensor.hpp:63-98): `lines` lines of
+ *     `ld_words` uint32 words; logical index 32k+b of a line is bit b (LSB first) of word
+ *     k; bit 1 = +1, bit 0 = -1; pad bits past the logical extent are 0. The reference
+ *     stores lines densely (ld_words == ceil(extent/32)); the device entry points accept
+ *     any ld_words >= ceil(extent/32).
+ *   - Return value: BNN_OK (0) or a bnn_status code; bnn_last_error() returns the
+ *     thread-local message, which reproduces the reference exception text where the
+ *     reference throws (ShapeError / EncodingError / ConfigError).
+ *   - The library never frees caller memory. Scratch space is taken from the CUDA
+ *     stream-ordered allocator on the caller's stream.
+ *   - There is no CPU fallback: every compute entry point runs on the GPU or fails with
+ *     BNN_E_CUDA.
+ */
+#ifndef BNN_CUDA_H
+#define BNN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the C ABI is the library's export surface */
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* bnn_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    BNN_OK = 0,
+    BNN_E_SHAPE = 1,    /* reference ShapeError   (tensor.hpp:11-13) */
+    BNN_E_ENCODING = 2, /* reference EncodingError (tensor.hpp:15-17) */
+    BNN_E_CONFIG = 3,   /* reference ConfigError  (tensor.hpp:19-21) */
+    BNN_E_CUDA = 4,     /* CUDA runtime / launch failure, or no sm_100 device */
+    BNN_E_IO = 5        /* reference IoError      (tensor.hpp:23-25) */
+} bnn_status;
+
+const char* bnn_last_error(void);
+int bnn_version(void);
+/* Name of the kernel variant the last GEMM call on this thread dispatched to
+ * ("popc", "umma_i8", ...); for tests and the benchmark. */
+const char* bnn_last_gemm_kernel(void);
+
+/* ConvGeometry (tensor.hpp:101-111), same field order. */
+typedef struct {
+    uint64_t kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w, in_channels, out_channels;
+} bnn_conv_geom;
+
+/* PackedBitMatrix::make (tensor.cpp:32-44): words per line for a packed extent. */
+size_t bnn_words_per_line(size_t extent);
+/* output_dims (tensor.cpp:46-63). BNN_E_SHAPE names the failing axis ("height"/"width"). */
+int bnn_output_dims(const bnn_conv_geom* g, size_t in_h, size_t in_w, size_t* out_h, size_t* out_w);
+
+/* ------------------------------------------------------------------ K1: encoder
+ * pack_cols(sign(x)) (binarize.cpp:55-73 after binarize.cpp:24-27): x is row-major [L, N];
+ * line j (column j) gets bit r = (x[r, j] >= 0). words: N lines x ld_words. */
+int bnn_sign_pack_cols_f32(const float* x, size_t L, size_t N, uint32_t* words, size_t ld_words,
+                           bnn_stream_t s);
+/* pack_rows(sign(x)) (binarize.cpp:39-53): x is row-major [D, L]; line i = row i. */
+int bnn_sign_pack_rows_f32(const float* x, size_t D, size_t L, uint32_t* words, size_t ld_words,
+                           bnn_stream_t s);
+/* Strict pack_cols / pack_rows of an already-binarized matrix: entries must be exactly
+ * +-1. *first_bad_dev (device int64, caller-initialised to INT64_MAX) receives the smallest
+ * row-major index r*cols+c of a non-+-1 entry (atomicMin), which is the entry the reference
+ * reports first (binarize.cpp:12-15). Stream-ordered; the caller checks the flag. */
+int bnn_pack_cols_f32(const float* x, size_t L, size_t N, uint32_t* words, size_t ld_words,
+                      int64_t* first_bad_dev, bnn_stream_t s);
+int bnn_pack_rows_f32(const float* x, size_t D, size_t L, uint32_t* words, size_t ld_words,
+                      int64_t* first_bad_dev, bnn_stream_t s);
+/* unpack (binarize.cpp:75-90); orientation 0 = row-packed [rows, cols], 1 = col-packed. */
+int bnn_unpack_f32(const uint32_t* words, size_t ld_words, size_t rows, size_t cols,
+                   int orientation, float* out, bnn_stream_t s);
+
+/* --------------------------------------------------------------- K2: binary im2col
+ * pack_cols(sign(im2col(x, b, g))) for every image b at once (network.cpp:72,
+ * lowering.cpp:7-43): x is [B, C, H, W]; line n = b*oh*ow + oy*ow + ox, bit
+ * r = (c*kH + kh)*kW + kw. Spatial zero padding encodes as bit 1 (sign(0) = +1). */
+int bnn_im2col_sign_pack_f32(const float* x, size_t B, size_t C, size_t H, size_t W,
+                             const bnn_conv_geom* g, uint32_t* words, size_t ld_words,
+                             bnn_stream_t s);
+
+/* ------------------------------------------------------------ K3: xnor-popcount GEMM
+ * xnor_gemm (kernels.cpp:53-88): w row-packed M lines, x col-packed N lines, both with
+ * ceil(L/32) significant words and zero pad bits. out[i*ldo + j] = L - 2*sum_k popc(w^x),
+ * identical to the reference's 2*sum popc(~(w^x)) - 32*wpl - pad. Rejects 32*wpl > 2^26
+ * like the reference (kernels.cpp:66-68). */
+int bnn_xnor_gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M,
+                      size_t N, size_t L, int32_t* out, size_t ldo, bnn_stream_t s);
+/* Fused epilogue: to_float + bias_add (kernels.cpp:90-107) + reshape_output
+ * (lowering.cpp:87-95). Column j = (img, p) with img = j / P, p = j % P is written to
+ * out[img*M*P + i*P + p]; P = N gives the row-major [M, N] linear layout, P = oh*ow the
+ * [B, D, oh, ow] conv layout. bias may be NULL (zero). */
+int bnn_xnor_gemm_bias_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx,
+                           size_t M, size_t N, size_t L, const float* bias, size_t P, float* out,
+                           bnn_stream_t s);
+
+/* -------------------------------------------------------------- layer forwards
+ * conv_forward_binary (network.cpp:65-79): x [B, C, H, W] -> out [B, D, oh, ow].
+ * packed_w: D lines x ldw words of pack_rows(sign(flatten_weights(W))). */
+int bnn_conv_forward_binary_f32(const float* x, size_t B, size_t C, size_t H, size_t W,
+                                const uint32_t* packed_w, size_t ldw, const float* bias,
+                                const bnn_conv_geom* g, float* out, bnn_stream_t s);
+/* linear_forward_packed (network.cpp:121-126): x [K, N] (features x batch) -> out [M, N]. */
+int bnn_linear_forward_packed_f32(const float* x, size_t K, size_t N, const uint32_t* packed_w,
+                                  size_t ldw, size_t M, const float* bias, float* out,
+                                  bnn_stream_t s);
+
+/* -------------------------------------------------------------- K4: glue ops */
+int bnn_sign_f32(const float* x, size_t n, float* out, bnn_stream_t s);  /* binarize.cpp:24 */
+int bnn_htanh_f32(const float* x, size_t n, float* out, bnn_stream_t s); /* binarize.cpp:34 */
+/* maxpool2 (network.cpp:133-149), x [B, C, H, W] with even H, W. */
+int bnn_maxpool2_f32(const float* x, size_t B, size_t C, size_t H, size_t W, float* out,
+                     bnn_stream_t s);
+/* affine_norm (network.cpp:151-175): out = fmaf(scale[ch], x, shift[ch]) where
+ * ch = (i / plane) % channels. Tensor form: plane = H*W, channels = C. Matrix form
+ * ([features, batch]): plane = batch, channels = features. */
+int bnn_affine_f32(const float* x, size_t n, size_t channels, size_t plane, const float* scale,
+                   const float* shift, float* out, bnn_stream_t s);
+/* flatten_to_columns (network.cpp:177-184): [B, F] -> [F, B]. */
+int bnn_flatten_to_columns_f32(const float* x, size_t B, size_t F, float* out, bnn_stream_t s);
+/* fill_random (tensor.cpp:65-96): out[i] = unit_random(seed, offset + i). Bit-identical to
+ * the CPU generator, so each shard generates its slice of a global tensor. */
+int bnn_fill_random_f32(uint64_t seed, uint64_t offset, size_t n, float* out, bnn_stream_t s);
+uint64_t bnn_mix64(uint64_t seed, uint64_t counter); /* tensor.cpp:65-71 (host) */
+/* fnv1a_hash (bench.cpp:23-33) of a device float buffer; synchronous. */
+int bnn_fnv1a_f32(const float* x, size_t n, uint64_t* hash, bnn_stream_t s);
+
+/* ------------------------------------------------------------- network engine
+ * build_network + network_forward, ExecKernel::Binary (network.cpp:203-420). Weights are
+ * generated on the device with fill_random from the reference seeds and packed once at
+ * build time; forward runs the whole graph on one stream. */
+enum { BNN_LAYER_CONV = 0, BNN_LAYER_LINEAR = 1, BNN_LAYER_MAXPOOL = 2, BNN_LAYER_AFFINE = 3,
+       BNN_LAYER_SIGN = 4, BNN_LAYER_HTANH = 5 }; /* LayerKind order, network.hpp:15 */
+
+typedef struct { /* LayerSpec (network.hpp:23-39), binary kernel, seeded weights */
+    uint32_t kind;
+    uint32_t has_seed;
+    uint64_t seed;
+    uint64_t out_channels, kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w;
+    uint64_t out_features;
+} bnn_layer_spec;
+
+typedef struct bnn_net bnn_net;
+
+/* build_default_network (network.cpp:422-465) into caller storage; returns layer count. */
+size_t bnn_default_spec(bnn_layer_spec* out, size_t cap);
+/* build_network (network.cpp:203-306) on the current CUDA device. ShapeError messages name
+ * the layer ("layer N (kind): ..."). */
+int bnn_net_create(const bnn_layer_spec* layers, size_t n_layers, size_t in_c, size_t in_h,
+                   size_t in_w, uint64_t seed, int binarize_weights, bnn_net** out);
+void bnn_net_destroy(bnn_net* net);
+size_t bnn_net_logits(const bnn_net* net);
+size_t bnn_net_num_layers(const bnn_net* net);
+/* Copy layer i's row-packed weights (dense reference layout, rows x ceil(cols/32)) and
+ * bias / affine parameters to host buffers (NULL to skip). */
+int bnn_net_layer_params(const bnn_net* net, size_t i, uint32_t* packed, size_t* rows,
+                         size_t* cols, float* bias, float* scale, float* shift);
+/* network_forward (network.cpp:330-420): x device [B, C, H, W] -> logits device
+ * [features, B] (the reference layout, network.hpp:104-105). Stream-ordered. */
+int bnn_net_forward(bnn_net* net, const float* x, size_t batch, float* logits, bnn_stream_t s);
+/* Per-layer CUDA-event timing, the device analogue of ForwardOptions::layer_seconds
+ * (network.hpp:93-97). When enabled, bnn_net_forward records events around every layer and
+ * around every GEMM launch on its stream. bnn_net_timing synchronizes on the recorded events
+ * and returns the totals (ms) accumulated since the last reset; arrays have one entry per
+ * layer (NULL to skip). */
+int bnn_net_set_timing(bnn_net* net, int enabled);
+int bnn_net_timing(bnn_net* net, double* layer_ms, double* gemm_ms, size_t* gemm_launches);
+int bnn_net_reset_timing(bnn_net* net);
+/* Layer i: out[0] kind, [1] GEMM M (rows of packed weights), [2] GEMM K, [3] GEMM columns per
+ * image (oh*ow for conv, 1 for linear, 0 otherwise), [4..6] output C, H, W, [7] output flat. */
+int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]);
+/* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */
+size_t bnn_net_last_launches(const bnn_net* net);
+/* Bytes of device memory held by the engine (weights + activation arena). */
+size_t bnn_net_device_bytes(const bnn_net* net);
+
+/* ------------------------------------------------------------- pipe-peak probes
+ * Microbenchmarks behind the K3 candidate choice (bops = 2 per bit-MAC), timed with CUDA
+ * events on stream s at the clocks of the moment; synchronous.
+ *   popc: LOP3 + POPC + IADD register tile (candidate A's inner loop without smem traffic)
+ *   bmma: mma.sync m16n8k256 b1 xor.popc (candidate B; software-emulated on sm_100a) */
+int bnn_probe_popc_peak(double* bops_per_s, double* ms, bnn_stream_t s);
+int bnn_probe_bmma_peak(double* bops_per_s, double* ms, bnn_stream_t s);
+
+/* ------------------------------------------------- host-buffer (reference-exact) API
+ * Same semantics as the reference functions; synchronous; internal stream. */
+int bnn_host_sign_pack(const float* x, size_t rows, size_t cols, int orientation,
+                       int apply_sign, uint32_t* words);
+int bnn_host_xnor_gemm(const uint32_t* w, size_t M, const uint32_t* x, size_t N, size_t L,
+                       int32_t* out);
+int bnn_host_conv_forward_binary(const float* x, size_t B, size_t C, size_t H, size_t W,
+                                 const uint32_t* packed_w, const float* bias,
+                                 const bnn_conv_geom* g, float* out);
+int bnn_host_linear_forward_packed(const float* x, size_t K, size_t N, const uint32_t* packed_w,
+                                   size_t M, const float* bias, float* out);
+int bnn_host_net_forward(bnn_net* net, const float* x, size_t batch, float* logits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* BNN_CUDA_H */

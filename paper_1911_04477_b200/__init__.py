@@ -1,0 +1,15 @@
+"""B200-native (sm_100a) binarized-layer hot path of arXiv 1911.04477.
+
+sign-binarize + bit-pack encoder (K1), binary im2col (K2) and the xnor-popcount GEMM (K3)
+behind the reference's operator API. The compute lives in ``libbnn_b200.so`` (CUDA C++
+behind the C ABI of ``include/bnn_cuda.h``); this package is the Python mirror of the
+reference interface (``api``) plus the ctypes binding (``_lib``).
+"""
+from ._lib import (BnnError, ConfigError, CudaError, EncodingError, IoError, ShapeError,  # noqa: F401
+                   EXPORTS, LIB_PATH, load)
+from .api import (COL_PACKED, ROW_PACKED, ConvGeometry, Network, PackedBitMatrix,  # noqa: F401
+                  affine_norm, bias_add, conv_forward_binary, default_layers, fill_random,
+                  flatten_to_columns, fnv1a_hash, htanh, im2col_sign_pack, linear_forward,
+                  linear_forward_packed, maxpool2, mix64, output_dims, pack_cols, pack_rows,
+                  sign, sign_pack_cols, sign_pack_rows, to_float, unpack, words_per_line,
+                  xnor_gemm)

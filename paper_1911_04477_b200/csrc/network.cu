@@ -1,0 +1,497 @@
+// Device network engine: build_network + network_forward for ExecKernel::Binary
+// (network.cpp:203-420) on one GPU and one stream.
+//
+// Build: parameters are generated ON THE DEVICE with the reference's counter-based
+// generator (bit-identical to fill_random, tensor.cpp:65-96) from the reference seeds
+// (base = layer seed or mix64(net seed, i); weights mix64(base,1), bias mix64(base,2),
+// affine scale mix64(base,3) -> 1 + 0.5u, shift mix64(base,4); network.cpp:217-290) and
+// packed once with K1 (pack_rows(sign(W)), network.cpp:247,271). Nothing is packed inside
+// a forward.
+//
+// Forward (general topology): conv = K2 binary im2col + K3 GEMM with the fused
+// to_float+bias+reshape epilogue; linear = flatten_to_columns (when coming from a tensor)
+// + K1 pack_cols(sign) + K3; maxpool / affine / htanh / sign = K4. Activations ping-pong
+// between two arena buffers sized for the largest layer at the requested batch.
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "bnn_common.cuh"
+
+namespace bnnk {
+
+int launch_pack_cols(const float*, size_t, size_t, uint32_t*, size_t, unsigned long long*,
+                     cudaStream_t);
+int launch_pack_rows(const float*, size_t, size_t, uint32_t*, size_t, unsigned long long*,
+                     cudaStream_t);
+int launch_im2col_sign_pack(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*,
+                            uint32_t*, size_t, cudaStream_t);
+int gemm_f32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, const float*,
+             size_t, float*, cudaStream_t);
+int launch_maxpool2(const float*, size_t, size_t, size_t, size_t, float*, cudaStream_t);
+int launch_affine(const float*, size_t, size_t, size_t, const float*, const float*, float*,
+                  cudaStream_t);
+int launch_transpose(const float*, size_t, size_t, float*, cudaStream_t);
+int launch_fill_random(uint64_t, uint64_t, size_t, float*, cudaStream_t);
+int launch_affine_scale(float*, size_t, cudaStream_t);
+int launch_unary(int, const float*, size_t, float*, cudaStream_t);
+
+namespace {
+
+const char* kind_name(uint32_t k) {
+    static const char* names[] = {"conv", "linear", "maxpool", "affine_norm", "sign", "htanh"};
+    return k < 6 ? names[k] : "?";
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(size_t b) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, b ? b : 16);
+        if (e != cudaSuccess)
+            return fail(BNN_E_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        bytes = b;
+        return BNN_OK;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct Layer {
+    bnn_layer_spec spec{};
+    bnn_conv_geom geom{};
+    size_t rows = 0, cols = 0, wpl = 0;  // packed weights: rows lines x wpl words, L = cols
+    DevBuf packed, bias, scale, shift;
+    size_t n_affine = 0;
+    size_t in_c = 0, in_h = 0, in_w = 0;  // input shape (per image)
+    bool in_flat = false;
+    size_t out_c = 0, out_h = 0, out_w = 0;
+    bool out_flat = false;
+};
+
+}  // namespace bnnk
+
+struct bnn_net {
+    std::vector<std::unique_ptr<bnnk::Layer>> layers;
+    size_t in_c = 0, in_h = 0, in_w = 0, logits = 0;
+    size_t max_act_per_image = 0;   // floats
+    size_t max_lines_words_per_image = 0;
+    // activation arena
+    size_t arena_batch = 0;
+    bnnk::DevBuf act[2], lines;
+    size_t last_launches = 0;
+    size_t weight_bytes = 0;
+    // per-layer CUDA-event timing (the device analogue of ForwardOptions::layer_seconds,
+    // network.hpp:93-97): events are recorded on the forward stream and resolved lazily.
+    bool timing = false;
+    struct Pending { size_t layer; int what; cudaEvent_t a, b; };  // what: 0 layer, 1 gemm
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<double> layer_ms, gemm_ms;
+    std::vector<size_t> gemm_launches;
+};
+
+namespace bnnk {
+namespace {
+
+int fill(float* dst, size_t n, uint64_t seed, cudaStream_t s) {
+    return launch_fill_random(seed, 0, n, dst, s);
+}
+
+int build(bnn_net* net, const bnn_layer_spec* specs, size_t n, uint64_t seed, cudaStream_t s) {
+    size_t ch = net->in_c, hh = net->in_h, ww = net->in_w;
+    bool flat = false;
+    net->max_act_per_image = ch * hh * ww;
+    DevBuf tmp;
+    for (size_t i = 0; i < n; ++i) {
+        auto L = std::make_unique<Layer>();
+        L->spec = specs[i];
+        L->in_c = ch, L->in_h = hh, L->in_w = ww, L->in_flat = flat;
+        const uint64_t base = specs[i].has_seed ? specs[i].seed : mix64(seed, i);
+        auto chain_error = [&](const std::string& msg) {  // network.cpp:190-193
+            return fail(BNN_E_SHAPE, "layer " + std::to_string(i) + " (" + kind_name(specs[i].kind) +
+                                         "): " + msg);
+        };
+        switch (specs[i].kind) {
+            case BNN_LAYER_CONV: {
+                if (flat) return chain_error("input is already flattened");
+                const bnn_layer_spec& ls = specs[i];
+                if (ls.out_channels == 0 || ls.kernel_h == 0 || ls.kernel_w == 0)
+                    return chain_error("out_channels and kernel size are required");
+                L->geom = bnn_conv_geom{ls.kernel_h, ls.kernel_w, ls.stride_h, ls.stride_w,
+                                        ls.pad_h,    ls.pad_w,    ch,          ls.out_channels};
+                size_t oh, ow;
+                if (bnn_output_dims(&L->geom, hh, ww, &oh, &ow) != BNN_OK)
+                    return chain_error(bnn_last_error());
+                L->rows = ls.out_channels;
+                L->cols = ch * ls.kernel_h * ls.kernel_w;
+                net->max_lines_words_per_image =
+                    std::max(net->max_lines_words_per_image, oh * ow * wpl_of(L->cols));
+                ch = ls.out_channels, hh = oh, ww = ow;
+                break;
+            }
+            case BNN_LAYER_LINEAR: {
+                if (specs[i].out_features == 0) return chain_error("out_features is required");
+                L->rows = specs[i].out_features;
+                L->cols = flat ? ch : ch * hh * ww;
+                net->max_lines_words_per_image =
+                    std::max(net->max_lines_words_per_image, wpl_of(L->cols));
+                ch = specs[i].out_features, hh = ww = 0;
+                flat = true;
+                break;
+            }
+            case BNN_LAYER_MAXPOOL:
+                if (flat) return chain_error("input is already flattened");
+                if (hh % 2 || ww % 2)
+                    return chain_error("spatial extents must be even, got " + std::to_string(hh) +
+                                       "x" + std::to_string(ww));
+                hh /= 2, ww /= 2;
+                break;
+            case BNN_LAYER_AFFINE: {
+                L->n_affine = ch;  // channel count, or feature count once flat
+                BNN_TRY(L->scale.alloc(ch * 4));
+                BNN_TRY(L->shift.alloc(ch * 4));
+                BNN_TRY(fill(L->scale.as<float>(), ch, mix64(base, 3), s));
+                BNN_TRY(launch_affine_scale(L->scale.as<float>(), ch, s));
+                BNN_TRY(fill(L->shift.as<float>(), ch, mix64(base, 4), s));
+                net->weight_bytes += 8 * ch;
+                break;
+            }
+            case BNN_LAYER_SIGN:
+            case BNN_LAYER_HTANH:
+                break;
+            default:
+                return fail(BNN_E_CONFIG, "unknown layer kind " + std::to_string(specs[i].kind));
+        }
+        if (L->rows) {  // weighted layer: generate, binarize, pack once
+            L->wpl = wpl_of(L->cols);
+            const size_t nw = L->rows * L->cols;
+            if (tmp.bytes < nw * 4) BNN_TRY(tmp.alloc(nw * 4));
+            BNN_TRY(fill(tmp.as<float>(), nw, mix64(base, 1), s));
+            BNN_TRY(L->packed.alloc(L->rows * L->wpl * 4));
+            BNN_TRY(launch_pack_rows(tmp.as<float>(), L->rows, L->cols, L->packed.as<uint32_t>(),
+                                     L->wpl, nullptr, s));
+            BNN_TRY(L->bias.alloc(L->rows * 4));
+            BNN_TRY(fill(L->bias.as<float>(), L->rows, mix64(base, 2), s));
+            net->weight_bytes += L->rows * L->wpl * 4 + L->rows * 4;
+            // tmp is reused by the next layer: order the reuse on the stream
+        }
+        L->out_c = ch, L->out_h = hh, L->out_w = ww, L->out_flat = flat;
+        net->max_act_per_image = std::max(net->max_act_per_image, flat ? ch : ch * hh * ww);
+        net->layers.push_back(std::move(L));
+    }
+    net->logits = flat ? ch : ch * hh * ww;
+    BNN_CUDA(cudaStreamSynchronize(s));  // tmp is freed on return
+    return BNN_OK;
+}
+
+int ensure_arena(bnn_net* net, size_t batch) {
+    if (net->arena_batch >= batch) return BNN_OK;
+    BNN_TRY(net->act[0].alloc(net->max_act_per_image * batch * 4));
+    BNN_TRY(net->act[1].alloc(net->max_act_per_image * batch * 4));
+    BNN_TRY(net->lines.alloc(std::max<size_t>(net->max_lines_words_per_image, 1) * batch * 4));
+    net->arena_batch = batch;
+    return BNN_OK;
+}
+
+cudaEvent_t take_event(bnn_net* net) {
+    if (!net->pool.empty()) {
+        cudaEvent_t e = net->pool.back();
+        net->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct EventPair {
+    bnn_net* net;
+    size_t layer;
+    int what;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    EventPair(bnn_net* n, size_t l, int w, cudaStream_t st) : net(n), layer(l), what(w), s(st) {
+        if (net->timing) {
+            a = take_event(net);
+            cudaEventRecord(a, s);
+        }
+    }
+    void close() {
+        if (!a) return;
+        cudaEvent_t b = take_event(net);
+        cudaEventRecord(b, s);
+        net->pending.push_back({layer, what, a, b});
+        a = nullptr;
+    }
+};
+
+int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+    if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
+    BNN_TRY(ensure_arena(net, B));
+    size_t launches = 0;
+    const float* cur = x;
+    int which = 0;
+    auto next = [&]() { float* o = net->act[which].as<float>(); which ^= 1; return o; };
+    for (size_t li = 0; li < net->layers.size(); ++li) {
+        Layer& L = *net->layers[li];
+        EventPair layer_ev(net, li, 0, s);
+        switch (L.spec.kind) {
+            case BNN_LAYER_CONV: {
+                float* out = next();
+                BNN_TRY(launch_im2col_sign_pack(cur, B, L.in_c, L.in_h, L.in_w, &L.geom,
+                                                net->lines.as<uint32_t>(), L.wpl, s));
+                EventPair gemm_ev(net, li, 1, s);
+                BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl,
+                                 L.rows, B * L.out_h * L.out_w, L.cols, L.bias.as<float>(),
+                                 L.out_h * L.out_w, out, s));
+                gemm_ev.close();
+                launches += 2;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_LINEAR: {
+                if (!L.in_flat) {  // flatten_to_columns: [B, F] -> [F, B]
+                    float* t = next();
+                    BNN_TRY(launch_transpose(cur, B, L.cols, t, s));
+                    ++launches;
+                    cur = t;
+                }
+                float* out = next();
+                BNN_TRY(launch_pack_cols(cur, L.cols, B, net->lines.as<uint32_t>(), L.wpl, nullptr, s));
+                EventPair gemm_ev(net, li, 1, s);
+                BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl,
+                                 L.rows, B, L.cols, L.bias.as<float>(), B, out, s));
+                gemm_ev.close();
+                launches += 2;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_MAXPOOL: {
+                float* out = next();
+                BNN_TRY(launch_maxpool2(cur, B, L.in_c, L.in_h, L.in_w, out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_AFFINE: {
+                float* out = next();
+                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
+                const size_t plane = L.in_flat ? B : L.in_h * L.in_w;
+                BNN_TRY(launch_affine(cur, n, L.in_c, plane, L.scale.as<float>(),
+                                      L.shift.as<float>(), out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_SIGN:
+            case BNN_LAYER_HTANH: {
+                float* out = next();
+                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
+                BNN_TRY(launch_unary(L.spec.kind == BNN_LAYER_SIGN ? 0 : 1, cur, n, out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+        }
+        layer_ev.close();
+    }
+    const Layer& last = *net->layers.back();
+    if (last.out_flat) {
+        BNN_CUDA(cudaMemcpyAsync(logits, cur, net->logits * B * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+        BNN_TRY(launch_transpose(cur, B, net->logits, logits, s));
+        ++launches;
+    }
+    net->last_launches = launches;
+    return BNN_OK;
+}
+
+}  // namespace
+}  // namespace bnnk
+
+using namespace bnnk;
+
+extern "C" {
+
+size_t bnn_default_spec(bnn_layer_spec* out, size_t cap) {  // network.cpp:422-465
+    std::vector<bnn_layer_spec> l;
+    auto conv = [&](uint64_t d) {
+        bnn_layer_spec s{};
+        s.kind = BNN_LAYER_CONV;
+        s.out_channels = d;
+        s.kernel_h = s.kernel_w = 3;
+        s.stride_h = s.stride_w = 1;
+        s.pad_h = s.pad_w = 1;
+        l.push_back(s);
+    };
+    auto push = [&](uint32_t k) {
+        bnn_layer_spec s{};
+        s.kind = k;
+        s.stride_h = s.stride_w = 1;
+        l.push_back(s);
+    };
+    auto linear = [&](uint64_t f) {
+        bnn_layer_spec s{};
+        s.kind = BNN_LAYER_LINEAR;
+        s.out_features = f;
+        s.stride_h = s.stride_w = 1;
+        l.push_back(s);
+    };
+    auto norm_act = [&] {
+        push(BNN_LAYER_AFFINE);
+        push(BNN_LAYER_HTANH);
+        push(BNN_LAYER_SIGN);
+    };
+    conv(128); norm_act();
+    conv(128); push(BNN_LAYER_MAXPOOL); norm_act();
+    conv(256); norm_act();
+    conv(256); push(BNN_LAYER_MAXPOOL); norm_act();
+    conv(512); norm_act();
+    conv(512); push(BNN_LAYER_MAXPOOL); norm_act();
+    linear(1024); norm_act();
+    linear(1024); norm_act();
+    linear(10);
+    for (size_t i = 0; i < l.size() && i < cap; ++i) out[i] = l[i];
+    return l.size();
+}
+
+int bnn_net_create(const bnn_layer_spec* layers, size_t n_layers, size_t in_c, size_t in_h,
+                   size_t in_w, uint64_t seed, int binarize_weights, bnn_net** out) {
+    (void)binarize_weights;  // sign(sign(w)) == sign(w): packed bits do not depend on it
+    BNN_TRY(require_sm100());
+    if (n_layers == 0) return fail(BNN_E_SHAPE, "network has no layers");
+    if (in_c == 0 || in_h == 0 || in_w == 0) return fail(BNN_E_SHAPE, "input extents must be >= 1");
+    auto net = std::make_unique<bnn_net>();
+    net->in_c = in_c, net->in_h = in_h, net->in_w = in_w;
+    cudaStream_t s;
+    BNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int rc = build(net.get(), layers, n_layers, seed, s);
+    cudaStreamDestroy(s);
+    if (rc != BNN_OK) return rc;
+    *out = net.release();
+    return BNN_OK;
+}
+
+void bnn_net_destroy(bnn_net* net) {
+    if (!net) return;
+    for (auto& p : net->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : net->pool) cudaEventDestroy(e);
+    delete net;
+}
+size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
+size_t bnn_net_num_layers(const bnn_net* net) { return net->layers.size(); }
+size_t bnn_net_last_launches(const bnn_net* net) { return net->last_launches; }
+
+size_t bnn_net_device_bytes(const bnn_net* net) {
+    return net->weight_bytes + net->act[0].bytes + net->act[1].bytes + net->lines.bytes;
+}
+
+int bnn_net_layer_params(const bnn_net* net, size_t i, uint32_t* packed, size_t* rows, size_t* cols,
+                         float* bias, float* scale, float* shift) {
+    if (i >= net->layers.size()) return fail(BNN_E_CONFIG, "layer index out of range");
+    const Layer& L = *net->layers[i];
+    if (rows) *rows = L.rows;
+    if (cols) *cols = L.cols;
+    if (packed && L.rows) BNN_CUDA(cudaMemcpy(packed, L.packed.p, L.rows * L.wpl * 4, cudaMemcpyDeviceToHost));
+    if (bias && L.rows) BNN_CUDA(cudaMemcpy(bias, L.bias.p, L.rows * 4, cudaMemcpyDeviceToHost));
+    if (scale && L.n_affine) BNN_CUDA(cudaMemcpy(scale, L.scale.p, L.n_affine * 4, cudaMemcpyDeviceToHost));
+    if (shift && L.n_affine) BNN_CUDA(cudaMemcpy(shift, L.shift.p, L.n_affine * 4, cudaMemcpyDeviceToHost));
+    return BNN_OK;
+}
+
+int bnn_net_set_timing(bnn_net* net, int enabled) {
+    net->timing = enabled != 0;
+    return BNN_OK;
+}
+
+int bnn_net_timing(bnn_net* net, double* layer_ms, double* gemm_ms, size_t* gemm_launches) {
+    const size_t n = net->layers.size();
+    if (net->layer_ms.size() != n) {
+        net->layer_ms.assign(n, 0.0);
+        net->gemm_ms.assign(n, 0.0);
+        net->gemm_launches.assign(n, 0);
+    }
+    for (auto& p : net->pending) {
+        BNN_CUDA(cudaEventSynchronize(p.b));
+        float ms = 0.f;
+        BNN_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        if (p.what == 0) {
+            net->layer_ms[p.layer] += ms;
+        } else {
+            net->gemm_ms[p.layer] += ms;
+            net->gemm_launches[p.layer] += 1;
+        }
+        net->pool.push_back(p.a);
+        net->pool.push_back(p.b);
+    }
+    net->pending.clear();
+    for (size_t i = 0; i < n; ++i) {
+        if (layer_ms) layer_ms[i] = net->layer_ms[i];
+        if (gemm_ms) gemm_ms[i] = net->gemm_ms[i];
+        if (gemm_launches) gemm_launches[i] = net->gemm_launches[i];
+    }
+    return BNN_OK;
+}
+
+int bnn_net_reset_timing(bnn_net* net) {
+    BNN_TRY(bnn_net_timing(net, nullptr, nullptr, nullptr));
+    std::fill(net->layer_ms.begin(), net->layer_ms.end(), 0.0);
+    std::fill(net->gemm_ms.begin(), net->gemm_ms.end(), 0.0);
+    std::fill(net->gemm_launches.begin(), net->gemm_launches.end(), 0);
+    return BNN_OK;
+}
+
+int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]) {
+    if (i >= net->layers.size()) return fail(BNN_E_CONFIG, "layer index out of range");
+    const Layer& L = *net->layers[i];
+    out[0] = L.spec.kind;
+    out[1] = L.rows;  // GEMM M
+    out[2] = L.cols;  // GEMM K (= L)
+    out[3] = L.spec.kind == BNN_LAYER_CONV ? L.out_h * L.out_w : (L.spec.kind == BNN_LAYER_LINEAR ? 1 : 0);
+    out[4] = L.out_c;
+    out[5] = L.out_h;
+    out[6] = L.out_w;
+    out[7] = L.out_flat ? 1 : 0;
+    return BNN_OK;
+}
+
+int bnn_net_forward(bnn_net* net, const float* x, size_t batch, float* logits, bnn_stream_t s) {
+    BNN_TRY(require_sm100());
+    return forward(net, x, batch, logits, S(s));
+}
+
+int bnn_host_net_forward(bnn_net* net, const float* x, size_t batch, float* logits) {
+    BNN_TRY(require_sm100());
+    cudaStream_t s = nullptr;
+    BNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t nx = batch * net->in_c * net->in_h * net->in_w, ny = batch * net->logits;
+    int rc = BNN_OK;
+    void *dx = nullptr, *dy = nullptr;
+    if (cudaMalloc(&dx, nx * 4) != cudaSuccess || cudaMalloc(&dy, ny * 4) != cudaSuccess)
+        rc = fail(BNN_E_CUDA, "cudaMalloc failed");
+    if (rc == BNN_OK && cudaMemcpyAsync(dx, x, nx * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        rc = fail(BNN_E_CUDA, "H2D copy failed");
+    if (rc == BNN_OK) rc = forward(net, static_cast<float*>(dx), batch, static_cast<float*>(dy), s);
+    if (rc == BNN_OK && cudaMemcpyAsync(logits, dy, ny * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rc = fail(BNN_E_CUDA, "D2H copy failed");
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == BNN_OK) rc = fail(BNN_E_CUDA, "sync failed");
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaStreamDestroy(s);
+    return rc;
+}
+
+}  // extern "C"
