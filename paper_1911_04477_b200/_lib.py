@@ -67,6 +67,7 @@ _SIGS = {
     "bnn_last_error": (C.c_char_p, []),
     "bnn_version": (_I, []),
     "bnn_last_gemm_kernel": (C.c_char_p, []),
+    "bnn_set_gemm_policy": (_I, [_I]),
     "bnn_words_per_line": (_SZ, [_SZ]),
     "bnn_output_dims": (_I, [_P, _SZ, _SZ, C.POINTER(_SZ), C.POINTER(_SZ)]),
     "bnn_sign_pack_cols_f32": (_I, [_P, _SZ, _SZ, _P, _SZ, _P]),

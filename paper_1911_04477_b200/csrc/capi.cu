@@ -78,11 +78,47 @@ int launch_pack_rows(const float*, size_t, size_t, uint32_t*, size_t, unsigned l
 int launch_im2col_sign_pack(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*,
                             uint32_t*, size_t, cudaStream_t);
 
+int launch_unpack_s8(const uint32_t*, size_t, size_t, size_t, int8_t*, size_t, cudaStream_t);
+int umma_gemm_s32(const int8_t*, size_t, const int8_t*, size_t, size_t, size_t, size_t, int32_t*,
+                  size_t, cudaStream_t);
+int umma_gemm_f32(const int8_t*, size_t, const int8_t*, size_t, size_t, size_t, size_t, const float*,
+                  size_t, float*, cudaStream_t);
+
+namespace {
+int g_policy = BNN_GEMM_AUTO;
+
+// Size rule: the tensor-core path pays an unpack pass
+// (1 bit -> 1 byte per operand element) and a ~4-6 us launch floor; below ~2^27 bit-MACs the
+// single-launch integer-pipe kernel finishes first.
+bool use_umma(size_t M, size_t N, size_t L) {
+    if (g_policy == BNN_GEMM_POPC) return false;
+    if (g_policy == BNN_GEMM_UMMA) return true;
+    return double(M) * double(N) * double(L) >= double(1u << 27);
+}
+
+// Unpack both packed operands to int8 rows (stride round_up(L, 32)) in stream-ordered scratch.
+int unpack_operands(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N,
+                    size_t L, Scratch& sw, Scratch& sx, size_t& ldk, cudaStream_t s) {
+    ldk = (L + 31) / 32 * 32;
+    BNN_TRY(sw.alloc(M * ldk, s));
+    BNN_TRY(sx.alloc(N * ldk, s));
+    BNN_TRY(launch_unpack_s8(w, ldw, M, L, sw.as<int8_t>(), ldk, s));
+    BNN_TRY(launch_unpack_s8(x, ldx, N, L, sx.as<int8_t>(), ldk, s));
+    return BNN_OK;
+}
+}  // namespace
+
 // GEMM dispatch (device pointers). Kept in one place so every caller (C ABI, layer
 // forwards, network engine) takes the same kernel for the same shape.
 int gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N,
              size_t L, int32_t* out, size_t ldo, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
+    if (use_umma(M, N, L)) {
+        Scratch sw, sx;
+        size_t ldk;
+        BNN_TRY(unpack_operands(w, ldw, x, ldx, M, N, L, sw, sx, ldk, s));
+        return umma_gemm_s32(sw.as<int8_t>(), ldk, sx.as<int8_t>(), ldk, M, N, ldk, out, ldo, s);
+    }
     return popc_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
 }
 
@@ -90,8 +126,16 @@ int gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_
              size_t L, const float* bias, size_t P, float* out, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
     if (P == 0 || N % P != 0) return fail(BNN_E_SHAPE, "xnor_gemm: N must be a multiple of P");
+    if (use_umma(M, N, L)) {
+        Scratch sw, sx;
+        size_t ldk;
+        BNN_TRY(unpack_operands(w, ldw, x, ldx, M, N, L, sw, sx, ldk, s));
+        return umma_gemm_f32(sw.as<int8_t>(), ldk, sx.as<int8_t>(), ldk, M, N, ldk, bias, P, out, s);
+    }
     return popc_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
 }
+
+int gemm_policy() { return g_policy; }
 
 int conv_forward(const float* x, size_t B, size_t C, size_t H, size_t W, const uint32_t* pw,
                  size_t ldw, const float* bias, const bnn_conv_geom* g, float* out, cudaStream_t s) {
@@ -133,6 +177,12 @@ extern "C" {
 const char* bnn_last_error(void) { return g_err.c_str(); }
 int bnn_version(void) { return 1; }
 const char* bnn_last_gemm_kernel(void) { return g_last_gemm; }
+
+int bnn_set_gemm_policy(int policy) {
+    if (policy < BNN_GEMM_AUTO || policy > BNN_GEMM_UMMA) return fail(BNN_E_CONFIG, "bad GEMM policy");
+    g_policy = policy;
+    return BNN_OK;
+}
 
 size_t bnn_words_per_line(size_t extent) { return wpl_of(extent); }
 

@@ -333,3 +333,57 @@ def test_network_device_path_and_deterministic(bnn, orc):
     assert np.array_equal(a, b)
     assert np.array_equal(a, net.forward(x))
     assert net.last_launches() > 0
+
+
+# ------------------------------------------------------- both K3 kernels, forced
+
+
+@pytest.fixture
+def policy(bnn):
+    lib = bnn.load()
+    yield lambda p: lib.bnn_set_gemm_policy({"auto": 0, "popc": 1, "umma": 2}[p])
+    lib.bnn_set_gemm_policy(0)
+
+
+@pytest.mark.parametrize("kernel", ["popc", "umma"])
+@pytest.mark.parametrize("m,n,L", [(1, 1, 1), (3, 4, 31), (16, 16, 33), (128, 256, 128), (130, 70, 9216),
+                                   (257, 513, 1000), (1024, 1024, 1024), (64, 1024, 576),
+                                   (1000, 300, 4096), (5, 3000, 200)])
+def test_gemm_kernels_vs_oracle(bnn, orc, policy, kernel, m, n, L):
+    policy(kernel)
+    w = orc.pack(orc.fill_random((m, L), m + 7), "rows", True)
+    x = orc.pack(orc.fill_random((L, n), n + 9), "cols", True)
+    got = bnn.xnor_gemm(bnn.PackedBitMatrix(m, L, "rows", w), bnn.PackedBitMatrix(L, n, "cols", x), L)
+    assert bnn.load().bnn_last_gemm_kernel().decode() == ("popc" if kernel == "popc" else "umma_i8")
+    assert np.array_equal(got, orc.xnor_gemm(w, x, L))
+
+
+@pytest.mark.parametrize("kernel", ["popc", "umma"])
+def test_gemm_kernels_golden_and_layers(bnn, orc, golden, policy, kernel):
+    policy(kernel)
+    arrays, meta = golden
+    for i, (m, n, L) in enumerate(meta["cases"]["gemm"]):
+        w = bnn.PackedBitMatrix(m, L, "rows", arrays[f"gemm{i}_w"])
+        x = bnn.PackedBitMatrix(L, n, "cols", arrays[f"gemm{i}_x"])
+        assert np.array_equal(bnn.xnor_gemm(w, x, L), arrays[f"gemm{i}_out"]), (m, n, L)
+    for i, c in enumerate(meta["cases"]["conv"]):
+        xs, ws, bs = c["seeds"]
+        g = c["geom"]
+        x = orc.fill_random(tuple(c["shape"]), xs)
+        pw = bnn.sign_pack_rows(orc.fill_random((g[7], g[0] * g[1] * g[6]), ws))
+        y = bnn.conv_forward_binary(x, pw, orc.fill_random((g[7],), bs), g)
+        assert orc.fnv1a(y) == c["fnv1a"], (kernel, c)
+    for c in meta["cases"]["linear"]:
+        xs, ws, bs = c["seeds"]
+        x = orc.fill_random((c["K"], c["N"]), xs)
+        pw = bnn.sign_pack_rows(orc.fill_random((c["M"], c["K"]), ws))
+        y = bnn.linear_forward_packed(x, pw, orc.fill_random((c["M"],), bs))
+        assert orc.fnv1a(y) == c["fnv1a"], (kernel, c)
+
+
+@pytest.mark.parametrize("kernel", ["popc", "umma"])
+def test_network_both_kernels(bnn, orc, policy, kernel):
+    policy(kernel)
+    net = bnn.Network(seed=1)
+    x = orc.fill_random((8, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
+    assert np.array_equal(net.forward(x), orc.net(seed=1).forward(x))
