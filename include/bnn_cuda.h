@@ -188,6 +188,15 @@ int bnn_net_reset_timing(bnn_net* net);
 /* Layer i: out[0] kind, [1] GEMM M (rows of packed weights), [2] GEMM K, [3] GEMM columns per
  * image (oh*ow for conv, 1 for linear, 0 otherwise), [4..6] output C, H, W, [7] output flat. */
 int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]);
+/* Engine selection. FUSED (fused.cu): one tcgen05 launch per weighted layer with the glue
+ * (bias, maxpool, affine_norm, htanh, sign) folded into its epilogue and packed-bit NHWC
+ * activations; available when the topology matches conv {[maxpool][affine][htanh][sign]
+ * conv|linear}* linear (the default network does). GENERIC: one kernel per reference op.
+ * AUTO (default) = FUSED when available. Both are bit-exact with the reference. */
+enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2 };
+int bnn_net_set_engine(bnn_net* net, int policy);
+/* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
+int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */
 size_t bnn_net_last_launches(const bnn_net* net);
 /* Bytes of device memory held by the engine (weights + activation arena). */

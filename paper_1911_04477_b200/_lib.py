@@ -96,6 +96,8 @@ _SIGS = {
     "bnn_net_layer_params": (_I, [_P, _SZ, _P, C.POINTER(_SZ), C.POINTER(_SZ), _P, _P, _P]),
     "bnn_net_forward": (_I, [_P, _P, _SZ, _P, _P]),
     "bnn_net_last_launches": (_SZ, [_P]),
+    "bnn_net_set_engine": (_I, [_P, _I]),
+    "bnn_net_engine": (_I, [_P]),
     "bnn_net_set_timing": (_I, [_P, _I]),
     "bnn_net_timing": (_I, [_P, _P, _P, _P]),
     "bnn_net_reset_timing": (_I, [_P]),

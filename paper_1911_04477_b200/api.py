@@ -476,6 +476,18 @@ class Network:
         check(load().bnn_net_forward(self._h, x.data_ptr(), B, out.data_ptr(), st))
         return out
 
+    ENGINES = {"auto": 0, "generic": 1, "fused": 2}
+
+    def set_engine(self, name: str) -> None:
+        """Select the device engine: "fused" (one tcgen05 launch per weighted layer, packed-bit
+        activations), "generic" (one kernel per reference op) or "auto" (fused when the topology
+        allows it). Both are bit-exact with the reference."""
+        check(load().bnn_net_set_engine(self._h, self.ENGINES[name]))
+
+    @property
+    def engine(self) -> str:
+        return {1: "generic", 2: "fused"}[int(load().bnn_net_engine(self._h))]
+
     def last_launches(self) -> int:
         return int(load().bnn_net_last_launches(self._h))
 

@@ -1,0 +1,663 @@
+// Fused binary layer on the 5th-generation tensor cores: implicit-GEMM binary conv / linear
+// with the inter-layer glue folded into the epilogue.
+//
+// One launch computes, for every output position of a conv (or every image of a linear
+// layer), what the reference computes as
+//
+//   conv_forward_binary / linear_forward_packed   (network.cpp:65-79, 121-126)
+//     = xnor_gemm(pack_rows(sign W), pack_cols(sign im2col(x)))  -> to_float -> bias_add
+//   [maxpool2]                                     (network.cpp:133-149)
+//   affine_norm   fmaf(scale, y, shift)            (network.cpp:151-175, FMA-contracted)
+//   htanh, sign                                    (binarize.cpp:24-37)
+//
+// and writes the result directly as the NEXT layer's packed input bits. Why this is exact:
+//   * the xnor-popcount value L - 2*popc(w ^ x) is the integer dot product of the +-1
+//     vectors, so it is computed as an int8 x int8 -> int32 tcgen05.mma (kind::i8) of the
+//     +-1 bytes; every accumulator is the reference's exact integer.
+//   * the reduction order of K is free for an exact integer sum, so weights and activations
+//     use the engine's K order (tap-major, channel-minor) instead of im2col's c-major order;
+//     the weights are permuted once at build time (prep kernel below).
+//   * float(acc) + bias is monotone in acc, so maxpool of the four floats equals the float of
+//     the max integer: the 2x2 max is taken on the accumulators.
+//   * sign(htanh(z)) = sign(z) = (z >= 0) for every z (htanh keeps the sign, -0.0 >= 0).
+//   * spatial zero padding reads as 0.0 in the reference's im2col and sign(0.0) = +1, so an
+//     out-of-image activation word is 0xFFFFFFFF.
+//
+// Data layout (HBM): activations between fused layers are packed bits, NHWC:
+// act[((b*H + y)*W + x)*Cw + w], bit j of word w = channel 32w + j (1 = +1). Conv layers
+// whose output is max-pooled enumerate their output rows pool-major
+// (row = ((b*OH/2 + py)*OW/2 + px)*4 + sub), so a pooling window is four adjacent TMEM
+// lanes and the pooled row index is row/4, the NHWC order of the pooled tensor.
+//
+// Kernel anatomy (persistent, one CTA per SM, 320 threads):
+//   warp 0      TMA producer of the weight tile B (int8 +-1, [Dpad, Kpad], K-major,
+//               SWIZZLE_128B), BN rows x 128 K-bytes per stage
+//   warp 1      TMEM allocator + single-thread UMMA issuer, M=128 x N=BN x K=32 per
+//               instruction, 4 per stage
+//   warps 2-5   epilogue: tcgen05.ld -> (2x2 max) -> +bias -> fma(scale, ., shift) -> >= 0
+//               -> 32-channel words -> vector stores; or float logits / NCHW floats
+//   warps 6-9   activation producers: one tile row (output position) per thread; read 4
+//               packed words per stage (one 16-byte load), expand bit -> +-1 byte and store
+//               them in the SWIZZLE_128B K-major layout the UMMA descriptor expects.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "bnn_common.cuh"
+#include "fused.cuh"
+#include "umma.cuh"
+
+namespace bnnk {
+
+using namespace umma;
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kThreads = 320;
+constexpr int kRows = 128;   // UMMA M
+constexpr int kKB = 128;     // K bytes per stage
+
+constexpr int kMaxF32K = 1024;  // float-input layers: K <= this (im2col offset table in smem)
+constexpr int kMaxQ = 1024;     // K words per layer (bits mode), entries of the offset table
+constexpr int kMaxPixTaps = 16; // pixel-packed first layer: taps (and taps*C <= 64)
+
+template <int BN>
+constexpr size_t fused_smem() {
+    static_assert(kMaxF32K <= kMaxQ, "one table region");
+    return 1024 + size_t(kStages) * (kRows + BN) * kKB + 256 + kMaxQ * 8;
+}
+
+__device__ __forceinline__ bool decode_row(const FusedGeom& g, int row, int& b, int& oy, int& ox) {
+    if (row >= g.rows) return false;
+    if (g.pool) {
+        const int s = row & 3, win = row >> 2;
+        const int pw = g.OW >> 1, ph = g.OH >> 1;
+        const int px = win % pw, t = win / pw;
+        const int py = t % ph;
+        b = t / ph;
+        oy = 2 * py + (s >> 1);
+        ox = 2 * px + (s & 1);
+    } else {
+        const int P = g.OH * g.OW;
+        b = row / P;
+        const int p = row - b * P;
+        oy = p / g.OW;
+        ox = p - oy * g.OW;
+    }
+    return true;
+}
+
+// Store one 16-byte chunk of row r at its SWIZZLE_128B position (chunk ^ (r % 8)).
+__device__ __forceinline__ void put_chunk(uint32_t tile, int r, int chunk, uint32_t a, uint32_t b, uint32_t c,
+                                          uint32_t d) {
+    st_shared_v4(tile + uint32_t(r) * 128u + (uint32_t(chunk ^ (r & 7)) << 4), a, b, c, d);
+}
+
+// One packed word (32 K positions) -> 32 operand bytes in {0, 1} (the bit itself; see the
+// u8 encoding note at fused_prep_weights). Byte j of output word s is bit 8j + s, so each
+// output word is one shift + one AND: 15 ALU ops for 32 bytes. The weights use the same
+// within-word order.
+__device__ __forceinline__ void put_word(uint32_t tile, int r, int i, uint32_t w) {
+    constexpr uint32_t m = 0x01010101u;
+    put_chunk(tile, r, 2 * i, w & m, (w >> 1) & m, (w >> 2) & m, (w >> 3) & m);
+    put_chunk(tile, r, 2 * i + 1, (w >> 4) & m, (w >> 5) & m, (w >> 6) & m, (w >> 7) & m);
+}
+
+// Per-row state of the activation producer for the current tile.
+struct RowCtx {
+    bool valid;
+    int pix;  // b*H (bits/pixel modes)
+    int y0, x0;  // oy*SH, ox*SW
+};
+
+// The 4 packed words (one 128-position K block) of one row. qtab[q] = {dy<<16 | dx&0xffff,
+// cw} for K word q (cw < 0: K padding). One 16-byte load when the block is one tap of
+// contiguous channels (Cw % 4 == 0), else word by word.
+__device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab, const RowCtx& rc, int kb) {
+    const uint32_t* act = static_cast<const uint32_t*>(g.in);
+    if (!rc.valid) return make_uint4(0, 0, 0, 0);
+    if ((g.Cw & 3) == 0) {
+        const int2 e = qtab[4 * kb];
+        const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
+        if (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
+            return __ldg(reinterpret_cast<const uint4*>(act + (size_t((rc.pix + iy) * g.W + ix)) * g.Cw + e.y));
+        return make_uint4(~0u, ~0u, ~0u, ~0u);  // spatial padding: sign(0.0) = +1
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int2 e = qtab[4 * kb + i];
+        const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
+        w[i] = e.y < 0 ? 0u  // K padding: 0 bytes, and the weights are 0 there too
+               : (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
+                   ? __ldg(act + size_t((rc.pix + iy) * g.W + ix) * g.Cw + e.y)
+                   : ~0u;
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Pixel-packed first layer (FIN_PIX): in[(b*H + y)*W + x] holds the C <= 32 sign bits of one
+// input pixel (pack_pixels_kernel). The row's K = T*C bits are gathered tap by tap,
+// tap-major / channel-minor (K <= 64: one K block). qtab[tap] = {dy<<16 | dx&0xffff, 0}.
+__device__ __forceinline__ uint4 load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
+    const uint32_t* pix = static_cast<const uint32_t*>(g.in);
+    if (!rc.valid) return make_uint4(0, 0, 0, 0);
+    const int T = g.KH * g.KW;
+    const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int tap = 0; tap < kMaxPixTaps; ++tap) {
+        if (tap < T) {
+            const int2 e = qtab[tap];
+            const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
+            const uint32_t v = (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
+                                   ? __ldg(pix + size_t(rc.pix + iy) * g.W + ix)
+                                   : cmask;  // padding: every channel +1
+            acc |= uint64_t(v) << (tap * g.C);
+        }
+    }
+    return make_uint4(uint32_t(acc), uint32_t(acc >> 32), 0u, 0u);
+}
+
+__device__ __forceinline__ void store_bits(uint32_t tile, int r, uint4 u) {
+    put_word(tile, r, 0, u.x);
+    put_word(tile, r, 1, u.y);
+    put_word(tile, r, 2, u.z);
+    put_word(tile, r, 3, u.w);
+}
+
+// One K block of one row, float NCHW input, reference im2col order r = (c*KH + ky)*KW + kx;
+// bytes in natural order, value (x >= 0) (binarize.cpp:9). tab[k] = {c*H*W + ky*W + kx, ky<<16|kx}.
+__device__ __forceinline__ void produce_f32(const FusedGeom& g, const int2* tab, uint32_t tile, int r,
+                                            bool valid, int b, int oy, int ox, int kb) {
+    const float* x = static_cast<const float*>(g.in) + size_t(b) * g.C * g.H * g.W;
+    const int y0 = oy * g.SH - g.PH, x0 = ox * g.SW - g.PW;
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+        const int k0 = kb * kKB + j * 16;
+        uint32_t u[4] = {0, 0, 0, 0};
+        if (valid && k0 < g.K) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int k = k0 + e;
+                if (k < g.K) {
+                    const int2 t = tab[k];
+                    const int iy = y0 + (t.y >> 16), ix = x0 + (t.y & 0xffff);
+                    float v = 0.0f;
+                    if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W) v = __ldg(x + t.x + y0 * g.W + x0);
+                    u[e >> 2] |= uint32_t(v >= 0.0f) << (8 * (e & 3));
+                }
+            }
+        }
+        put_chunk(tile, r, j, u[0], u[1], u[2], u[3]);
+    }
+}
+
+// Profiling aid (FusedGeom::dbg, set by BNN_FUSED_PROFILE=1): cycles each role spends
+// blocked on its barriers, accumulated over CTAs. Slots: [role*4 + 0/1] waits, [role*4 + 3]
+// total cycles; roles 0 TMA, 1 MMA, 2 epilogue, 3 producer.
+__device__ __forceinline__ long long dclock() {
+#ifdef __CUDA_ARCH__
+    return clock64();
+#else
+    return 0;
+#endif
+}
+
+struct WaitClock {
+    long long w[2];
+    long long t_start;
+    __device__ __forceinline__ WaitClock() : w{0, 0}, t_start(dclock()) {}
+    __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int slot) {
+        const long long t0 = dclock();
+        mbar_wait(bar, parity);
+        w[slot] += dclock() - t0;
+    }
+    __device__ __forceinline__ void flush(unsigned long long* dbg, int role) {
+        if (!dbg) return;
+        atomicAdd(dbg + role * 4 + 0, (unsigned long long)w[0]);
+        atomicAdd(dbg + role * 4 + 1, (unsigned long long)w[1]);
+        atomicAdd(dbg + role * 4 + 3, (unsigned long long)(dclock() - t_start));
+    }
+};
+
+template <int BN, int IN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_layer_kernel(const __grid_constant__ CUtensorMap tmW, const FusedGeom g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw);
+    uint8_t* sA = smem;                                   // [kStages][128 * 128]
+    uint8_t* sB = smem + size_t(kStages) * kRows * kKB;   // [kStages][BN * 128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kStages) * BN * kKB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int2* ftab = reinterpret_cast<int2*>(bars + 32);      // offset table [kMaxQ]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tiles = (g.rows + kRows - 1) / kRows;
+    const int n_tiles = g.n_tiles;
+    const int tiles = m_tiles * n_tiles;
+    const int KB = g.KB;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmW);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], kRows + 1);  // 128 producer threads + the TMA expect_tx arrive
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (IN == FIN_F32) {  // im2col offset table: k -> (c*H*W + ky*W + kx, ky, kx)
+        const int khw = g.KH * g.KW;
+        for (int k = threadIdx.x; k < g.K; k += blockDim.x) {
+            const int c = k / khw, t = k - c * khw, ky = t / g.KW, kx = t - ky * g.KW;
+            ftab[k] = make_int2(c * g.H * g.W + ky * g.W + kx, (ky << 16) | kx);
+        }
+    } else if (IN == FIN_BITS) {  // K word q -> (tap offset, channel word); all divisions here
+        const int kw_total = g.K >> 5;
+        for (int q = threadIdx.x; q < 4 * KB; q += blockDim.x) {
+            int2 e = make_int2(0, -1);
+            if (q < kw_total) {
+                const int tap = q / g.Cw, cw = q - tap * g.Cw, ky = tap / g.KW, kx = tap - ky * g.KW;
+                e = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), cw);
+            }
+            ftab[q] = e;
+        }
+    } else {  // FIN_PIX: tap -> offset
+        for (int tap = threadIdx.x; tap < g.KH * g.KW; tap += blockDim.x) {
+            const int ky = tap / g.KW, kx = tap - ky * g.KW;
+            ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
+        }
+    }
+    if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // -------------------------------------------------------------- weight TMA
+        if (lane == 0) {
+            WaitClock wc;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int nt = t % n_tiles;
+                for (int kb = 0; kb < KB; ++kb) {
+                    wc.wait(&empty[stage], phase ^ 1, 0);
+                    mbar_arrive_expect_tx(&full[stage], BN * kKB);
+                    tma_load_2d(&tmW, &full[stage], sB + size_t(stage) * BN * kKB, kb * kKB, nt * BN);
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+            wc.flush(g.dbg, 0);
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------------- UMMA issuer
+        constexpr uint32_t idesc = idesc_i8(kRows, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        WaitClock wc;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            wc.wait(&tempty[acc], acc_phase ^ 1, 0);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+            for (int kb = 0; kb < KB; ++kb) {
+                wc.wait(&full[stage], phase, 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sA + size_t(stage) * kRows * kKB);
+                    const uint32_t b0 = smem_u32(sB + size_t(stage) * BN * kKB);
+#pragma unroll
+                    for (int k = 0; k < kKB / 32; ++k)
+                        mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                               (kb | k) != 0);
+                    mma_commit(&empty[stage]);
+                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == kStages) stage = 0, phase ^= 1;
+            }
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+        if (lane == 0) wc.flush(g.dbg, 1);
+    } else if (warp < 6) {
+        // -------------------------------------------------------------- epilogue
+        // Accumulator u = sum_k bit_k * w_k (bits in {0,1}, weights +-1); the reference's
+        // xnor-popcount value is a = 2u - S_d with S_d = sum_k w_k (prm.z).
+        const int q = warp & 3;  // TMEM lane quarter of this warp
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        WaitClock wc;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int mt = t / n_tiles, nt = t % n_tiles;
+            const int row = mt * kRows + r;
+            const int n0 = nt * BN;
+            const bool valid = row < g.rows;
+            wc.wait(&tfull[acc], acc_phase, 0);
+            tc_fence_after();
+            uint32_t words[BN / 32];
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), v);
+                const int4 pl = __ldg(g.prm + n0 + c * 32 + lane);  // this lane's channel
+                tmem_ld_wait();
+                if (g.dbg_mode & 2) {
+                    words[0] = v[0];
+                } else if (EPI == FEPI_BITS) {
+                    // bit = (u >= Tu) ^ flip: the exact float predicate of the reference
+                    // (fma(scale, float(a) + bias, shift) >= 0), monotone in a, tabulated at
+                    // build time (prep_params_kernel). Pooling: the predicate of the max is the
+                    // OR of the (u >= Tu) terms, so the 2x2 max is a word OR over 4 lanes.
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int tu = __shfl_sync(0xffffffffu, pl.x, j);
+                        w |= uint32_t(int(v[j]) >= tu) << j;
+                    }
+                    if (g.pool) {
+                        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                    }
+                    w ^= __ballot_sync(0xffffffffu, pl.y != 0);
+#pragma unroll
+                    for (int cc = 0; cc < BN / 32; ++cc)  // static register index
+                        if (cc == c) words[cc] = w;
+                } else {
+                    // to_float(a) + bias (kernels.cpp:90-107): one rounding of an exact integer
+                    const int P = g.OH * g.OW;
+                    const int b = valid ? row / P : 0, p = row - b * P;
+#pragma unroll 4
+                    for (int j = 0; j < 32; ++j) {
+                        const int d = n0 + c * 32 + j;
+                        const int sd = __shfl_sync(0xffffffffu, pl.z, j);
+                        const float bias = __int_as_float(__shfl_sync(0xffffffffu, pl.w, j));
+                        const float y = __fadd_rn(__int2float_rn(2 * int(v[j]) - sd), bias);
+                        if (valid && d < g.D) {
+                            if (EPI == FEPI_LOGITS)
+                                g.out_f32[size_t(d) * g.ldo + row] = y;
+                            else
+                                g.out_f32[(size_t(b) * g.D + d) * P + p] = y;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM buffer free before the stores drain
+            if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
+                const int orow = g.pool ? (row >> 2) : row;
+                uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
+                if ((BN / 32) % 4 == 0 && (g.Dw & 3) == 0) {
+#pragma unroll
+                    for (int c = 0; c < BN / 32; c += 4)
+                        *reinterpret_cast<uint4*>(dst + c) =
+                            make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BN / 32; ++c)
+                        if (n0 + 32 * c < g.D) dst[c] = words[c];
+                }
+            }
+            if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+        if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
+    } else {
+        // -------------------------------------------------------------- activation producers
+        const int r = threadIdx.x - 6 * 32;  // tile row 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        WaitClock wc;
+        if (IN != FIN_F32) {
+            // flattened (tile, kb) stream with the global loads issued kPF blocks ahead, so
+            // the L2 latency overlaps the expansion of the blocks in between
+            constexpr int kPF = 3;
+            int t_ld = blockIdx.x, kb_ld = 0;  // next block to load
+            RowCtx rc;
+            auto set_row = [&]() {
+                int b = 0, oy = 0, ox = 0;
+                rc.valid = t_ld < tiles && decode_row(g, (t_ld / n_tiles) * kRows + r, b, oy, ox);
+                rc.pix = b * g.H, rc.y0 = oy * g.SH, rc.x0 = ox * g.SW;
+            };
+            set_row();
+            uint4 pf[kPF];
+            auto next_load = [&]() -> uint4 {
+                uint4 u = make_uint4(0, 0, 0, 0);
+                if (t_ld < tiles) {
+                    u = IN == FIN_BITS ? load_bits(g, ftab, rc, kb_ld) : load_pix(g, ftab, rc);
+                    if (++kb_ld == KB) {
+                        kb_ld = 0;
+                        t_ld += gridDim.x;
+                        set_row();
+                    }
+                }
+                return u;
+            };
+#pragma unroll
+            for (int i = 0; i < kPF; ++i) pf[i] = next_load();
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                for (int kb = 0; kb < KB; ++kb) {
+                    const uint4 u = pf[0];
+#pragma unroll
+                    for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1];
+                    pf[kPF - 1] = next_load();
+                    wc.wait(&empty[stage], phase ^ 1, 0);
+                    if (!(g.dbg_mode & 1)) store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
+                    fence_proxy_async_smem();
+                    mbar_arrive(&full[stage]);
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+        } else {
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int b = 0, oy = 0, ox = 0;
+                const bool valid = decode_row(g, (t / n_tiles) * kRows + r, b, oy, ox);
+                for (int kb = 0; kb < KB; ++kb) {
+                    wc.wait(&empty[stage], phase ^ 1, 0);
+                    produce_f32(g, ftab, smem_u32(sA + size_t(stage) * kRows * kKB), r, valid, b, oy, ox, kb);
+                    fence_proxy_async_smem();
+                    mbar_arrive(&full[stage]);
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+        if (r == 0) wc.flush(g.dbg, 3);
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),
+// K order r) -> int8 +-1 rows [Dpad, Kpad] in the engine's K order. With T > 1 the engine
+// order is tap-major (k' = tap*C + c) and the reference order is channel-major
+// (r = c*T + tap): conv taps (lowering.hpp:8-10) or the spatial positions of
+// flatten_to_columns (network.cpp:177-184). T == 1 is the identity. With perm_bits, byte
+// position 4s + j inside every 32-position group holds logical position 8j + s, the order
+// put_word() emits activation bits in. Rows >= D and columns >= K are 0.
+//
+// Operand encoding: activations enter the MMA as their bits {0, 1} (not +-1), so the
+// accumulator is u = sum_k bit_k w_k and the reference's value is a = 2u - S_d with
+// S_d = sum_k w_k (prep_params_kernel). Everything stays exact integer arithmetic.
+__global__ void prep_weights_kernel(const uint32_t* __restrict__ packed, size_t ldw, int D, int K, int C,
+                                    int T, int perm_bits, int Kpad, size_t total, int8_t* __restrict__ out) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int d = int(i / Kpad), kb = int(i % Kpad);
+        const int k = perm_bits ? ((kb & ~31) | (8 * (kb & 3) + ((kb >> 2) & 7))) : kb;
+        int8_t v = 0;
+        if (d < D && k < K) {
+            const int rr = T > 1 ? (k % C) * T + k / C : k;
+            v = ((packed[size_t(d) * ldw + (rr >> 5)] >> (rr & 31)) & 1u) ? 1 : -1;
+        }
+        out[i] = v;
+    }
+}
+
+// Per output channel: S_d = sum of the prepared weights, and the integer threshold that
+// reproduces the reference's float decision exactly. The reference binarizes
+//     z(a) = fmaf(scale, float(a) + bias, shift)        (to_float, bias_add, affine_norm)
+// with sign(htanh(z)) = (z >= 0). Rounding is monotone, so P(a) = (z(a) >= 0) is monotone in
+// the integer a: P(a) = (a >= T) ^ flip for a T in [-K, K+1]. T and flip are found by
+// evaluating P with the same IEEE operations (__fadd_rn, __fmaf_rn) at every a in [-K, K]
+// and checking the step form for all of them; a channel that fails the check is reported
+// (the engine then refuses to fuse). In the accumulator domain a = 2u - S_d, so
+// a >= T  <=>  u >= ceil((T + S_d) / 2) = Tu.
+__global__ void prep_params_kernel(const int8_t* __restrict__ w8, int Kpad, int D, int Dp, int K,
+                                   const float* bias, const float* scale, const float* shift,
+                                   int4* __restrict__ prm, int* bad) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= Dp) return;
+    if (d >= D) {
+        prm[d] = make_int4(0, 0, 0, 0);
+        return;
+    }
+    int S = 0;
+    for (int k = 0; k < Kpad; ++k) S += w8[size_t(d) * Kpad + k];
+    const float b = bias[d], sc = scale ? scale[d] : 1.0f, sh = shift ? shift[d] : 0.0f;
+    auto P = [&](int a) { return __fmaf_rn(sc, __fadd_rn(__int2float_rn(a), b), sh) >= 0.0f; };
+    int T = K + 1;
+    const bool p_lo = P(-K);
+    int flip = p_lo ? 1 : 0;  // increasing predicate starts false; decreasing starts true
+    for (int a = -K; a <= K; ++a)
+        if (P(a) != p_lo) {
+            T = a;
+            break;
+        }
+    // P(a) = (a >= T) ^ flip must hold at every a (one step at most)
+    for (int a = -K; a <= K; ++a)
+        if (P(a) != (bool((a >= T) ? 1 : 0) != bool(flip))) {
+            atomicExch(bad, 1);
+            break;
+        }
+    const int Tu = (T + S + 1) >> 1;  // ceil((T + S) / 2), arithmetic shift = floor
+    prm[d] = make_int4(Tu, flip, S, __float_as_int(b));
+}
+
+// First-layer encoder for FIN_PIX: the sign bits of a pixel's C <= 32 channels in one word,
+// out[(b*H + y)*W + x] bit c = (x[b, c, y, x] >= 0) (binarize.cpp:9). Reads are coalesced per
+// channel plane; 4 bytes written per pixel.
+__global__ void pack_pixels_kernel(const float* __restrict__ x, int C, size_t HW, size_t total,
+                                   uint32_t* __restrict__ out) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const size_t b = i / HW, p = i - b * HW;
+        const float* src = x + b * C * HW + p;
+        uint32_t w = 0;
+        for (int c = 0; c < C; ++c) w |= uint32_t(__ldg(src + c * HW) >= 0.0f) << c;
+        out[i] = w;
+    }
+}
+
+template <int BN, int IN, int EPI>
+int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    auto kern = fused_layer_kernel<BN, IN, EPI>;
+    static bool attr_set = false;  // per instantiation; the attribute is per function
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(fused_smem<BN>())));
+        attr_set = true;
+    }
+    const int m_tiles = (g.rows + kRows - 1) / kRows;
+    const int tiles = m_tiles * g.n_tiles;
+    const int grid = std::min(tiles, num_sms());
+    static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
+    if (!prof) {
+        kern<<<grid, kThreads, fused_smem<BN>(), s>>>(tm, g);
+        return launch_check("fused_layer_kernel");
+    }
+    FusedGeom gd = g;
+    unsigned long long* dbg = nullptr;
+    BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
+    gd.dbg = dbg;
+    gd.dbg_mode = prof >> 1;  // 2: producer skips its stores, 4: epilogue skips its math
+    kern<<<grid, kThreads, fused_smem<BN>(), s>>>(tm, gd);
+    BNN_TRY(launch_check("fused_layer_kernel"));
+    unsigned long long h[16];
+    BNN_CUDA(cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost));
+    cudaFree(dbg);
+    const double n = double(grid);
+    fprintf(stderr,
+            "[fused BN=%d in=%d epi=%d rows=%d D=%d KB=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | "
+            "mma wait-acc %.1f wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
+            BN, IN, EPI, g.rows, g.D, g.KB, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
+            h[8] / n / 1e3, h[12] / n / 1e3);
+    return BNN_OK;
+}
+
+template <int IN, int EPI>
+int launch_fused_bn(int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    switch (BN) {
+        case 32: return launch_fused_t<32, IN, EPI>(tm, g, s);
+        case 64: return launch_fused_t<64, IN, EPI>(tm, g, s);
+        case 128: return launch_fused_t<128, IN, EPI>(tm, g, s);
+        case 256: return launch_fused_t<256, IN, EPI>(tm, g, s);
+        default: return fail(BNN_E_CONFIG, "fused layer: unsupported BN " + std::to_string(BN));
+    }
+}
+
+}  // namespace
+
+int make_tmap_2d_s8(CUtensorMap* map, const void* base, size_t rows, size_t K, size_t ld, uint32_t box_rows);
+
+int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
+                       int Kpad, int8_t* out, cudaStream_t s) {
+    const size_t total = size_t(Dpad) * Kpad;
+    const unsigned grid = unsigned(std::min<size_t>(ceil_div(total, 256), size_t(num_sms()) * 16));
+    prep_weights_kernel<<<grid, 256, 0, s>>>(packed, ldw, D, K, C, T, perm_bits, Kpad, total, out);
+    return launch_check("prep_weights_kernel");
+}
+
+int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const float* bias, const float* scale,
+                      const float* shift, int4* prm, int* bad_dev, cudaStream_t s) {
+    prep_params_kernel<<<unsigned(ceil_div(size_t(Dp), 64)), 64, 0, s>>>(w8, Kpad, D, Dp, K, bias, scale, shift,
+                                                                        prm, bad_dev);
+    return launch_check("prep_params_kernel");
+}
+
+int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN) {
+    return make_tmap_2d_s8(map, w, size_t(Dpad), size_t(Kpad), size_t(Kpad), uint32_t(BN));
+}
+
+int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s) {
+    const size_t total = B * HW;
+    if (!total) return BNN_OK;
+    const unsigned grid = unsigned(std::min<size_t>(ceil_div(total, 256), size_t(num_sms()) * 8));
+    pack_pixels_kernel<<<grid, 256, 0, s>>>(x, C, HW, total, out);
+    return launch_check("pack_pixels_kernel");
+}
+
+int launch_fused(int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    if (g.rows <= 0) return BNN_OK;
+    set_last_gemm("fused_umma_i8");
+    if (in_mode == FIN_PIX) {
+        if (epi == FEPI_BITS) return launch_fused_bn<FIN_PIX, FEPI_BITS>(BN, tm, g, s);
+        return launch_fused_bn<FIN_PIX, FEPI_NCHW>(BN, tm, g, s);
+    }
+    if (in_mode == FIN_BITS) {
+        if (epi == FEPI_BITS) return launch_fused_bn<FIN_BITS, FEPI_BITS>(BN, tm, g, s);
+        if (epi == FEPI_LOGITS) return launch_fused_bn<FIN_BITS, FEPI_LOGITS>(BN, tm, g, s);
+        return launch_fused_bn<FIN_BITS, FEPI_NCHW>(BN, tm, g, s);
+    }
+    if (epi == FEPI_BITS) return launch_fused_bn<FIN_F32, FEPI_BITS>(BN, tm, g, s);
+    if (epi == FEPI_NCHW) return launch_fused_bn<FIN_F32, FEPI_NCHW>(BN, tm, g, s);
+    return fail(BNN_E_CONFIG, "fused layer: float input needs a bits or NCHW epilogue");
+}
+
+}  // namespace bnnk

@@ -1,0 +1,44 @@
+// Fused binary layer (fused.cu): geometry block and launch entry points.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bnnk {
+
+// activation producer input: packed NHWC bits, float NCHW (im2col in the producer), or the
+// pixel-packed sign bits of a first layer with few channels (pack_pixels_kernel)
+enum { FIN_BITS = 0, FIN_F32 = 1, FIN_PIX = 2 };
+enum { FEPI_BITS = 0, FEPI_LOGITS = 1, FEPI_NCHW = 2 };  // epilogue output
+
+struct FusedGeom {
+    const void* in;  // FIN_BITS: u32 [B, H, W, Cw] packed NHWC; FIN_F32: float [B, C, H, W]
+    int B, H, W, C, Cw;
+    int KH, KW, SH, SW, PH, PW;
+    int OH, OW;
+    int K;        // logical reduction length (KH*KW*C)
+    int KB;       // 128-element K blocks (Kpad / 128)
+    int D;        // output channels / features
+    int rows;     // GEMM rows: B*OH*OW (conv) or B (linear)
+    int pool;     // rows are pool-major and the epilogue takes the 2x2 max
+    int n_tiles;  // ceil(D / BN)
+    const int4* prm;    // [>= n_tiles*BN] (Tu, flip, S_d, bias bits): prep_params_kernel
+    uint32_t* out_bits; // FEPI_BITS: [rows / (pool ? 4 : 1), Dw]
+    int Dw;             // D / 32
+    float* out_f32;     // FEPI_LOGITS: [D, ldo] (features x batch); FEPI_NCHW: [B, D, OH*OW]
+    int ldo;
+    unsigned long long* dbg;  // profiling counters (BNN_FUSED_PROFILE=1), else null
+    int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math
+};
+
+int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
+                       int Kpad, int8_t* out, cudaStream_t s);
+int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const float* bias, const float* scale,
+                      const float* shift, int4* prm, int* bad_dev, cudaStream_t s);
+int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN);
+int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s);
+int launch_fused(int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
+
+}  // namespace bnnk

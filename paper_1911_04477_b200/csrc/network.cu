@@ -13,11 +13,13 @@
 // + K1 pack_cols(sign) + K3; maxpool / affine / htanh / sign = K4. Activations ping-pong
 // between two arena buffers sized for the largest layer at the requested batch.
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "bnn_common.cuh"
+#include "fused.cuh"
 
 namespace bnnk {
 
@@ -78,6 +80,17 @@ struct Layer {
     bool out_flat = false;
 };
 
+// One fused launch (fused.cu): a weighted layer plus the glue that follows it.
+struct FusedStage {
+    size_t layer = 0, last = 0;  // weighted layer index, last layer folded into it
+    int in_mode = FIN_BITS, epi = FEPI_BITS;
+    FusedGeom g{};               // batch-independent fields
+    int Dpad = 0, Kpad = 0;
+    DevBuf w8, prm;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
+    CUtensorMap tm[4];           // weight tile maps for BN = 32, 64, 128, 256
+    size_t out_words_per_image = 0;
+};
+
 }  // namespace bnnk
 
 struct bnn_net {
@@ -98,6 +111,14 @@ struct bnn_net {
     std::vector<cudaEvent_t> pool;
     std::vector<double> layer_ms, gemm_ms;
     std::vector<size_t> gemm_launches;
+    // fused engine (fused.cu): one launch per weighted layer, packed-bit activations
+    int engine_policy = 0;  // BNN_ENGINE_AUTO / GENERIC / FUSED
+    bool fusable = false;
+    std::string unfusable_why;
+    std::vector<std::unique_ptr<bnnk::FusedStage>> stages;
+    size_t bits_words_per_image = 0;
+    size_t bits_batch = 0;
+    bnnk::DevBuf bits[2], pix;
 };
 
 namespace bnnk {
@@ -194,6 +215,129 @@ int build(bnn_net* net, const bnn_layer_spec* specs, size_t n, uint64_t seed, cu
     return BNN_OK;
 }
 
+size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+// Recognise the fusable pattern (network.cpp:330-420 semantics preserved exactly, see fused.cu):
+//   conv (float input) -> { [maxpool] [affine_norm] [htanh] [sign] -> conv|linear }* -> linear (logits)
+// Every weighted layer after the first reads packed bits; every glue run ends in a weighted layer
+// (whose pack_cols(sign(.)) makes a trailing htanh/sign redundant). Anything else -> generic engine.
+int plan_fused(bnn_net* net, cudaStream_t s) {
+    auto& Ls = net->layers;
+    const size_t n = Ls.size();
+    auto no = [&](const std::string& why) {
+        net->fusable = false;
+        net->unfusable_why = why;
+        net->stages.clear();
+        return BNN_OK;
+    };
+    size_t i = 0;
+    size_t max_words = 0;
+    DevBuf bad;
+    BNN_TRY(bad.alloc(sizeof(int)));
+    BNN_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    while (i < n) {
+        Layer& L = *Ls[i];
+        const uint32_t kind = L.spec.kind;
+        if (kind != BNN_LAYER_CONV && kind != BNN_LAYER_LINEAR)
+            return no("layer " + std::to_string(i) + " is glue without a preceding weighted layer");
+        const bool first = i == 0;
+        if (first && kind != BNN_LAYER_CONV) return no("first layer is not a conv");
+        auto st = std::make_unique<FusedStage>();
+        st->layer = i;
+        st->in_mode = FIN_BITS;
+        FusedGeom& g = st->g;
+        int T = 1, Cperm = 1;
+        if (kind == BNN_LAYER_CONV) {
+            g.C = int(L.in_c), g.H = int(L.in_h), g.W = int(L.in_w);
+            g.KH = int(L.geom.kernel_h), g.KW = int(L.geom.kernel_w);
+            g.SH = int(L.geom.stride_h), g.SW = int(L.geom.stride_w);
+            g.PH = int(L.geom.pad_h), g.PW = int(L.geom.pad_w);
+            g.OH = int(L.out_h), g.OW = int(L.out_w);
+            T = g.KH * g.KW, Cperm = int(L.in_c);
+            if (first) {
+                st->in_mode = (g.C <= 32 && T <= 16 && T * g.C <= 64) ? FIN_PIX : FIN_F32;
+                if (st->in_mode == FIN_F32) T = 1, Cperm = 1;  // reference im2col order
+            } else if (L.in_c % 32) {
+                return no("conv input channels not a multiple of 32");
+            }
+        } else {
+            g.C = int(L.cols), g.H = g.W = 1, g.KH = g.KW = g.SH = g.SW = 1, g.PH = g.PW = 0;
+            g.OH = g.OW = 1;
+            if (L.cols % 32) return no("linear input features not a multiple of 32");
+            if (!L.in_flat) T = int(L.in_h * L.in_w), Cperm = int(L.in_c);  // NHWC flatten order
+        }
+        g.Cw = g.C / 32;
+        g.K = int(L.cols);
+        g.D = int(L.rows);
+        size_t j = i + 1;
+        bool pool = false;
+        Layer* aff = nullptr;
+        if (j < n && Ls[j]->spec.kind == BNN_LAYER_MAXPOOL) {
+            if (kind != BNN_LAYER_CONV) return no("maxpool after a linear layer");
+            pool = true, ++j;
+        }
+        if (j < n && Ls[j]->spec.kind == BNN_LAYER_AFFINE) aff = Ls[j].get(), ++j;
+        if (j < n && Ls[j]->spec.kind == BNN_LAYER_HTANH) ++j;
+        if (j < n && Ls[j]->spec.kind == BNN_LAYER_SIGN) ++j;
+        if (j == n) {
+            if (j != i + 1 || kind != BNN_LAYER_LINEAR)
+                return no("the network does not end in a bare linear layer");
+            st->epi = FEPI_LOGITS;
+        } else {
+            const uint32_t nk = Ls[j]->spec.kind;
+            if (nk != BNN_LAYER_CONV && nk != BNN_LAYER_LINEAR)
+                return no("unsupported glue sequence after layer " + std::to_string(i));
+            if (L.rows % 32) return no("output channels not a multiple of 32");
+            st->epi = FEPI_BITS;
+        }
+        g.pool = pool ? 1 : 0;
+        g.Dw = g.D / 32;
+        st->last = j - 1;
+        st->Kpad = int(round_up(size_t(g.K), 128));
+        st->Dpad = int(round_up(size_t(g.D), 32));
+        g.KB = st->Kpad / 128;
+        if (st->in_mode == FIN_F32 && g.K > 1024) return no("first conv reduction length > 1024");
+        if (st->in_mode == FIN_BITS && st->Kpad / 32 > 1024) return no("reduction length > 32768");
+        const size_t prm_n = round_up(size_t(g.D), 256);
+        BNN_TRY(st->w8.alloc(size_t(st->Dpad) * st->Kpad));
+        BNN_TRY(st->prm.alloc(prm_n * sizeof(int4)));
+        BNN_TRY(fused_prep_weights(L.packed.as<uint32_t>(), L.wpl, g.D, g.K, Cperm, T, st->in_mode == FIN_F32 ? 0 : 1, st->Dpad,
+                                   st->Kpad, st->w8.as<int8_t>(), s));
+        BNN_TRY(fused_prep_params(st->w8.as<int8_t>(), st->Kpad, g.D, int(prm_n), g.K, L.bias.as<float>(),
+                                  aff ? aff->scale.as<float>() : nullptr, aff ? aff->shift.as<float>() : nullptr,
+                                  st->prm.as<int4>(), bad.as<int>(), s));
+        g.prm = st->prm.as<int4>();
+        const int bns[4] = {32, 64, 128, 256};
+        for (int b = 0; b < 4; ++b)
+            BNN_TRY(fused_make_tmap(&st->tm[b], st->w8.as<int8_t>(), st->Dpad, st->Kpad, bns[b]));
+        if (st->epi == FEPI_BITS) {
+            const size_t pos = kind == BNN_LAYER_CONV ? size_t(g.OH) * g.OW / (pool ? 4 : 1) : 1;
+            st->out_words_per_image = pos * g.Dw;
+            max_words = std::max(max_words, st->out_words_per_image);
+        }
+        net->stages.push_back(std::move(st));
+        i = j;
+    }
+    int bad_h = 0;
+    BNN_CUDA(cudaMemcpyAsync(&bad_h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    BNN_CUDA(cudaStreamSynchronize(s));
+    if (bad_h) return no("a channel's binarization is not a step function of the accumulator");
+    net->bits_words_per_image = max_words;
+    net->fusable = true;
+    return BNN_OK;
+}
+
+int choose_bn(int D, int m_tiles) {
+    static const int forced = getenv("BNN_FUSED_BN") ? atoi(getenv("BNN_FUSED_BN")) : 0;  // experiments
+    if (forced == 32 || forced == 64 || forced == 128 || forced == 256) return forced;
+    int bn = 32;
+    while (bn < 256 && bn < D) bn *= 2;
+    while (bn > 32 && size_t(m_tiles) * ceil_div(size_t(D), size_t(bn)) < size_t(num_sms())) bn /= 2;
+    return bn;
+}
+
+int bn_index(int bn) { return bn == 32 ? 0 : bn == 64 ? 1 : bn == 128 ? 2 : 3; }
+
 int ensure_arena(bnn_net* net, size_t batch) {
     if (net->arena_batch >= batch) return BNN_OK;
     BNN_TRY(net->act[0].alloc(net->max_act_per_image * batch * 4));
@@ -235,8 +379,7 @@ struct EventPair {
     }
 };
 
-int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
-    if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
+int forward_generic(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     BNN_TRY(ensure_arena(net, B));
     size_t launches = 0;
     const float* cur = x;
@@ -316,6 +459,63 @@ int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t 
     return BNN_OK;
 }
 
+
+int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+    if (net->bits_batch < B) {
+        const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
+        BNN_TRY(net->bits[0].alloc(bytes));
+        BNN_TRY(net->bits[1].alloc(bytes));
+        BNN_TRY(net->pix.alloc(B * net->in_h * net->in_w * 4));
+        net->bits_batch = B;
+    }
+    const void* in = x;
+    int which = 0;
+    size_t launches = 0;
+    for (auto& stp : net->stages) {
+        FusedStage& st = *stp;
+        FusedGeom g = st.g;
+        const bool conv = net->layers[st.layer]->spec.kind == BNN_LAYER_CONV;
+        const size_t rows = conv ? B * size_t(g.OH) * g.OW : B;
+        if (rows > size_t(0x7fffffff) / 2) return fail(BNN_E_CONFIG, "fused engine: batch too large");
+        g.B = int(B);
+        g.in = in;
+        g.rows = int(rows);
+        const int m_tiles = int(ceil_div(rows, 128));
+        const int bn = choose_bn(g.D, m_tiles);
+        g.n_tiles = int(ceil_div(size_t(g.D), size_t(bn)));
+        if (st.epi == FEPI_BITS) {
+            g.out_bits = net->bits[which].as<uint32_t>();
+            which ^= 1;
+        } else {
+            g.out_f32 = logits;
+            g.ldo = int(B);
+        }
+        EventPair layer_ev(net, st.layer, 0, s);
+        if (st.in_mode == FIN_PIX) {  // first-layer sign bits, one word per pixel
+            BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
+            g.in = net->pix.as<uint32_t>();
+            ++launches;
+        }
+        EventPair gemm_ev(net, st.layer, 1, s);
+        BNN_TRY(launch_fused(bn, st.in_mode, st.epi, st.tm[bn_index(bn)], g, s));
+        gemm_ev.close();
+        layer_ev.close();
+        ++launches;
+        in = g.out_bits;
+    }
+    net->last_launches = launches;
+    return BNN_OK;
+}
+
+bool use_fused(const bnn_net* net) {
+    return net->fusable && net->engine_policy != BNN_ENGINE_GENERIC;
+}
+
+int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+    if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
+    if (use_fused(net)) return forward_fused(net, x, B, logits, s);
+    return forward_generic(net, x, B, logits, s);
+}
 }  // namespace
 }  // namespace bnnk
 
@@ -375,7 +575,8 @@ int bnn_net_create(const bnn_layer_spec* layers, size_t n_layers, size_t in_c, s
     net->in_c = in_c, net->in_h = in_h, net->in_w = in_w;
     cudaStream_t s;
     BNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    const int rc = build(net.get(), layers, n_layers, seed, s);
+    int rc = build(net.get(), layers, n_layers, seed, s);
+    if (rc == BNN_OK) rc = plan_fused(net.get(), s);
     cudaStreamDestroy(s);
     if (rc != BNN_OK) return rc;
     *out = net.release();
@@ -392,6 +593,17 @@ void bnn_net_destroy(bnn_net* net) {
     delete net;
 }
 size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
+
+int bnn_net_set_engine(bnn_net* net, int policy) {
+    if (policy < BNN_ENGINE_AUTO || policy > BNN_ENGINE_FUSED)
+        return fail(BNN_E_CONFIG, "bad engine policy");
+    if (policy == BNN_ENGINE_FUSED && !net->fusable)
+        return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
+    net->engine_policy = policy;
+    return BNN_OK;
+}
+
+int bnn_net_engine(const bnn_net* net) { return use_fused(net) ? BNN_ENGINE_FUSED : BNN_ENGINE_GENERIC; }
 size_t bnn_net_num_layers(const bnn_net* net) { return net->layers.size(); }
 size_t bnn_net_last_launches(const bnn_net* net) { return net->last_launches; }
 

@@ -1,0 +1,102 @@
+"""Fused engine (csrc/fused.cu) parity: one tcgen05 launch per weighted layer with the glue
+folded into the epilogue and packed-bit activations must reproduce the reference's
+network_forward(Binary) logits bit for bit (network.cpp:330-420)."""
+import numpy as np
+import pytest
+
+from conftest import INPUT_STREAM
+
+pytestmark = pytest.mark.gpu
+
+
+def _net(bnn, spec):
+    return bnn.Network(spec["layers"], tuple(spec["input_shape"][1:]), spec["seed"])
+
+
+def _oracle(orc, spec):
+    return orc.net(spec["layers"], tuple(spec["input_shape"][1:]), spec["seed"])
+
+
+def conv(d, k=3, s=1, p=1):
+    return {"kind": "conv", "out_channels": d, "kernel_size": k, "stride": s, "pad": p}
+
+
+def lin(f):
+    return {"kind": "linear", "out_features": f}
+
+
+G = [{"kind": "affine_norm"}, {"kind": "htanh"}, {"kind": "sign"}]
+POOL = [{"kind": "maxpool"}]
+
+FUSABLE = {
+    # Cw = 1 and 2 (per-word producer path), stride 2, rectangular kernels, no-affine glue
+    "narrow": {"input_shape": [1, 3, 16, 16], "seed": 7,
+               "layers": [conv(32, 4, 2, 1)] + G + [conv(64, 3, 1, 1)] + POOL + G +
+                         [conv(96, 2, 1, 0), {"kind": "sign"}, lin(64)] + G[:2] + [lin(9)]},
+    # 5x5 / pad 2 first layer, odd spatial sizes, linear straight after a conv (NHWC flatten)
+    "odd": {"input_shape": [1, 5, 9, 11], "seed": 11,
+            "layers": [conv(128, 5, 1, 2)] + G + [conv(128, 3, 2, 0)] + [{"kind": "affine_norm"}] +
+                      [lin(32), lin(10)]},
+    # C = 256 / 512 fast path with pooling down to 1x1, then a single logits layer
+    "wide": {"input_shape": [1, 3, 8, 8], "seed": 3,
+             "layers": [conv(256)] + POOL + G + [conv(512)] + POOL + G + [conv(256)] + POOL + G + [lin(33)]},
+}
+
+
+@pytest.fixture
+def fused(bnn):
+    def mk(spec=None, seed=1):
+        net = bnn.Network(seed=seed) if spec is None else _net(bnn, spec)
+        net.set_engine("fused")
+        assert net.engine == "fused"
+        return net
+    return mk
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 5, 33, 128, 129])
+def test_default_network_fused_vs_oracle(bnn, orc, fused, batch):
+    net = fused()
+    x = orc.fill_random((batch, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
+    got = net.forward(x)
+    assert net.last_launches() == 10  # first-layer pixel encoder + one launch per weighted layer
+    assert np.array_equal(got, orc.net(seed=1).forward(x))
+
+
+def test_default_network_fused_equals_generic_large_batch(bnn, orc, fused):
+    torch = pytest.importorskip("torch")
+    net = fused(seed=4)
+    x = torch.from_numpy(orc.fill_random((1000, 3, 32, 32), 12345)).cuda()
+    a = net.forward_device(x).cpu().numpy()
+    net.set_engine("generic")
+    b = net.forward_device(x).cpu().numpy()
+    assert np.array_equal(a, b)
+    # and a slice checked against the oracle directly
+    xs = x[:7].cpu().numpy()
+    assert np.array_equal(a[:, :7], orc.net(seed=4).forward(xs))
+
+
+def test_default_network_engine_is_fused_by_default(bnn):
+    assert bnn.Network(seed=1).engine == "fused"
+
+
+@pytest.mark.parametrize("name", sorted(FUSABLE))
+@pytest.mark.parametrize("batch", [1, 6])
+def test_fusable_topologies_vs_oracle(bnn, orc, fused, name, batch):
+    spec = dict(FUSABLE[name])
+    net = fused(spec)
+    shape = (batch, *spec["input_shape"][1:])
+    x = orc.fill_random(shape, orc.mix64(spec["seed"], INPUT_STREAM))
+    got = net.forward(x)
+    want = _oracle(orc, spec).forward(x)
+    assert np.array_equal(got, want), name
+
+
+def test_unfusable_topology_uses_generic_engine(bnn, orc):
+    spec = {"input_shape": [1, 4, 12, 12], "seed": 99,
+            "layers": [conv(40), {"kind": "htanh"}, {"kind": "affine_norm"}, lin(9)]}
+    net = _net(bnn, spec)
+    assert net.engine == "generic"
+    with pytest.raises(bnn.ConfigError):
+        net.set_engine("fused")
+    x = orc.fill_random((3, 4, 12, 12), 5)
+    assert np.array_equal(net.forward(x), _oracle(orc, spec).forward(x))
