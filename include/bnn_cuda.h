@@ -195,6 +195,10 @@ int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]);
  * AUTO (default) = FUSED when available. Both are bit-exact with the reference. */
 enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2 };
 int bnn_net_set_engine(bnn_net* net, int policy);
+/* Fused-engine tile shape override, process-wide (tests / experiments): cta_group 1 (M=128
+ * per CTA) or 2 (CTA pairs, M=256, tcgen05 cta_group::2), bn = MMA N in {32,64,128,256};
+ * 0 = automatic (the default). */
+int bnn_set_fused_tiling(int cta_group, int bn);
 /* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
 int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */

@@ -40,6 +40,7 @@
 //               packed words per stage (one 16-byte load), expand bit -> +-1 byte and store
 //               them in the SWIZZLE_128B K-major layout the UMMA descriptor expects.
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -53,8 +54,9 @@ using namespace umma;
 
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kThreads = 320;
+constexpr int kStages = 4;   // CG = 1: A 16 KB + B up to 32 KB per stage
+constexpr int kStages2 = 6;  // CG = 2: A 16 KB + B up to 16 KB per stage (per CTA)
+constexpr int kThreads = 320;  // 10 warps: TMA, MMA, 4 epilogue, 4 producer
 constexpr int kRows = 128;   // UMMA M
 constexpr int kKB = 128;     // K bytes per stage
 
@@ -62,10 +64,10 @@ constexpr int kMaxF32K = 1024;  // float-input layers: K <= this (im2col offset 
 constexpr int kMaxQ = 1024;     // K words per layer (bits mode), entries of the offset table
 constexpr int kMaxPixTaps = 16; // pixel-packed first layer: taps (and taps*C <= 64)
 
-template <int BN>
+template <int BN, int CG>
 constexpr size_t fused_smem() {
     static_assert(kMaxF32K <= kMaxQ, "one table region");
-    return 1024 + size_t(kStages) * (kRows + BN) * kKB + 256 + kMaxQ * 8;
+    return 1024 + size_t(CG == 2 ? kStages2 : kStages) * (kRows + BN / CG) * kKB + 256 + kMaxQ * 8;
 }
 
 __device__ __forceinline__ bool decode_row(const FusedGeom& g, int row, int& b, int& oy, int& ox) {
@@ -140,23 +142,36 @@ __device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab,
 // Pixel-packed first layer (FIN_PIX): in[(b*H + y)*W + x] holds the C <= 32 sign bits of one
 // input pixel (pack_pixels_kernel). The row's K = T*C bits are gathered tap by tap,
 // tap-major / channel-minor (K <= 64: one K block). qtab[tap] = {dy<<16 | dx&0xffff, 0}.
-__device__ __forceinline__ uint4 load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
+// load_pix() only issues the loads (their values are consumed kPF blocks later by
+// gather_pix(), so the L2 latency is hidden like the bits path's).
+struct PixRaw {
+    uint32_t v[kMaxPixTaps];
+};
+
+__device__ __forceinline__ PixRaw load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
     const uint32_t* pix = static_cast<const uint32_t*>(g.in);
-    if (!rc.valid) return make_uint4(0, 0, 0, 0);
     const int T = g.KH * g.KW;
     const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
-    uint64_t acc = 0;
+    PixRaw raw;
 #pragma unroll
     for (int tap = 0; tap < kMaxPixTaps; ++tap) {
-        if (tap < T) {
-            const int2 e = qtab[tap];
-            const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
-            const uint32_t v = (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
-                                   ? __ldg(pix + size_t(rc.pix + iy) * g.W + ix)
-                                   : cmask;  // padding: every channel +1
-            acc |= uint64_t(v) << (tap * g.C);
-        }
+        const int2 e = qtab[tap < T ? tap : 0];
+        const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
+        uint32_t v = cmask;  // padding: every channel +1
+        if (rc.valid && tap < T && unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
+            v = __ldg(pix + size_t(rc.pix + iy) * g.W + ix);
+        raw.v[tap] = v;
     }
+    return raw;
+}
+
+__device__ __forceinline__ uint4 gather_pix(const FusedGeom& g, const PixRaw& raw, bool valid) {
+    if (!valid) return make_uint4(0, 0, 0, 0);
+    const int T = g.KH * g.KW;
+    uint64_t acc = 0;
+#pragma unroll
+    for (int tap = 0; tap < kMaxPixTaps; ++tap)
+        if (tap < T) acc |= uint64_t(raw.v[tap]) << (tap * g.C);
     return make_uint4(uint32_t(acc), uint32_t(acc >> 32), 0u, 0u);
 }
 
@@ -222,38 +237,49 @@ struct WaitClock {
     }
 };
 
-template <int BN, int IN, int EPI>
+// CG = 1: one CTA computes a 128-row tile with M=128 x N=BN instructions.
+// CG = 2: a CTA pair (cluster of 2) computes a 256-row tile with cta_group::2 M=256 x N=BN
+// instructions issued by the even CTA: each CTA produces its own 128 activation rows, TMA-loads
+// half of the weight tile (BN/2 rows), and holds its 128 accumulator rows in its own TMEM. The
+// i8 MMA costs the same per instruction for any N <= 256 at M=128 (measured, profiles/), so
+// layers with D = 128 need the pair to reach the full tensor rate; the pair also halves each
+// SM's weight traffic.
+template <int BN, int IN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_layer_kernel(const __grid_constant__ CUtensorMap tmW, const FusedGeom g) {
+    constexpr int kS = CG == 2 ? kStages2 : kStages;
+    constexpr int BH = BN / CG;  // weight rows held by this CTA
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base - raw);
-    uint8_t* sA = smem;                                   // [kStages][128 * 128]
-    uint8_t* sB = smem + size_t(kStages) * kRows * kKB;   // [kStages][BN * 128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kStages) * BN * kKB);
+    uint8_t* sA = smem;                               // [kS][128 * 128]
+    uint8_t* sB = smem + size_t(kS) * kRows * kKB;    // [kS][BH * 128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kS) * BH * kKB);
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* empty = bars + kS;
+    uint64_t* tfull = bars + 2 * kS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int2* ftab = reinterpret_cast<int2*>(bars + 32);      // offset table [kMaxQ]
+    int2* ftab = reinterpret_cast<int2*>(bars + 32);  // offset table [kMaxQ]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m_tiles = (g.rows + kRows - 1) / kRows;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const int unit = blockIdx.x / CG, units = gridDim.x / CG;
+    const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
     const int n_tiles = g.n_tiles;
     const int tiles = m_tiles * n_tiles;
     const int KB = g.KB;
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], kRows + 1);  // 128 producer threads + the TMA expect_tx arrive
+        for (int s = 0; s < kS; ++s) {
+            mbar_init(&full[s], 4 * CG + CG);  // one arrive per producer warp + per TMA thread
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * CG);
         }
         fence_mbar_init();
     }
@@ -279,11 +305,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
         }
     }
-    if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+    if (warp == 1) {
+        if (CG == 2)
+            tmem_alloc_cg2<2 * BN>(tmem_slot);
+        else
+            tmem_alloc<2 * BN>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+
+    // barrier the producers / TMA / epilogue signal: the even CTA's (shared::cluster address)
+    auto leader = [&](uint64_t* bar) { return CG == 2 ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
 
     if (warp == 0) {
         // -------------------------------------------------------------- weight TMA
@@ -291,48 +326,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             WaitClock wc;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int t = unit; t < tiles; t += units) {
                 const int nt = t % n_tiles;
                 for (int kb = 0; kb < KB; ++kb) {
                     wc.wait(&empty[stage], phase ^ 1, 0);
-                    mbar_arrive_expect_tx(&full[stage], BN * kKB);
-                    tma_load_2d(&tmW, &full[stage], sB + size_t(stage) * BN * kKB, kb * kKB, nt * BN);
-                    if (++stage == kStages) stage = 0, phase ^= 1;
+                    uint8_t* dst = sB + size_t(stage) * BH * kKB;
+                    if (CG == 2) {
+                        const uint32_t fb = leader(&full[stage]);
+                        mbar_arrive_expect_tx_cluster(fb, BH * kKB);
+                        tma_load_2d_cg2(&tmW, fb, dst, kb * kKB, nt * BN + int(rank) * BH);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], BH * kKB);
+                        tma_load_2d(&tmW, &full[stage], dst, kb * kKB, nt * BN);
+                    }
+                    if (++stage == kS) stage = 0, phase ^= 1;
                 }
             }
             wc.flush(g.dbg, 0);
         }
     } else if (warp == 1) {
         // -------------------------------------------------------------- UMMA issuer
-        constexpr uint32_t idesc = idesc_i8(kRows, BN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        WaitClock wc;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-            wc.wait(&tempty[acc], acc_phase ^ 1, 0);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-            for (int kb = 0; kb < KB; ++kb) {
-                wc.wait(&full[stage], phase, 1);
+        if (CG == 1 || rank == 0) {
+            constexpr uint32_t idesc = idesc_i8(kRows * CG, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            WaitClock wc;
+            for (int t = unit; t < tiles; t += units) {
+                wc.wait(&tempty[acc], acc_phase ^ 1, 0);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = smem_u32(sA + size_t(stage) * kRows * kKB);
-                    const uint32_t b0 = smem_u32(sB + size_t(stage) * BN * kKB);
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < KB; ++kb) {
+                    wc.wait(&full[stage], phase, 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + size_t(stage) * kRows * kKB);
+                        const uint32_t b0 = smem_u32(sB + size_t(stage) * BH * kKB);
 #pragma unroll
-                    for (int k = 0; k < kKB / 32; ++k)
-                        mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                               (kb | k) != 0);
-                    mma_commit(&empty[stage]);
-                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                        for (int k = 0; k < kKB / 32; ++k) {
+                            if (CG == 2)
+                                mma_i8_cg2(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                           (kb | k) != 0);
+                            else
+                                mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                       (kb | k) != 0);
+                        }
+                        if (CG == 2) {
+                            mma_commit_cg2_mc(&empty[stage], 3);  // both CTAs' slots free
+                            if (kb == KB - 1) mma_commit_cg2_mc(&tfull[acc], 3);
+                        } else {
+                            mma_commit(&empty[stage]);
+                            if (kb == KB - 1) mma_commit(&tfull[acc]);
+                        }
+                    }
+                    __syncwarp();
+                    if (++stage == kS) stage = 0, phase ^= 1;
                 }
-                __syncwarp();
-                if (++stage == kStages) stage = 0, phase ^= 1;
+                if (++acc == 2) acc = 0, acc_phase ^= 1;
             }
-            if (++acc == 2) acc = 0, acc_phase ^= 1;
+            if (lane == 0) wc.flush(g.dbg, 1);
         }
-        if (lane == 0) wc.flush(g.dbg, 1);
     } else if (warp < 6) {
         // -------------------------------------------------------------- epilogue
         // Accumulator u = sum_k bit_k * w_k (bits in {0,1}, weights +-1); the reference's
@@ -342,9 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         WaitClock wc;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int t = unit; t < tiles; t += units) {
             const int mt = t / n_tiles, nt = t % n_tiles;
-            const int row = mt * kRows + r;
+            const int row = mt * kRows * CG + int(rank) * kRows + r;
             const int n0 = nt * BN;
             const bool valid = row < g.rows;
             wc.wait(&tfull[acc], acc_phase, 0);
@@ -398,11 +452,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM buffer free before the stores drain
+            if (lane == 0) {  // TMEM buffer free before the stores drain
+                if (CG == 2)
+                    mbar_arrive_cluster(leader(&tempty[acc]));
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
             if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
                 const int orow = g.pool ? (row >> 2) : row;
                 uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
-                if ((BN / 32) % 4 == 0 && (g.Dw & 3) == 0) {
+                if ((BN / 32) % 4 == 0 && (g.Dw & 3) == 0 && n0 + BN <= g.D) {
 #pragma unroll
                     for (int c = 0; c < BN / 32; c += 4)
                         *reinterpret_cast<uint4*>(dst + c) =
@@ -418,60 +477,79 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
     } else {
         // -------------------------------------------------------------- activation producers
+        // One tile row per thread: the row's 4 packed words of the block -> 128 operand bytes
+        // in the UMMA layout. The words are loaded kPF blocks ahead into registers.
+        // Measured limits (profiles/): the per-stage proxy fence (fence.proxy.async =
+        // MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC) drains in-flight loads, and the A-tile stores
+        // compete with the UMMA operand reads and the weight TMA for shared-memory bandwidth.
         const int r = threadIdx.x - 6 * 32;  // tile row 0..127
+        const int row_off = int(rank) * kRows + r;
         int stage = 0;
         uint32_t phase = 0;
         WaitClock wc;
+        auto publish = [&](int st) {  // this warp's rows of stage st are written
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2)
+                    mbar_arrive_cluster(leader(&full[st]));
+                else
+                    mbar_arrive(&full[st]);
+            }
+        };
         if (IN != FIN_F32) {
-            // flattened (tile, kb) stream with the global loads issued kPF blocks ahead, so
-            // the L2 latency overlaps the expansion of the blocks in between
             constexpr int kPF = 3;
-            int t_ld = blockIdx.x, kb_ld = 0;  // next block to load
+            using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw>::type;
+            int t_ld = unit, kb_ld = 0;  // next block to load
             RowCtx rc;
             auto set_row = [&]() {
                 int b = 0, oy = 0, ox = 0;
-                rc.valid = t_ld < tiles && decode_row(g, (t_ld / n_tiles) * kRows + r, b, oy, ox);
+                rc.valid = t_ld < tiles && decode_row(g, (t_ld / n_tiles) * kRows * CG + row_off, b, oy, ox);
                 rc.pix = b * g.H, rc.y0 = oy * g.SH, rc.x0 = ox * g.SW;
             };
             set_row();
-            uint4 pf[kPF];
-            auto next_load = [&]() -> uint4 {
-                uint4 u = make_uint4(0, 0, 0, 0);
-                if (t_ld < tiles) {
-                    u = IN == FIN_BITS ? load_bits(g, ftab, rc, kb_ld) : load_pix(g, ftab, rc);
-                    if (++kb_ld == KB) {
-                        kb_ld = 0;
-                        t_ld += gridDim.x;
-                        set_row();
-                    }
+            Raw pf[kPF];
+            bool pv[kPF];  // row validity of each prefetched block (pixel gather)
+            auto next_load = [&](Raw& dst, bool& v) {
+                v = rc.valid;
+                if constexpr (IN == FIN_BITS) {
+                    dst = t_ld < tiles ? load_bits(g, ftab, rc, kb_ld) : make_uint4(0, 0, 0, 0);
+                } else {
+                    dst = load_pix(g, ftab, rc);
                 }
-                return u;
+                if (t_ld < tiles && ++kb_ld == KB) {
+                    kb_ld = 0;
+                    t_ld += units;
+                    set_row();
+                }
             };
 #pragma unroll
-            for (int i = 0; i < kPF; ++i) pf[i] = next_load();
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
+            for (int t = unit; t < tiles; t += units) {
                 for (int kb = 0; kb < KB; ++kb) {
-                    const uint4 u = pf[0];
+                    uint4 u;
+                    if constexpr (IN == FIN_BITS)
+                        u = pf[0];
+                    else
+                        u = gather_pix(g, pf[0], pv[0]);
 #pragma unroll
-                    for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1];
-                    pf[kPF - 1] = next_load();
+                    for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1], pv[i] = pv[i + 1];
+                    next_load(pf[kPF - 1], pv[kPF - 1]);
                     wc.wait(&empty[stage], phase ^ 1, 0);
                     if (!(g.dbg_mode & 1)) store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
-                    fence_proxy_async_smem();
-                    mbar_arrive(&full[stage]);
-                    if (++stage == kStages) stage = 0, phase ^= 1;
+                    publish(stage);
+                    if (++stage == kS) stage = 0, phase ^= 1;
                 }
             }
         } else {
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int t = unit; t < tiles; t += units) {
                 int b = 0, oy = 0, ox = 0;
-                const bool valid = decode_row(g, (t / n_tiles) * kRows + r, b, oy, ox);
+                const bool valid = decode_row(g, (t / n_tiles) * kRows * CG + row_off, b, oy, ox);
                 for (int kb = 0; kb < KB; ++kb) {
                     wc.wait(&empty[stage], phase ^ 1, 0);
                     produce_f32(g, ftab, smem_u32(sA + size_t(stage) * kRows * kKB), r, valid, b, oy, ox, kb);
-                    fence_proxy_async_smem();
-                    mbar_arrive(&full[stage]);
-                    if (++stage == kStages) stage = 0, phase ^= 1;
+                    publish(stage);
+                    if (++stage == kS) stage = 0, phase ^= 1;
                 }
             }
         }
@@ -480,7 +558,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<2 * BN>(tmem_base);
+    if (CG == 2) {
+        cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
+        if (warp == 1) tmem_dealloc_cg2<2 * BN>(tmem_base);
+    } else if (warp == 1) {
+        tmem_dealloc<2 * BN>(tmem_base);
+    }
 }
 
 // Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),
@@ -564,52 +647,69 @@ __global__ void pack_pixels_kernel(const float* __restrict__ x, int C, size_t HW
     }
 }
 
-template <int BN, int IN, int EPI>
+template <int BN, int IN, int EPI, int CG>
 int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_layer_kernel<BN, IN, EPI>;
+    auto kern = fused_layer_kernel<BN, IN, EPI, CG>;
+    constexpr size_t smem = fused_smem<BN, CG>();
     static bool attr_set = false;  // per instantiation; the attribute is per function
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(fused_smem<BN>())));
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         attr_set = true;
     }
-    const int m_tiles = (g.rows + kRows - 1) / kRows;
+    const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
     const int tiles = m_tiles * g.n_tiles;
-    const int grid = std::min(tiles, num_sms());
+    const int grid = std::min(tiles, num_sms() / CG) * CG;
     static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
-    if (!prof) {
-        kern<<<grid, kThreads, fused_smem<BN>(), s>>>(tm, g);
-        return launch_check("fused_layer_kernel");
-    }
     FusedGeom gd = g;
     unsigned long long* dbg = nullptr;
-    BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
-    BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
-    gd.dbg = dbg;
-    gd.dbg_mode = prof >> 1;  // 2: producer skips its stores, 4: epilogue skips its math
-    kern<<<grid, kThreads, fused_smem<BN>(), s>>>(tm, gd);
+    if (prof) {
+        BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+        BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
+        gd.dbg = dbg;
+        gd.dbg_mode = prof >> 1;  // 2: producer skips its stores, 4: epilogue skips its math
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CG == 2 ? 1 : 0;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
     BNN_TRY(launch_check("fused_layer_kernel"));
-    unsigned long long h[16];
-    BNN_CUDA(cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost));
-    cudaFree(dbg);
-    const double n = double(grid);
-    fprintf(stderr,
-            "[fused BN=%d in=%d epi=%d rows=%d D=%d KB=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | "
-            "mma wait-acc %.1f wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
-            BN, IN, EPI, g.rows, g.D, g.KB, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
-            h[8] / n / 1e3, h[12] / n / 1e3);
+    if (prof) {
+        unsigned long long h[16];
+        BNN_CUDA(cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost));
+        cudaFree(dbg);
+        const double n = double(grid);
+        fprintf(stderr,
+                "[fused CG=%d BN=%d in=%d epi=%d rows=%d D=%d KB=%d grid=%d] per-CTA kcycles: total %.1f | tma wait "
+                "%.1f | mma wait-acc %.1f wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
+                CG, BN, IN, EPI, g.rows, g.D, g.KB, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3 * CG,
+                h[5] / n / 1e3 * CG, h[8] / n / 1e3, h[12] / n / 1e3);
+    }
     return BNN_OK;
 }
 
-template <int IN, int EPI>
+template <int IN, int EPI, int CG>
 int launch_fused_bn(int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     switch (BN) {
-        case 32: return launch_fused_t<32, IN, EPI>(tm, g, s);
-        case 64: return launch_fused_t<64, IN, EPI>(tm, g, s);
-        case 128: return launch_fused_t<128, IN, EPI>(tm, g, s);
-        case 256: return launch_fused_t<256, IN, EPI>(tm, g, s);
+        case 32: return launch_fused_t<32, IN, EPI, CG>(tm, g, s);
+        case 64: return launch_fused_t<64, IN, EPI, CG>(tm, g, s);
+        case 128: return launch_fused_t<128, IN, EPI, CG>(tm, g, s);
+        case 256: return launch_fused_t<256, IN, EPI, CG>(tm, g, s);
         default: return fail(BNN_E_CONFIG, "fused layer: unsupported BN " + std::to_string(BN));
     }
+}
+
+template <int IN, int EPI>
+int launch_fused_cg(int cg, int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    return cg == 2 ? launch_fused_bn<IN, EPI, 2>(BN, tm, g, s) : launch_fused_bn<IN, EPI, 1>(BN, tm, g, s);
 }
 
 }  // namespace
@@ -643,20 +743,20 @@ int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out
     return launch_check("pack_pixels_kernel");
 }
 
-int launch_fused(int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+int launch_fused(int cg, int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
-    set_last_gemm("fused_umma_i8");
+    set_last_gemm(cg == 2 ? "fused_umma_i8_cg2" : "fused_umma_i8");
     if (in_mode == FIN_PIX) {
-        if (epi == FEPI_BITS) return launch_fused_bn<FIN_PIX, FEPI_BITS>(BN, tm, g, s);
-        return launch_fused_bn<FIN_PIX, FEPI_NCHW>(BN, tm, g, s);
+        if (epi == FEPI_BITS) return launch_fused_cg<FIN_PIX, FEPI_BITS>(cg, BN, tm, g, s);
+        return launch_fused_cg<FIN_PIX, FEPI_NCHW>(cg, BN, tm, g, s);
     }
     if (in_mode == FIN_BITS) {
-        if (epi == FEPI_BITS) return launch_fused_bn<FIN_BITS, FEPI_BITS>(BN, tm, g, s);
-        if (epi == FEPI_LOGITS) return launch_fused_bn<FIN_BITS, FEPI_LOGITS>(BN, tm, g, s);
-        return launch_fused_bn<FIN_BITS, FEPI_NCHW>(BN, tm, g, s);
+        if (epi == FEPI_BITS) return launch_fused_cg<FIN_BITS, FEPI_BITS>(cg, BN, tm, g, s);
+        if (epi == FEPI_LOGITS) return launch_fused_cg<FIN_BITS, FEPI_LOGITS>(cg, BN, tm, g, s);
+        return launch_fused_cg<FIN_BITS, FEPI_NCHW>(cg, BN, tm, g, s);
     }
-    if (epi == FEPI_BITS) return launch_fused_bn<FIN_F32, FEPI_BITS>(BN, tm, g, s);
-    if (epi == FEPI_NCHW) return launch_fused_bn<FIN_F32, FEPI_NCHW>(BN, tm, g, s);
+    if (epi == FEPI_BITS) return launch_fused_cg<FIN_F32, FEPI_BITS>(cg, BN, tm, g, s);
+    if (epi == FEPI_NCHW) return launch_fused_cg<FIN_F32, FEPI_NCHW>(cg, BN, tm, g, s);
     return fail(BNN_E_CONFIG, "fused layer: float input needs a bits or NCHW epilogue");
 }
 

@@ -39,6 +39,8 @@ int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const fl
                       const float* shift, int4* prm, int* bad_dev, cudaStream_t s);
 int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN);
 int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s);
-int launch_fused(int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
+// cg = 1: CTA-local M=128 tiles; cg = 2: CTA pairs with cta_group::2 M=256 tiles. tm must be
+// the weight map whose box has BN / cg rows.
+int launch_fused(int cg, int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
 
 }  // namespace bnnk

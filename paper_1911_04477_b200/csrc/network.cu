@@ -87,7 +87,7 @@ struct FusedStage {
     FusedGeom g{};               // batch-independent fields
     int Dpad = 0, Kpad = 0;
     DevBuf w8, prm;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
-    CUtensorMap tm[4];           // weight tile maps for BN = 32, 64, 128, 256
+    CUtensorMap tm[5];           // weight tile maps, box rows 16, 32, 64, 128, 256 (= BN / cta_group)
     size_t out_words_per_image = 0;
 };
 
@@ -307,8 +307,8 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
                                   aff ? aff->scale.as<float>() : nullptr, aff ? aff->shift.as<float>() : nullptr,
                                   st->prm.as<int4>(), bad.as<int>(), s));
         g.prm = st->prm.as<int4>();
-        const int bns[4] = {32, 64, 128, 256};
-        for (int b = 0; b < 4; ++b)
+        const int bns[5] = {16, 32, 64, 128, 256};
+        for (int b = 0; b < 5; ++b)
             BNN_TRY(fused_make_tmap(&st->tm[b], st->w8.as<int8_t>(), st->Dpad, st->Kpad, bns[b]));
         if (st->epi == FEPI_BITS) {
             const size_t pos = kind == BNN_LAYER_CONV ? size_t(g.OH) * g.OW / (pool ? 4 : 1) : 1;
@@ -327,16 +327,28 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
     return BNN_OK;
 }
 
-int choose_bn(int D, int m_tiles) {
-    static const int forced = getenv("BNN_FUSED_BN") ? atoi(getenv("BNN_FUSED_BN")) : 0;  // experiments
-    if (forced == 32 || forced == 64 || forced == 128 || forced == 256) return forced;
-    int bn = 32;
+// Tile shape for a launch: cta_group (1: M=128 per CTA, 2: M=256 per CTA pair) and BN (the
+// MMA N, weight rows per tile): the widest BN that still gives every CTA (pair) a tile.
+int g_forced_cg = -1, g_forced_bn = -1;  // bnn_set_fused_tiling (tests, experiments); -1: from env
+
+void choose_tile(int D, size_t rows, int& cg, int& bn) {
+    if (g_forced_cg < 0) g_forced_cg = getenv("BNN_FUSED_CG") ? atoi(getenv("BNN_FUSED_CG")) : 0;
+    if (g_forced_bn < 0) g_forced_bn = getenv("BNN_FUSED_BN") ? atoi(getenv("BNN_FUSED_BN")) : 0;
+    const int forced_cg = g_forced_cg, forced_bn = g_forced_bn;
+    const size_t units2 = size_t(num_sms()) / 2;
+    // CTA pairs measured no faster than single CTAs here (the i8 MMA runs ~128 cycles per
+    // instruction for any N <= 256 in both modes, and shared-memory bandwidth bounds both;
+    // profiles/r01_fused_cg_modes.log), so pairs are opt-in.
+    (void)units2;
+    cg = forced_cg == 1 || forced_cg == 2 ? forced_cg : 1;
+    const size_t m_tiles = ceil_div(rows, size_t(128 * cg)), units = size_t(num_sms()) / cg;
+    bn = 32;
     while (bn < 256 && bn < D) bn *= 2;
-    while (bn > 32 && size_t(m_tiles) * ceil_div(size_t(D), size_t(bn)) < size_t(num_sms())) bn /= 2;
-    return bn;
+    while (bn > 32 && m_tiles * ceil_div(size_t(D), size_t(bn)) < units) bn /= 2;
+    if (forced_bn == 32 || forced_bn == 64 || forced_bn == 128 || forced_bn == 256) bn = forced_bn;
 }
 
-int bn_index(int bn) { return bn == 32 ? 0 : bn == 64 ? 1 : bn == 128 ? 2 : 3; }
+int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : box == 128 ? 3 : 4; }
 
 int ensure_arena(bnn_net* net, size_t batch) {
     if (net->arena_batch >= batch) return BNN_OK;
@@ -480,8 +492,8 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         g.B = int(B);
         g.in = in;
         g.rows = int(rows);
-        const int m_tiles = int(ceil_div(rows, 128));
-        const int bn = choose_bn(g.D, m_tiles);
+        int cg = 1, bn = 32;
+        choose_tile(g.D, rows, cg, bn);
         g.n_tiles = int(ceil_div(size_t(g.D), size_t(bn)));
         if (st.epi == FEPI_BITS) {
             g.out_bits = net->bits[which].as<uint32_t>();
@@ -497,7 +509,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             ++launches;
         }
         EventPair gemm_ev(net, st.layer, 1, s);
-        BNN_TRY(launch_fused(bn, st.in_mode, st.epi, st.tm[bn_index(bn)], g, s));
+        BNN_TRY(launch_fused(cg, bn, st.in_mode, st.epi, st.tm[box_index(bn / cg)], g, s));
         gemm_ev.close();
         layer_ev.close();
         ++launches;
@@ -600,6 +612,14 @@ int bnn_net_set_engine(bnn_net* net, int policy) {
     if (policy == BNN_ENGINE_FUSED && !net->fusable)
         return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
     net->engine_policy = policy;
+    return BNN_OK;
+}
+
+int bnn_set_fused_tiling(int cta_group, int bn) {
+    if ((cta_group != 0 && cta_group != 1 && cta_group != 2) ||
+        (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256))
+        return fail(BNN_E_CONFIG, "fused tiling: cta_group in {0,1,2}, bn in {0,32,64,128,256}");
+    g_forced_cg = cta_group, g_forced_bn = bn;
     return BNN_OK;
 }
 

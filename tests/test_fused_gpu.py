@@ -43,8 +43,17 @@ FUSABLE = {
 }
 
 
+@pytest.fixture(params=["auto", "cg1", "cg2"])
+def tiling(bnn, request):
+    """Every fused test runs with the automatic tile choice and with each cta_group forced."""
+    lib = bnn.load()
+    bnn._lib.check(lib.bnn_set_fused_tiling({"auto": 0, "cg1": 1, "cg2": 2}[request.param], 0))
+    yield request.param
+    lib.bnn_set_fused_tiling(0, 0)
+
+
 @pytest.fixture
-def fused(bnn):
+def fused(bnn, tiling):
     def mk(spec=None, seed=1):
         net = bnn.Network(seed=seed) if spec is None else _net(bnn, spec)
         net.set_engine("fused")
@@ -60,6 +69,21 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, batch):
     got = net.forward(x)
     assert net.last_launches() == 10  # first-layer pixel encoder + one launch per weighted layer
     assert np.array_equal(got, orc.net(seed=1).forward(x))
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+def test_forced_tile_shapes_vs_oracle(bnn, orc, cg, bn):
+    lib = bnn.load()
+    net = bnn.Network(seed=1)
+    net.set_engine("fused")
+    x = orc.fill_random((9, 3, 32, 32), orc.mix64(2, INPUT_STREAM))
+    try:
+        bnn._lib.check(lib.bnn_set_fused_tiling(cg, bn))
+        got = net.forward(x)
+    finally:
+        lib.bnn_set_fused_tiling(0, 0)
+    assert np.array_equal(got, orc.net(seed=1).forward(x)), (cg, bn)
 
 
 def test_default_network_fused_equals_generic_large_batch(bnn, orc, fused):
