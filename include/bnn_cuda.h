@@ -7,7 +7,7 @@
  *   bnn_*        device pointers, stream-ordered (enqueue only; no host sync unless
  *                the function says so). Used by the network engine and the benchmark.
  *   bnn_host_*   host pointers with the reference's exact semantics: H2D copy, kernel,
- *                D2H copy, synchronous. include/bnn/*.hpp re-exposes these under the
+ *                D2H copy, synchronous. include/bnn_b200.hpp re-exposes these under the
  *                reference C++ signatures.
  *
  * Conventions
@@ -135,6 +135,10 @@ int bnn_maxpool2_f32(const float* x, size_t B, size_t C, size_t H, size_t W, flo
  * ([features, batch]): plane = batch, channels = features. */
 int bnn_affine_f32(const float* x, size_t n, size_t channels, size_t plane, const float* scale,
                    const float* shift, float* out, bnn_stream_t s);
+/* to_float (kernels.cpp:90-95): out[i] = (float)a[i]. */
+int bnn_to_float_s32(const int32_t* a, size_t n, float* out, bnn_stream_t s);
+/* bias_add (kernels.cpp:97-107), in place: a[d*cols + j] += bias[d]. */
+int bnn_bias_add_f32(float* a, size_t rows, size_t cols, const float* bias, bnn_stream_t s);
 /* flatten_to_columns (network.cpp:177-184): [B, F] -> [F, B]. */
 int bnn_flatten_to_columns_f32(const float* x, size_t B, size_t F, float* out, bnn_stream_t s);
 /* fill_random (tensor.cpp:65-96): out[i] = unit_random(seed, offset + i). Bit-identical to

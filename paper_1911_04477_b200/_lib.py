@@ -85,6 +85,8 @@ _SIGS = {
     "bnn_maxpool2_f32": (_I, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
     "bnn_affine_f32": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "bnn_flatten_to_columns_f32": (_I, [_P, _SZ, _SZ, _P, _P]),
+    "bnn_to_float_s32": (_I, [_P, _SZ, _P, _P]),
+    "bnn_bias_add_f32": (_I, [_P, _SZ, _SZ, _P, _P]),
     "bnn_fill_random_f32": (_I, [_U64, _U64, _SZ, _P, _P]),
     "bnn_mix64": (_U64, [_U64, _U64]),
     "bnn_fnv1a_f32": (_I, [_P, _SZ, C.POINTER(_U64), _P]),

@@ -49,6 +49,21 @@ __global__ void affine_kernel(const float* __restrict__ x, size_t n, size_t chan
     }
 }
 
+// to_float (kernels.cpp:90-95): exact int32 -> float conversion (round to nearest).
+__global__ void to_float_kernel(const int32_t* __restrict__ a, size_t n, float* __restrict__ out) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        out[i] = __int2float_rn(a[i]);
+}
+
+// bias_add (kernels.cpp:97-107): a[d, j] += bias[d], one rounding per element.
+__global__ void bias_add_kernel(float* __restrict__ a, size_t rows, size_t cols, const float* __restrict__ bias) {
+    const size_t n = rows * cols;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        a[i] = __fadd_rn(a[i], bias[i / cols]);
+}
+
 __global__ void transpose_kernel(const float* __restrict__ x, size_t rows, size_t cols,
                                  float* __restrict__ out) {
     __shared__ float tile[32][33];
@@ -133,6 +148,20 @@ int bnn_affine_f32(const float* x, size_t n, size_t channels, size_t plane, cons
     BNN_TRY(require_sm100());
     if (channels == 0 || plane == 0) return fail(BNN_E_SHAPE, "affine_norm: empty parameters");
     return launch_affine(x, n, channels, plane, scale, shift, out, S(s));
+}
+
+int bnn_to_float_s32(const int32_t* a, size_t n, float* out, bnn_stream_t s) {
+    BNN_TRY(require_sm100());
+    if (n == 0) return BNN_OK;
+    to_float_kernel<<<grid_for(n, 256), 256, 0, S(s)>>>(a, n, out);
+    return launch_check("to_float_kernel");
+}
+
+int bnn_bias_add_f32(float* a, size_t rows, size_t cols, const float* bias, bnn_stream_t s) {
+    BNN_TRY(require_sm100());
+    if (rows * cols == 0) return BNN_OK;
+    bias_add_kernel<<<grid_for(rows * cols, 256), 256, 0, S(s)>>>(a, rows, cols, bias);
+    return launch_check("bias_add_kernel");
 }
 
 int bnn_flatten_to_columns_f32(const float* x, size_t B, size_t F, float* out, bnn_stream_t s) {
