@@ -3,16 +3,20 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
 
 Workload (BASELINE.json configs[2], the images/sec half of the headline metric): the
-reference's default network (build_default_network, network.cpp:422-465; 6 binary 3x3 convs
-128/128p/256/256p/512/512p + binary FC 1024/1024/10, affine-htanh-sign between layers), seed 1,
-synthetic 32x32x3 input from the reference generator (fill_random with the bench stream,
-bench.cpp:68-78), batch B per GPU (default 256). A step = one full network_forward of one
-batch. Multi-GPU (torchrun): each rank runs its contiguous batch shard independently with
-replicated packed weights; the only collective is the final NCCL logits gather.
+reference's default network (build_default_network, network.cpp:422-465: six binary 3x3 convs
+128/128p/256/256p/512/512p + binary FC 1024/1024/10 with affine-htanh-sign between layers),
+seed 1, synthetic 32x32x3 input from the reference generator (fill_random with the bench
+input stream, bench.cpp:68-78), batch B per GPU (default 256). A step = one full
+network_forward of one batch through the fused engine (one tcgen05 launch per weighted layer,
+replayed as a CUDA graph). Multi-GPU (torchrun): each rank runs its contiguous batch shard
+independently with replicated packed weights; the only collective is the final NCCL logits
+gather.
 
 Timing: W warm-up steps, then K steps bracketed by barrier + cuda.synchronize; each step is
-timed with CUDA events on the launching stream and L2 is flushed between steps (a 256 MiB
-write, outside the events); value = images over the MAX over ranks of the summed step times.
+timed with CUDA events on the launching stream, L2 is flushed before every step (a 256 MiB
+write, outside the events); value = images of all ranks / the MAX over ranks of the summed
+step times. A second, separately timed pass records per-layer CUDA events for the breakdown
+and the dominant kernel's per-launch time (roofline).
 
 --impl reference: the UNMODIFIED reference CPU implementation (oracle/_ref, compiled from
 /root/reference/proj) on this host's cores, rank 0 only, a bounded sample per step.
@@ -34,111 +38,134 @@ sys.path.insert(0, ROOT)
 INPUT_STREAM = 0x696E707574  # bench.cpp:76-77
 IMG = 3 * 32 * 32
 L2_FLUSH_BYTES = 256 << 20
+METRIC = "BNN CIFAR-10 (VGG-small, binary conv/FC) inference images/sec"
+WORKLOAD = "cfg3 BNN VGG-small CIFAR-10 forward (BASELINE.json configs[2]), all binary conv/FC layers"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=256, help="images per GPU per step")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep", default="1,64,1024,4096,16384", help="batch sweep (N=1 only)")
     return ap.parse_args()
 
 
 def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 # ------------------------------------------------------------------------ clocks
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
-
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled (NVML, every 5 ms) while the timed region runs."""
 
     def __init__(self, index: int):
-        self.index, self.proc, self.lines = index, None, []
+        self.index, self.samples, self.reasons, self.stop_ev = index, [], set(), threading.Event()
+        self.smax, self.err = None, None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml as nv
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as e:  # no NVML: record why
+            self.err = f"nvml unavailable: {e}"
+
+    def _run(self):
+        nv = self.nv
+        names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                 nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, n in names.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            parts = [p.strip() for p in l.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.err:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": [self.err]}
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.smax,
+                "samples": len(self.samples), "reasons": sorted(self.reasons), "source": "nvml, 5 ms"}
 
 
 # ------------------------------------------------------------------ CPU baseline
 
 
 def cpu_reference_rate(seconds: float, seed: int):
-    """Time the UNMODIFIED reference network_forward(Binary) on this host's cores.
-
-    Batch-sharded over all host threads (the reference is re-entrant); each
-    thread runs network_forward on its slice with the reference's threads = 1 GEMM setting.
-    Returns (images/s, cores, kind, sample description).
-    """
+    """The UNMODIFIED reference network_forward(Binary) on this host's cores (batch-sharded over
+    all host threads; the reference is re-entrant; threads = 1 GEMM setting)."""
     from oracle import RefLib
 
     ref = RefLib()
     net = ref.net_default(seed)
     cores = os.cpu_count() or 1
-    # calibrate with one image per core, then size the sample to ~`seconds`
     x = ref.fill_random((cores, 3, 32, 32), ref.mix64(seed, INPUT_STREAM))
     t0 = time.perf_counter()
     net.forward(x, batch_threads=cores)
-    per_round = time.perf_counter() - t0
-    rounds = max(1, int(seconds / max(per_round, 1e-3)))
+    rounds = max(1, int(seconds / max(time.perf_counter() - t0, 1e-3)))
     n = cores * rounds
     x = ref.fill_random((n, 3, 32, 32), ref.mix64(seed, INPUT_STREAM))
     t0 = time.perf_counter()
     net.forward(x, batch_threads=cores)
     dt = time.perf_counter() - t0
-    return n / dt, cores, f"reference-{ref.isa}", f"{n} images of the same network/input stream"
+    return n / dt, cores, ref.isa, f"{n} images of the same network and input stream"
+
+
+# ------------------------------------------------------------------ peaks
+
+
+def int8_tensor_peak(dev):
+    """Measured dense int8 tensor throughput on this GPU at this moment: cuBLASLt int8 GEMM
+    (torch._int_mm) 8192^3, best of 10, TOPS (2 ops per MAC). Fallback: 2x the driver-measured
+    bf16 cuBLAS burst figure (B200 dense int8 : bf16 = 2 : 1)."""
+    import torch
+
+    try:
+        n = 8192
+        a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=dev)
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * n ** 3 / (best * 1e-3) / 1e12, "measured: cuBLASLt int8 GEMM 8192^3 (torch._int_mm), best of 10"
+    except Exception as e:
+        try:
+            pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            return 2 * pk["bf16_tflops"], f"2 x MEASURED_PEAKS bf16_tflops (int8 GEMM probe failed: {e})"
+        except Exception:
+            return 2 * 1590.0, "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------------- ours
@@ -161,46 +188,48 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     lib = bnn.load()
     B = args.batch
-    stream = torch.cuda.current_stream().cuda_stream
+    st = torch.cuda.Stream(device=dev)
+    S = st.cuda_stream
 
     net = bnn.Network(seed=args.seed)
+    engine = net.engine
     n_layers = len(net.layers)
-    # this rank's shard of the global synthetic batch, generated on device at its global offset
+    # this rank's shard of the global synthetic batch (weak scaling: B per GPU), generated on the
+    # device at its global element offset (paper_1911_04477_b200/shard.py)
+    from paper_1911_04477_b200.shard import input_offset, shard_range
+
+    assert shard_range(B * world, world, rank)[1] == B
     x = torch.empty((B, 3, 32, 32), dtype=torch.float32, device=dev)
-    _lib.check(lib.bnn_fill_random_f32(bnn.mix64(args.seed, INPUT_STREAM), rank * B * IMG, B * IMG,
-                                       x.data_ptr(), stream))
+    _lib.check(lib.bnn_fill_random_f32(bnn.mix64(args.seed, INPUT_STREAM), input_offset(B * world, world, rank),
+                                       B * IMG, x.data_ptr(), S))
     logits = torch.empty((net.logits, B), dtype=torch.float32, device=dev)
     gathered = torch.empty((world, net.logits, B), dtype=torch.float32, device=dev) if world > 1 else None
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step():
-        net.forward_device(x, logits, stream)
-        if world > 1:  # the only collective: final logits gather (NCCL)
+        net.forward_device(x, logits, S)
+        if world > 1:  # the only collective: the final logits gather (NCCL)
             dist.all_gather_into_tensor(gathered, logits)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    lib.bnn_net_set_timing(net.handle, 1)
-    lib.bnn_net_reset_timing(net.handle)
-    clocks = ClockSampler(local)
-    clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.fill_(float(i))  # > L2 (126 MB): every step starts cold
-        ev[i][0].record()
-        step()
-        ev[i][1].record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    lib.bnn_net_set_timing(net.handle, 0)
+    with torch.cuda.stream(st):
+        for _ in range(max(args.warmup, 3)):
+            step()
+        st.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        clocks = ClockSampler(local)
+        clocks.start()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # > L2 (126 MB): every step starts cold
+            ev[i][0].record(st)
+            step()
+            ev[i][1].record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if world > 1:
@@ -208,8 +237,19 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     launches_per_step = net.last_launches()
+    images = world * B * args.steps
+    value = images / (total_ms * 1e-3)
 
-    # per-layer + dominant-GEMM timing, recorded live inside the timed steps
+    # ---- separately timed pass: per-layer events (breakdown + the dominant kernel's launch time)
+    lib.bnn_net_set_timing(net.handle, 1)
+    lib.bnn_net_reset_timing(net.handle)
+    prof_steps = max(5, min(args.steps, 20))
+    with torch.cuda.stream(st):
+        for i in range(prof_steps):
+            flush.fill_(float(i))
+            net.forward_device(x, logits, S)
+        st.synchronize()
+    lib.bnn_net_set_timing(net.handle, 0)
     layer_ms = (C.c_double * n_layers)()
     gemm_ms = (C.c_double * n_layers)()
     gemm_n = (C.c_size_t * n_layers)()
@@ -219,67 +259,81 @@ def run_ours(args):
         sh = (C.c_size_t * 8)()
         _lib.check(lib.bnn_net_layer_shape(net.handle, i, sh))
         shapes.append(list(sh))
-    bops = []
-    for i, sh in enumerate(shapes):
-        cols = sh[3] * B
-        bops.append(2.0 * sh[1] * sh[2] * cols if sh[3] else 0.0)
+    # algorithmic work per weighted layer and batch: 2*M*K*N int8 tensor ops (1 MAC per bit-MAC;
+    # = the bops of SURVEY.md §8(d): 1.2339 G per image for the whole network)
+    ops = [2.0 * sh[1] * sh[2] * sh[3] * B if sh[3] else 0.0 for sh in shapes]
     top = max(range(n_layers), key=lambda i: gemm_ms[i])
     per_launch_ms = gemm_ms[top] / max(1, gemm_n[top])
-    achieved_tops = bops[top] / (per_launch_ms * 1e-3) / 1e12
-
-    # chosen pipe's peak at this run's clocks (microbenchmark)
-    peak, pms = C.c_double(), C.c_double()
-    _lib.check(lib.bnn_probe_popc_peak(C.byref(peak), C.byref(pms), stream))
-    bpeak = C.c_double()
-    _lib.check(lib.bnn_probe_bmma_peak(C.byref(bpeak), C.byref(pms), stream))
-    kernel_name = lib.bnn_last_gemm_kernel().decode()
-    peak_tops = peak.value / 1e12
-
+    achieved = ops[top] / (per_launch_ms * 1e-3) / 1e12
+    step_prof_ms = sum(layer_ms[i] for i in range(n_layers)) / prof_steps
+    peak, peak_src = int8_tensor_peak(dev) if rank == 0 else (None, None)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(kernel_name, {}).get(f"layer{top}")
+            traffic = json.load(open(tpath)).get(f"b{B}", {}).get(f"layer{top}")
         except (ValueError, OSError):
             traffic = None
+    kernel_name = lib.bnn_last_gemm_kernel().decode()
 
-    images = world * B * args.steps
-    value = images / (total_ms * 1e-3)
-    total_bops = sum(bops) * world
-
-    # ---- end to end through the public API: pinned host input -> H2D -> forward -> D2H
+    # ---- end to end through the public API: pinned host input -> H2D -> forward -> D2H logits
     e2e = None
     if not args.no_e2e:
         hx = x.cpu().pin_memory()
-        hy = torch.empty((net.logits, B), dtype=torch.float32).pin_memory()
+        hy = torch.empty((world if world > 1 else 1, net.logits, B), dtype=torch.float32).pin_memory()
         dx = torch.empty_like(x)
-        for _ in range(2):
-            dx.copy_(hx, non_blocking=True)
-            net.forward_device(dx, logits, stream)
-            hy.copy_(logits, non_blocking=True)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            dx.copy_(hx, non_blocking=True)
-            net.forward_device(dx, logits, stream)
+        with torch.cuda.stream(st):
+            def e2e_step():
+                dx.copy_(hx, non_blocking=True)
+                net.forward_device(dx, logits, S)
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered, logits)
+                    hy.copy_(gathered, non_blocking=True)
+                else:
+                    hy[0].copy_(logits, non_blocking=True)
+                st.synchronize()  # the step's result is on the host
+
+            for _ in range(3):
+                e2e_step()
             if world > 1:
-                dist.all_gather_into_tensor(gathered, logits)
-                hy_all = gathered.cpu() if rank == 0 else None  # noqa: F841
-            else:
-                hy.copy_(logits, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        e2e_s = time.perf_counter() - t0
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                e2e_step()
+            e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": B * IMG * 4,
-               "d2h_bytes_per_step": net.logits * B * 4 * (world if world > 1 else 1),
-               "timer": "host wall clock around synchronous steps, max over ranks"}
+               "d2h_bytes_per_step": net.logits * B * 4 * world,
+               "timer": "host clock around K synchronous steps (pinned H2D + forward + D2H), max over ranks"}
 
-    # correctness spot-check of this run's logits against the oracle (first 4 images)
+    # ---- batch sweep (BASELINE.json configs[4]), N=1: images/s at each per-GPU batch
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = {}
+        for b in [int(v) for v in args.sweep.split(",") if v]:
+            xb = torch.empty((b, 3, 32, 32), dtype=torch.float32, device=dev)
+            _lib.check(lib.bnn_fill_random_f32(bnn.mix64(args.seed, INPUT_STREAM), 0, b * IMG, xb.data_ptr(), S))
+            yb = torch.empty((net.logits, b), dtype=torch.float32, device=dev)
+            n_it = 10 if b >= 1024 else 30
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    net.forward_device(xb, yb, S)
+                tot = 0.0
+                for i in range(n_it):
+                    flush.fill_(float(i))
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    net.forward_device(xb, yb, S)
+                    e1.record(st)
+                    st.synchronize()
+                    tot += e0.elapsed_time(e1)
+            sweep[str(b)] = round(b * n_it / (tot * 1e-3), 1)
+            del xb, yb
+
+    # ---- correctness spot-check of this run's network against the oracle (first 4 images)
     parity = None
     if rank == 0:
         try:
@@ -287,24 +341,23 @@ def run_ours(args):
 
             orc = Oracle()
             xs = orc.fill_random((4, 3, 32, 32), orc.mix64(args.seed, INPUT_STREAM))
-            got = net.forward(xs)
-            parity = bool(np.array_equal(got, orc.net(seed=args.seed).forward(xs)))
+            parity = bool(np.array_equal(net.forward(xs), orc.net(seed=args.seed).forward(xs)))
         except Exception as e:  # the checker must never break the benchmark line
             parity = f"oracle unavailable: {e}"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, kind, sample = cpu_reference_rate(args.cpu_seconds, args.seed)
-            cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "reference",
-                   "sample": sample, "build": kind}
+            v, cores, isa, sample = cpu_reference_rate(args.cpu_seconds, args.seed)
+            cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "reference", "sample": sample,
+                   "build": f"oracle/_ref/libbnnref_{isa}.so (unmodified reference, -O3 -march={isa})"}
         except Exception as e:
-            cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+            cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
+        net_ops = sum(ops)
         line = {
-            "metric": "BNN CIFAR-10 (VGG-small, binary conv/FC) inference images/sec",
+            "metric": METRIC,
             "value": value,
             "unit": "images/s",
             "n_gpus": world,
@@ -314,28 +367,30 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "u32 packed bits (popcount int32 accumulate), f32 epilogue",
-            "data": "synthetic: reference fill_random input stream, seed-derived weights",
-            "config": {"workload": "cfg3 BNN VGG-small CIFAR-10 forward (BASELINE.json configs[2])",
-                       "batch_per_gpu": B, "global_batch": B * world,
-                       "parallelism": f"dp{world} batch shards, replicated packed weights, "
-                                      "NCCL logits gather",
-                       "l2": "flushed between steps (256 MiB write outside the step events)",
-                       "binary_tops": total_bops * args.steps / (total_ms * 1e-3) / 1e12},
+            "dtype": "binary (+-1 bits; int8 tensor-core MMA, int32 accumulate), f32 logits",
+            "data": "synthetic: reference fill_random input stream (seed 1), seed-derived weights",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+                       "parallelism": f"dp{world}: batch shards, replicated packed weights, NCCL logits gather",
+                       "engine": engine, "l2": "flushed before every step (256 MiB write outside the events)",
+                       "binary_tops": net_ops * world * args.steps / (total_ms * 1e-3) / 1e12},
             "gpu_launches": launches_per_step * args.steps,
-            "roofline": {"bound": "int-pipe (POPC)", "achieved": achieved_tops, "peak": peak_tops,
-                         "unit": "T bops/s", "frac": achieved_tops / peak_tops, "traffic": traffic,
-                         "kernel": f"xnor_gemm_{kernel_name} (layer {top}: M={shapes[top][1]} "
-                                   f"K={shapes[top][2]} N={shapes[top][3] * B})",
-                         "per_launch_ms": per_launch_ms,
-                         "peak_source": "bnn_probe_popc_peak microbenchmark at this run's clocks",
-                         "bmma_emulated_peak": bpeak.value / 1e12,
-                         "kernel_share_of_step": gemm_ms[top] / total_ms if world == 1 else None},
-            "layers_ms_per_step": {f"{i}:{net.layers[i]['kind']}": round(layer_ms[i] / args.steps, 4)
+            "roofline": {
+                "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": f"{kernel_name} layer {top} ({net.layers[top]['kind']}: M={shapes[top][1]} "
+                          f"K={shapes[top][2]} N={shapes[top][3] * B})",
+                "per_launch_ms": per_launch_ms,
+                "work_per_launch": f"2*M*K*N = {ops[top]:.4g} int8 tensor ops (1 MAC per bit-MAC)",
+                "peak_source": peak_src,
+                "kernel_share_of_step": gemm_ms[top] / prof_steps / step_prof_ms if step_prof_ms else None,
+                "network_frac": (net_ops / (step_prof_ms * 1e-3) / 1e12) / peak if peak and step_prof_ms else None,
+            },
+            "layers_ms_per_step": {f"{i}:{net.layers[i]['kind']}": round(layer_ms[i] / prof_steps, 4)
                                    for i in range(n_layers) if layer_ms[i] > 0},
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "batch_sweep_images_per_s": sweep,
             "parity_vs_oracle": parity,
         }
         print(json.dumps(line), flush=True)
@@ -355,8 +410,7 @@ def run_reference(args):
     ref = RefLib()
     net = ref.net_default(args.seed)
     cores = os.cpu_count() or 1
-    # bounded sample per step: one image per host thread (the whole run stays within minutes)
-    per_step = cores
+    per_step = cores  # bounded sample per step: one image per host thread
     x = ref.fill_random((per_step, 3, 32, 32), ref.mix64(args.seed, INPUT_STREAM))
     for _ in range(args.warmup):
         net.forward(x, batch_threads=cores)
@@ -367,30 +421,19 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = per_step * args.steps / total
-    line = {
-        "impl": "reference",
-        "metric": "BNN CIFAR-10 (VGG-small, binary conv/FC) inference images/sec",
-        "value": value,
-        "unit": "images/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "u32 packed bits (popcount), f32 epilogue",
-        "data": "synthetic: reference fill_random input stream, seed-derived weights",
-        "config": {"workload": "cfg3 BNN VGG-small CIFAR-10 forward (BASELINE.json configs[2])",
-                   "batch_per_gpu": args.batch, "global_batch": args.batch * world,
-                   "parallelism": "CPU: batch shards over host threads",
-                   "sample_images_per_step": per_step},
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "binary (+-1 bits, popcount), f32 epilogue",
+        "data": "synthetic: reference fill_random input stream (seed 1), seed-derived weights",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                   "parallelism": "CPU: batch shards over host threads", "sample_images_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "reference",
                          "sample": f"{per_step} images per step (bounded sample of the batch), "
-                                   f"oracle/_ref libbnnref_{ref.isa}.so"},
+                                   f"oracle/_ref/libbnnref_{ref.isa}.so"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    }), flush=True)
 
 
 def main():

@@ -203,6 +203,10 @@ int bnn_net_set_engine(bnn_net* net, int policy);
  * per CTA) or 2 (CTA pairs, M=256, tcgen05 cta_group::2), bn = MMA N in {32,64,128,256};
  * 0 = automatic (the default). */
 int bnn_set_fused_tiling(int cta_group, int bn);
+/* CUDA-graph replay of the fused forward for a repeated (x, batch, logits, stream) on a
+ * non-default stream (default on). The first call runs eagerly, the second captures, later
+ * calls replay the graph. */
+int bnn_net_set_graphs(bnn_net* net, int enabled);
 /* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
 int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */

@@ -116,6 +116,16 @@ struct bnn_net {
     bool fusable = false;
     std::string unfusable_why;
     std::vector<std::unique_ptr<bnnk::FusedStage>> stages;
+    bool use_graphs = true;
+    struct Graph {
+        const float* x = nullptr;
+        size_t B = 0;
+        float* logits = nullptr;
+        cudaStream_t s = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        size_t launches = 0;
+        int epoch = 0;
+    } graph;
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix;
@@ -330,6 +340,7 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
 // Tile shape for a launch: cta_group (1: M=128 per CTA, 2: M=256 per CTA pair) and BN (the
 // MMA N, weight rows per tile): the widest BN that still gives every CTA (pair) a tile.
 int g_forced_cg = -1, g_forced_bn = -1;  // bnn_set_fused_tiling (tests, experiments); -1: from env
+int g_tiling_epoch = 0;                   // bumped by bnn_set_fused_tiling: invalidates captured graphs
 
 void choose_tile(int D, size_t rows, int& cg, int& bn) {
     if (g_forced_cg < 0) g_forced_cg = getenv("BNN_FUSED_CG") ? atoi(getenv("BNN_FUSED_CG")) : 0;
@@ -523,9 +534,51 @@ bool use_fused(const bnn_net* net) {
     return net->fusable && net->engine_policy != BNN_ENGINE_GENERIC;
 }
 
+// The fused forward is a fixed sequence of ~10 launches; for a repeated (x, B, logits, stream)
+// it is captured once into a CUDA graph and replayed (one launch from the host). Not used
+// with per-layer timing (events), the profiling mode, or the legacy default stream (which
+// cannot be captured).
+int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
+    const bool graphable = net->use_graphs && !net->timing && !prof && s != nullptr;
+    if (!graphable) return forward_fused(net, x, B, logits, s);
+    bnn_net::Graph& gc = net->graph;
+    if (gc.epoch != g_tiling_epoch) {
+        if (gc.exec) cudaGraphExecDestroy(gc.exec);
+        gc = bnn_net::Graph{};
+        gc.epoch = g_tiling_epoch;
+    }
+    if (gc.exec && gc.x == x && gc.B == B && gc.logits == logits && gc.s == s) {
+        BNN_CUDA(cudaGraphLaunch(gc.exec, s));
+        net->last_launches = gc.launches;
+        return BNN_OK;
+    }
+    if (!(gc.x == x && gc.B == B && gc.logits == logits && gc.s == s)) {
+        // first sighting: run eagerly (sizes the arena, sets kernel attributes), remember the key
+        gc.x = x, gc.B = B, gc.logits = logits, gc.s = s;
+        if (gc.exec) cudaGraphExecDestroy(gc.exec), gc.exec = nullptr;
+        return forward_fused(net, x, B, logits, s);
+    }
+    cudaGraph_t graph = nullptr;
+    BNN_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = forward_fused(net, x, B, logits, s);
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (rc != BNN_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    BNN_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&gc.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    BNN_CUDA(ie);
+    gc.launches = net->last_launches;
+    BNN_CUDA(cudaGraphLaunch(gc.exec, s));
+    return BNN_OK;
+}
+
 int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
-    if (use_fused(net)) return forward_fused(net, x, B, logits, s);
+    if (use_fused(net)) return forward_graphed(net, x, B, logits, s);
     return forward_generic(net, x, B, logits, s);
 }
 }  // namespace
@@ -602,6 +655,7 @@ void bnn_net_destroy(bnn_net* net) {
         cudaEventDestroy(p.b);
     }
     for (auto e : net->pool) cudaEventDestroy(e);
+    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
     delete net;
 }
 size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
@@ -612,6 +666,8 @@ int bnn_net_set_engine(bnn_net* net, int policy) {
     if (policy == BNN_ENGINE_FUSED && !net->fusable)
         return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
     net->engine_policy = policy;
+    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
+    net->graph = bnn_net::Graph{};
     return BNN_OK;
 }
 
@@ -620,6 +676,14 @@ int bnn_set_fused_tiling(int cta_group, int bn) {
         (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256))
         return fail(BNN_E_CONFIG, "fused tiling: cta_group in {0,1,2}, bn in {0,32,64,128,256}");
     g_forced_cg = cta_group, g_forced_bn = bn;
+    ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_net_set_graphs(bnn_net* net, int enabled) {
+    net->use_graphs = enabled != 0;
+    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
+    net->graph = bnn_net::Graph{};
     return BNN_OK;
 }
 

@@ -124,3 +124,25 @@ def test_unfusable_topology_uses_generic_engine(bnn, orc):
         net.set_engine("fused")
     x = orc.fill_random((3, 4, 12, 12), 5)
     assert np.array_equal(net.forward(x), _oracle(orc, spec).forward(x))
+
+
+def test_graph_replay_matches_eager(bnn, orc):
+    """Repeated forwards on a side stream are captured into a CUDA graph and replayed; the
+    replayed logits must equal the eager ones and the oracle's, also after the input changes."""
+    torch = pytest.importorskip("torch")
+    net = bnn.Network(seed=6)
+    st = torch.cuda.Stream()
+    x = torch.from_numpy(orc.fill_random((37, 3, 32, 32), 77)).cuda()
+    out = torch.empty((10, 37), device="cuda")
+    want = orc.net(seed=6).forward(x.cpu().numpy())
+    with torch.cuda.stream(st):
+        for _ in range(4):  # eager, capture, replay, replay
+            out.zero_()
+            net.forward_device(x, out, st.cuda_stream)
+            st.synchronize()
+            assert np.array_equal(out.cpu().numpy(), want)
+        x2 = torch.from_numpy(orc.fill_random((37, 3, 32, 32), 78)).cuda()
+        x.copy_(x2)  # same buffer, new contents: the replayed graph reads them
+        net.forward_device(x, out, st.cuda_stream)
+        st.synchronize()
+    assert np.array_equal(out.cpu().numpy(), orc.net(seed=6).forward(x2.cpu().numpy()))
