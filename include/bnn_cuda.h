@@ -207,6 +207,9 @@ int bnn_set_fused_tiling(int cta_group, int bn);
  * non-default stream (default on). The first call runs eagerly, the second captures, later
  * calls replay the graph. */
 int bnn_net_set_graphs(bnn_net* net, int enabled);
+/* Fused engine: keep the activation operand in TMEM (tcgen05.st + the TS-form MMA, default 1)
+ * or stage it in shared memory (0). Process-wide; both are bit-exact. */
+int bnn_set_fused_tmem_a(int enabled);
 /* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
 int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */

@@ -56,18 +56,20 @@ namespace {
 
 constexpr int kStages = 4;   // CG = 1: A 16 KB + B up to 32 KB per stage
 constexpr int kStages2 = 6;  // CG = 2: A 16 KB + B up to 16 KB per stage (per CTA)
-constexpr int kThreads = 320;  // 10 warps: TMA, MMA, 4 epilogue, 4 producer
+constexpr int kThreads = 448;  // 14 warps: TMA, MMA, 4+4 epilogue (2-5, 10-13), 4 producer (6-9)
 constexpr int kRows = 128;   // UMMA M
 constexpr int kKB = 128;     // K bytes per stage
 
 constexpr int kMaxF32K = 1024;  // float-input layers: K <= this (im2col offset table in smem)
 constexpr int kMaxQ = 1024;     // K words per layer (bits mode), entries of the offset table
+constexpr int kMaxD = 2048;     // output channels of a bits-epilogue launch (threshold table)
 constexpr int kMaxPixTaps = 16; // pixel-packed first layer: taps (and taps*C <= 64)
 
-template <int BN, int CG>
+template <int BN, int CG, int ATM>
 constexpr size_t fused_smem() {
     static_assert(kMaxF32K <= kMaxQ, "one table region");
-    return 1024 + size_t(CG == 2 ? kStages2 : kStages) * (kRows + BN / CG) * kKB + 256 + kMaxQ * 8;
+    return 1024 + size_t(CG == 2 ? kStages2 : kStages) * ((ATM ? 0 : kRows) + BN / CG) * kKB + 256 + kMaxQ * 8 +
+           kMaxD * 4 + kMaxD / 8;
 }
 
 __device__ __forceinline__ bool decode_row(const FusedGeom& g, int row, int& b, int& oy, int& ox) {
@@ -244,17 +246,36 @@ struct WaitClock {
 // i8 MMA costs the same per instruction for any N <= 256 at M=128 (measured, profiles/), so
 // layers with D = 128 need the pair to reach the full tensor rate; the pair also halves each
 // SM's weight traffic.
-template <int BN, int IN, int EPI, int CG>
+// ATM = 1: the activation operand A lives in TMEM (tcgen05.st by the producers, the MMA reads
+// it with the TS form) instead of shared memory. This takes the A tile off the shared-memory
+// port (its stores and the MMA's reads) and replaces the per-stage proxy fence (a MEMBAR that
+// drained the producers' prefetch loads) with tcgen05.wait::st. TMEM then holds the A stages
+// (32 columns each) next to the accumulators; with BN = 256 there is room for one accumulator
+// only, so the epilogue of tile i no longer overlaps the MMAs of tile i+1.
+template <int BN, int ATM>
+struct TmemPlan {
+    static constexpr int kAStage = 32;  // columns per A stage (128 K-bytes per lane)
+    static constexpr int kAcc = ATM ? (2 * BN + kStages * kAStage <= 512 ? 2 : 1) : 2;
+    static constexpr int kACol = kAcc * BN;  // first A-stage column
+    static constexpr int kUsed = kACol + (ATM ? kStages * kAStage : 0);
+    static constexpr uint32_t kCols = kUsed <= 32 ? 32 : kUsed <= 64 ? 64 : kUsed <= 128 ? 128 : kUsed <= 256 ? 256 : 512;
+    static_assert(kUsed <= 512, "TMEM budget");
+};
+
+template <int BN, int IN, int EPI, int CG, int ATM>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_layer_kernel(const __grid_constant__ CUtensorMap tmW, const FusedGeom g) {
+    static_assert(!(ATM && (CG == 2 || IN == FIN_F32)), "TMEM A operand: CTA-local, bits/pixel input");
+    using TP = TmemPlan<BN, ATM>;
     constexpr int kS = CG == 2 ? kStages2 : kStages;
     constexpr int BH = BN / CG;  // weight rows held by this CTA
+    constexpr int kAcc = TP::kAcc;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base - raw);
-    uint8_t* sA = smem;                               // [kS][128 * 128]
-    uint8_t* sB = smem + size_t(kS) * kRows * kKB;    // [kS][BH * 128]
+    uint8_t* sA = smem;                                           // [kS][128 * 128] (SS form only)
+    uint8_t* sB = smem + (ATM ? 0 : size_t(kS) * kRows * kKB);    // [kS][BH * 128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kS) * BH * kKB);
     uint64_t* full = bars;
     uint64_t* empty = bars + kS;
@@ -262,6 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int2* ftab = reinterpret_cast<int2*>(bars + 32);  // offset table [kMaxQ]
+    int* tu_s = reinterpret_cast<int*>(ftab + kMaxQ);                 // [kMaxD] thresholds Tu
+    uint32_t* flip_s = reinterpret_cast<uint32_t*>(tu_s + kMaxD);     // [kMaxD / 32] flip words
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -279,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * CG);
+            mbar_init(&tempty[a], 8 * CG);  // eight epilogue warps per CTA
         }
         fence_mbar_init();
     }
@@ -305,11 +328,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
         }
     }
+    if (EPI == FEPI_BITS) {  // this launch's thresholds and flip bits, for every n tile
+        const int dp = n_tiles * BN;
+        for (int d = threadIdx.x; d < dp; d += blockDim.x) tu_s[d] = __ldg(g.prm + d).x;
+        for (int d0 = warp * 32; d0 < dp; d0 += (kThreads / 32) * 32) {
+            const uint32_t f = __ballot_sync(0xffffffffu, __ldg(g.prm + d0 + lane).y != 0);
+            if (lane == 0) flip_s[d0 >> 5] = f;
+        }
+    }
     if (warp == 1) {
         if (CG == 2)
-            tmem_alloc_cg2<2 * BN>(tmem_slot);
+            tmem_alloc_cg2<TP::kCols>(tmem_slot);
         else
-            tmem_alloc<2 * BN>(tmem_slot);
+            tmem_alloc<TP::kCols>(tmem_slot);
     }
     tc_fence_before();
     __syncthreads();
@@ -365,7 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t b0 = smem_u32(sB + size_t(stage) * BH * kKB);
 #pragma unroll
                         for (int k = 0; k < kKB / 32; ++k) {
-                            if (CG == 2)
+                            if (ATM)
+                                mma_i8_ts(d_tmem, tmem_base + uint32_t(TP::kACol + stage * TP::kAStage + 8 * k),
+                                          sdesc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+                            else if (CG == 2)
                                 mma_i8_cg2(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
                                            (kb | k) != 0);
                             else
@@ -383,16 +417,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (++stage == kS) stage = 0, phase ^= 1;
                 }
-                if (++acc == 2) acc = 0, acc_phase ^= 1;
+                if (++acc == kAcc) acc = 0, acc_phase ^= 1;
             }
             if (lane == 0) wc.flush(g.dbg, 1);
         }
-    } else if (warp < 6) {
+    } else if (warp < 6 || warp >= 10) {
         // -------------------------------------------------------------- epilogue
         // Accumulator u = sum_k bit_k * w_k (bits in {0,1}, weights +-1); the reference's
         // xnor-popcount value is a = 2u - S_d with S_d = sum_k w_k (prm.z).
+        // Eight warps: warps 2-5 convert the first half of the tile's 32-column chunks,
+        // warps 10-13 the second half (same TMEM lane quarter = same rows), which halves the
+        // time the accumulator stays busy after the last MMA.
         const int q = warp & 3;  // TMEM lane quarter of this warp
         const int r = q * 32 + lane;
+        constexpr int NC = BN / 32;
+        const int c_lo = warp >= 10 ? (NC + 1) / 2 : 0, c_hi = warp >= 10 ? NC : (NC + 1) / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
         WaitClock wc;
@@ -404,12 +443,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             wc.wait(&tfull[acc], acc_phase, 0);
             tc_fence_after();
             uint32_t words[BN / 32];
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c * 32), v);
-                const int4 pl = __ldg(g.prm + n0 + c * 32 + lane);  // this lane's channel
-                tmem_ld_wait();
+            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+            // TMEM loads double-buffered: chunk c+1 is in flight while chunk c is converted
+            // (tcgen05.wait::ld waits for every outstanding load, so it comes first).
+            uint32_t va[32], vb[32];
+            auto convert = [&](const uint32_t(&v)[32], int c) {
                 if (g.dbg_mode & 2) {
                     words[0] = v[0];
                 } else if (EPI == FEPI_BITS) {
@@ -417,22 +455,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // (fma(scale, float(a) + bias, shift) >= 0), monotone in a, tabulated at
                     // build time (prep_params_kernel). Pooling: the predicate of the max is the
                     // OR of the (u >= Tu) terms, so the 2x2 max is a word OR over 4 lanes.
+                    // Thresholds come from shared memory as broadcast 16-byte loads.
+                    const int4* t4 = reinterpret_cast<const int4*>(tu_s + n0 + c * 32);
                     uint32_t w = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int tu = __shfl_sync(0xffffffffu, pl.x, j);
-                        w |= uint32_t(int(v[j]) >= tu) << j;
+                    for (int j = 0; j < 32; j += 4) {
+                        const int4 t = t4[j >> 2];
+                        w |= (uint32_t(int(v[j]) >= t.x) << j) | (uint32_t(int(v[j + 1]) >= t.y) << (j + 1)) |
+                             (uint32_t(int(v[j + 2]) >= t.z) << (j + 2)) | (uint32_t(int(v[j + 3]) >= t.w) << (j + 3));
                     }
                     if (g.pool) {
                         w |= __shfl_xor_sync(0xffffffffu, w, 1);
                         w |= __shfl_xor_sync(0xffffffffu, w, 2);
                     }
-                    w ^= __ballot_sync(0xffffffffu, pl.y != 0);
+                    w ^= flip_s[(n0 >> 5) + c];
 #pragma unroll
                     for (int cc = 0; cc < BN / 32; ++cc)  // static register index
                         if (cc == c) words[cc] = w;
                 } else {
                     // to_float(a) + bias (kernels.cpp:90-107): one rounding of an exact integer
+                    const int4 pl = __ldg(g.prm + n0 + c * 32 + lane);  // this lane's channel
                     const int P = g.OH * g.OW;
                     const int b = valid ? row / P : 0, p = row - b * P;
 #pragma unroll 4
@@ -449,6 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+            };
+            // TMEM loads double-buffered: chunk c+1 is in flight while chunk c is converted
+            // (tcgen05.wait::ld waits for every outstanding load, so it comes first).
+            if (c_lo < c_hi) tmem_ld32(tbase + uint32_t(c_lo * 32), va);
+#pragma unroll 1
+            for (int c = c_lo; c < c_hi; c += 2) {
+                tmem_ld_wait();
+                if (c + 1 < c_hi) tmem_ld32(tbase + uint32_t((c + 1) * 32), vb);
+                convert(va, c);
+                if (c + 1 < c_hi) {
+                    tmem_ld_wait();
+                    if (c + 2 < c_hi) tmem_ld32(tbase + uint32_t((c + 2) * 32), va);
+                    convert(vb, c + 1);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -461,34 +517,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
                 const int orow = g.pool ? (row >> 2) : row;
                 uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
-                if ((BN / 32) % 4 == 0 && (g.Dw & 3) == 0 && n0 + BN <= g.D) {
+                constexpr int H = (NC + 1) / 2;  // chunks per half
+                if (H % 4 == 0 && (g.Dw & 3) == 0 && n0 + BN <= g.D) {
 #pragma unroll
-                    for (int c = 0; c < BN / 32; c += 4)
-                        *reinterpret_cast<uint4*>(dst + c) =
-                            make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
+                    for (int c = 0; c < NC; c += 4)
+                        if (c >= c_lo && c < c_hi)
+                            *reinterpret_cast<uint4*>(dst + c) =
+                                make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
                 } else {
 #pragma unroll
-                    for (int c = 0; c < BN / 32; ++c)
-                        if (n0 + 32 * c < g.D) dst[c] = words[c];
+                    for (int c = 0; c < NC; ++c)
+                        if (c >= c_lo && c < c_hi && n0 + 32 * c < g.D) dst[c] = words[c];
                 }
             }
-            if (++acc == 2) acc = 0, acc_phase ^= 1;
+            if (++acc == kAcc) acc = 0, acc_phase ^= 1;
         }
         if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
     } else {
-        // -------------------------------------------------------------- activation producers
+        // -------------------------------------------------------------- activation producers (warps 6-9)
         // One tile row per thread: the row's 4 packed words of the block -> 128 operand bytes
         // in the UMMA layout. The words are loaded kPF blocks ahead into registers.
         // Measured limits (profiles/): the per-stage proxy fence (fence.proxy.async =
         // MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC) drains in-flight loads, and the A-tile stores
         // compete with the UMMA operand reads and the weight TMA for shared-memory bandwidth.
-        const int r = threadIdx.x - 6 * 32;  // tile row 0..127
+        // tile row 0..127; with A in TMEM a warp may only write its lane quarter (warp % 4)
+        const int r = ATM ? 32 * (warp & 3) + lane : threadIdx.x - 6 * 32;
         const int row_off = int(rank) * kRows + r;
         int stage = 0;
         uint32_t phase = 0;
         WaitClock wc;
         auto publish = [&](int st) {  // this warp's rows of stage st are written
-            fence_proxy_async_smem();
+            if (ATM) {
+                tmem_st_wait();
+                tc_fence_before();
+            } else {
+                fence_proxy_async_smem();
+            }
             __syncwarp();
             if (lane == 0) {
                 if (CG == 2)
@@ -536,7 +600,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1], pv[i] = pv[i + 1];
                     next_load(pf[kPF - 1], pv[kPF - 1]);
                     wc.wait(&empty[stage], phase ^ 1, 0);
-                    if (!(g.dbg_mode & 1)) store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
+                    if (ATM) {
+                        // bytes 4s..4s+3 of word i's 32-byte segment = column 8i + s (put_word's order)
+                        uint32_t v[32];
+                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
+                        tc_fence_after();
+                        tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) +
+                                      uint32_t(TP::kACol + stage * TP::kAStage), v);
+                    } else if (!(g.dbg_mode & 1)) {
+                        store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
+                    }
                     publish(stage);
                     if (++stage == kS) stage = 0, phase ^= 1;
                 }
@@ -560,9 +637,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (CG == 2) {
         cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
-        if (warp == 1) tmem_dealloc_cg2<2 * BN>(tmem_base);
+        if (warp == 1) tmem_dealloc_cg2<TP::kCols>(tmem_base);
     } else if (warp == 1) {
-        tmem_dealloc<2 * BN>(tmem_base);
+        tmem_dealloc<TP::kCols>(tmem_base);
     }
 }
 
@@ -647,10 +724,10 @@ __global__ void pack_pixels_kernel(const float* __restrict__ x, int C, size_t HW
     }
 }
 
-template <int BN, int IN, int EPI, int CG>
+template <int BN, int IN, int EPI, int CG, int ATM>
 int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_layer_kernel<BN, IN, EPI, CG>;
-    constexpr size_t smem = fused_smem<BN, CG>();
+    auto kern = fused_layer_kernel<BN, IN, EPI, CG, ATM>;
+    constexpr size_t smem = fused_smem<BN, CG, ATM>();
     static bool attr_set = false;  // per instantiation; the attribute is per function
     if (!attr_set) {
         BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -696,20 +773,26 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     return BNN_OK;
 }
 
-template <int IN, int EPI, int CG>
+template <int IN, int EPI, int CG, int ATM>
 int launch_fused_bn(int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     switch (BN) {
-        case 32: return launch_fused_t<32, IN, EPI, CG>(tm, g, s);
-        case 64: return launch_fused_t<64, IN, EPI, CG>(tm, g, s);
-        case 128: return launch_fused_t<128, IN, EPI, CG>(tm, g, s);
-        case 256: return launch_fused_t<256, IN, EPI, CG>(tm, g, s);
+        case 32: return launch_fused_t<32, IN, EPI, CG, ATM>(tm, g, s);
+        case 64: return launch_fused_t<64, IN, EPI, CG, ATM>(tm, g, s);
+        case 128: return launch_fused_t<128, IN, EPI, CG, ATM>(tm, g, s);
+        case 256: return launch_fused_t<256, IN, EPI, CG, ATM>(tm, g, s);
         default: return fail(BNN_E_CONFIG, "fused layer: unsupported BN " + std::to_string(BN));
     }
 }
 
+int g_atmem = -1;  // A operand in TMEM for CTA-local tiles (bnn_set_fused_tmem_a); -1: env / default on
+
 template <int IN, int EPI>
 int launch_fused_cg(int cg, int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    return cg == 2 ? launch_fused_bn<IN, EPI, 2>(BN, tm, g, s) : launch_fused_bn<IN, EPI, 1>(BN, tm, g, s);
+    if (cg == 2) return launch_fused_bn<IN, EPI, 2, 0>(BN, tm, g, s);
+    if (g_atmem < 0) g_atmem = getenv("BNN_FUSED_TMEM_A") ? atoi(getenv("BNN_FUSED_TMEM_A")) : 1;
+    if constexpr (IN != FIN_F32)
+        if (g_atmem) return launch_fused_bn<IN, EPI, 1, 1>(BN, tm, g, s);
+    return launch_fused_bn<IN, EPI, 1, 0>(BN, tm, g, s);
 }
 
 }  // namespace
@@ -743,9 +826,16 @@ int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out
     return launch_check("pack_pixels_kernel");
 }
 
+int fused_set_tmem_a(int enabled) {
+    g_atmem = enabled ? 1 : 0;
+    return BNN_OK;
+}
+
+int fused_tmem_a() { return g_atmem != 0; }
+
 int launch_fused(int cg, int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
-    set_last_gemm(cg == 2 ? "fused_umma_i8_cg2" : "fused_umma_i8");
+    set_last_gemm(cg == 2 ? "fused_umma_i8_cg2" : (in_mode != FIN_F32 && g_atmem != 0) ? "fused_umma_i8_tmem_a" : "fused_umma_i8");
     if (in_mode == FIN_PIX) {
         if (epi == FEPI_BITS) return launch_fused_cg<FIN_PIX, FEPI_BITS>(cg, BN, tm, g, s);
         return launch_fused_cg<FIN_PIX, FEPI_NCHW>(cg, BN, tm, g, s);

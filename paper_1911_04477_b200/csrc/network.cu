@@ -299,6 +299,7 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
                 return no("unsupported glue sequence after layer " + std::to_string(i));
             if (L.rows % 32) return no("output channels not a multiple of 32");
             st->epi = FEPI_BITS;
+            if (round_up(L.rows, 256) > 2048) return no("more than 2048 output channels");
         }
         g.pool = pool ? 1 : 0;
         g.Dw = g.D / 32;
@@ -685,6 +686,11 @@ int bnn_net_set_graphs(bnn_net* net, int enabled) {
     if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
     net->graph = bnn_net::Graph{};
     return BNN_OK;
+}
+
+int bnn_set_fused_tmem_a(int enabled) {
+    ++g_tiling_epoch;  // captured graphs hold the old kernels
+    return fused_set_tmem_a(enabled);
 }
 
 int bnn_net_engine(const bnn_net* net) { return use_fused(net) ? BNN_ENGINE_FUSED : BNN_ENGINE_GENERIC; }

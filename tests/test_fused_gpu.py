@@ -43,13 +43,16 @@ FUSABLE = {
 }
 
 
-@pytest.fixture(params=["auto", "cg1", "cg2"])
+@pytest.fixture(params=["auto", "smem_a", "cg1", "cg2"])
 def tiling(bnn, request):
-    """Every fused test runs with the automatic tile choice and with each cta_group forced."""
+    """Every fused test runs with the automatic tile choice (A operand in TMEM), with the A
+    operand staged in shared memory, and with each cta_group forced."""
     lib = bnn.load()
-    bnn._lib.check(lib.bnn_set_fused_tiling({"auto": 0, "cg1": 1, "cg2": 2}[request.param], 0))
+    bnn._lib.check(lib.bnn_set_fused_tiling({"auto": 0, "smem_a": 0, "cg1": 1, "cg2": 2}[request.param], 0))
+    bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if request.param == "smem_a" else 1))
     yield request.param
     lib.bnn_set_fused_tiling(0, 0)
+    lib.bnn_set_fused_tmem_a(1)
 
 
 @pytest.fixture
@@ -71,19 +74,21 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, batch):
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 
-@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("mode", ["cg1_tmem", "cg1_smem", "cg2"])
 @pytest.mark.parametrize("bn", [32, 64, 128, 256])
-def test_forced_tile_shapes_vs_oracle(bnn, orc, cg, bn):
+def test_forced_tile_shapes_vs_oracle(bnn, orc, mode, bn):
     lib = bnn.load()
     net = bnn.Network(seed=1)
     net.set_engine("fused")
     x = orc.fill_random((9, 3, 32, 32), orc.mix64(2, INPUT_STREAM))
     try:
-        bnn._lib.check(lib.bnn_set_fused_tiling(cg, bn))
+        bnn._lib.check(lib.bnn_set_fused_tiling(2 if mode == "cg2" else 1, bn))
+        bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if mode == "cg1_smem" else 1))
         got = net.forward(x)
     finally:
         lib.bnn_set_fused_tiling(0, 0)
-    assert np.array_equal(got, orc.net(seed=1).forward(x)), (cg, bn)
+        lib.bnn_set_fused_tmem_a(1)
+    assert np.array_equal(got, orc.net(seed=1).forward(x)), (mode, bn)
 
 
 def test_default_network_fused_equals_generic_large_batch(bnn, orc, fused):
