@@ -207,6 +207,9 @@ int bnn_set_fused_tiling(int cta_group, int bn);
  * non-default stream (default on). The first call runs eagerly, the second captures, later
  * calls replay the graph. */
 int bnn_net_set_graphs(bnn_net* net, int enabled);
+/* Fused engine split-K for few, K-deep output tiles (the linear layers at small batch): 0 auto
+ * (default), 1 off, or a forced power of two <= 16. Process-wide; bit-exact either way. */
+int bnn_set_fused_split(int split);
 /* Fused engine: keep the activation operand in TMEM (tcgen05.st + the TS-form MMA, default 1)
  * or stage it in shared memory (0). Process-wide; both are bit-exact. */
 int bnn_set_fused_tmem_a(int enabled);

@@ -288,11 +288,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    asm volatile("griddepcontrol.launch_dependents;");  // the next layer may start its prologue
     const int unit = blockIdx.x / CG, units = gridDim.x / CG;
     const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
     const int n_tiles = g.n_tiles;
-    const int tiles = m_tiles * n_tiles;
+    const int S = g.ksplit;  // split-K factor (>= 1): tile t is (output tile t / S, K slice t % S)
+    const int tiles = m_tiles * n_tiles * S;
     const int KB = g.KB;
+    auto kb_begin = [&](int t) { return (t % S) * KB / S; };
+    auto kb_end = [&](int t) { return (t % S + 1) * KB / S; };
+    auto tile_n = [&](int t) { return (t / S) % n_tiles; };
+    auto tile_m = [&](int t) { return (t / S) / n_tiles; };
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW);
@@ -347,6 +353,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above touches only this launch's constants
+    // (weights' tensor map, thresholds, tables, TMEM, barriers), so it overlaps the previous
+    // layer's tail. From here on the previous layer's output is read and a buffer it may still
+    // be reading is written: wait for it to complete.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // barrier the producers / TMA / epilogue signal: the even CTA's (shared::cluster address)
     auto leader = [&](uint64_t* bar) { return CG == 2 ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
@@ -358,8 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = unit; t < tiles; t += units) {
-                const int nt = t % n_tiles;
-                for (int kb = 0; kb < KB; ++kb) {
+                const int nt = tile_n(t), kb1 = kb_end(t);
+                for (int kb = kb_begin(t); kb < kb1; ++kb) {
                     wc.wait(&empty[stage], phase ^ 1, 0);
                     uint8_t* dst = sB + size_t(stage) * BH * kKB;
                     if (CG == 2) {
@@ -388,7 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 wc.wait(&tempty[acc], acc_phase ^ 1, 0);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < KB; ++kb) {
+                const int kb0 = kb_begin(t), kb1 = kb_end(t);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     wc.wait(&full[stage], phase, 1);
                     tc_fence_after();
                     if (lane == 0) {
@@ -398,20 +410,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = 0; k < kKB / 32; ++k) {
                             if (ATM)
                                 mma_i8_ts(d_tmem, tmem_base + uint32_t(TP::kACol + stage * TP::kAStage + 8 * k),
-                                          sdesc_k_sw128(b0 + 32 * k), idesc, (kb | k) != 0);
+                                          sdesc_k_sw128(b0 + 32 * k), idesc, (kb != kb0 || k != 0));
                             else if (CG == 2)
                                 mma_i8_cg2(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                           (kb | k) != 0);
+                                           (kb != kb0 || k != 0));
                             else
                                 mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                       (kb | k) != 0);
+                                       (kb != kb0 || k != 0));
                         }
                         if (CG == 2) {
                             mma_commit_cg2_mc(&empty[stage], 3);  // both CTAs' slots free
-                            if (kb == KB - 1) mma_commit_cg2_mc(&tfull[acc], 3);
+                            if (kb == kb1 - 1) mma_commit_cg2_mc(&tfull[acc], 3);
                         } else {
                             mma_commit(&empty[stage]);
-                            if (kb == KB - 1) mma_commit(&tfull[acc]);
+                            if (kb == kb1 - 1) mma_commit(&tfull[acc]);
                         }
                     }
                     __syncwarp();
@@ -432,11 +444,86 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         constexpr int NC = BN / 32;
         const int c_lo = warp >= 10 ? (NC + 1) / 2 : 0, c_hi = warp >= 10 ? NC : (NC + 1) / 2;
+        // Split-K completion (S > 1, CTA-local tiles, no pooling): the S CTAs of an output tile
+        // publish their partial sums, meet at a counter, and each reduces 128/S rows of the tile
+        // (its K-slice index picks the rows); the last one out resets the counters for the
+        // next launch. The S CTAs are co-resident (grid = tiles <= SMs, one CTA per SM).
+        const int et = (warp < 6 ? warp - 2 : warp - 6) * 32 + lane;  // 0..255 over the 8 warps
+        auto epi_bar = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };  // the 8 epilogue warps
+        auto split_reduce = [&](int t, int mt, int n0) {
+            const int u = t / S, ks = t % S;
+            __threadfence();  // this thread's partials, device-wide
+            epi_bar();
+            if (warp == 2 && lane == 0) {
+                atomicAdd(g.sem + 2 * u, 1u);
+                unsigned seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.sem + 2 * u) : "memory");
+                } while (seen < unsigned(S));
+                __threadfence();
+            }
+            __syncwarp();  // bar.sync is .aligned: the warp must arrive converged
+            epi_bar();
+            // each thread sums 4 adjacent columns of one row over the S slices (independent
+            // 16-byte L2 loads, all in flight); 8 adjacent lanes hold one 32-channel word
+            const int rp = kRows / S;
+            constexpr int C4 = BN / 4;  // 4-column groups per row (a multiple of 8)
+            for (int i0 = 0; i0 < rp * C4; i0 += 256) {
+                const int i = i0 + et;
+                const bool live = i < rp * C4;
+                const int row2 = mt * kRows + ks * rp + (live ? i / C4 : 0), c4 = i % C4;
+                const int n = n0 + 4 * c4;
+                int4 sum = make_int4(0, 0, 0, 0);
+                if (live) {
+                    const int4* src = reinterpret_cast<const int4*>(g.ws + size_t(row2) * g.ws_ld + n);
+                    const size_t slice = size_t(g.ws_rows) * g.ws_ld / 4;  // int4 stride between slices
+#pragma unroll 4
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        const int4 v4 = __ldcg(src + s2 * slice);
+                        sum.x += v4.x, sum.y += v4.y, sum.z += v4.z, sum.w += v4.w;
+                    }
+                }
+                const bool out = live && row2 < g.rows && n < g.D;
+                if (EPI == FEPI_BITS) {
+                    uint32_t w = 0;
+                    if (live) {
+                        const int4 t4 = *reinterpret_cast<const int4*>(tu_s + n);
+                        w = (uint32_t(sum.x >= t4.x) | (uint32_t(sum.y >= t4.y) << 1) | (uint32_t(sum.z >= t4.z) << 2) |
+                             (uint32_t(sum.w >= t4.w) << 3))
+                            << (4 * (c4 & 7));
+                    }
+                    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+                    if (out && (c4 & 7) == 0) g.out_bits[size_t(row2) * g.Dw + (n >> 5)] = w ^ flip_s[n >> 5];
+                } else if (out) {
+                    const int sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int d = n + j;
+                        if (d >= g.D) break;
+                        const int4 pd = __ldg(g.prm + d);
+                        const float y = __fadd_rn(__int2float_rn(2 * sv[j] - pd.z), __int_as_float(pd.w));
+                        if (EPI == FEPI_LOGITS) {
+                            g.out_f32[size_t(d) * g.ldo + row2] = y;
+                        } else {
+                            const int P = g.OH * g.OW, b = row2 / P;
+                            g.out_f32[(size_t(b) * g.D + d) * P + (row2 - b * P)] = y;
+                        }
+                    }
+                }
+            }
+            epi_bar();
+            if (warp == 2 && lane == 0 && atomicAdd(g.sem + 2 * u + 1, 1u) == unsigned(S - 1)) {
+                g.sem[2 * u] = 0;  // every CTA of the tile is past its wait and its reads
+                g.sem[2 * u + 1] = 0;
+            }
+        };
         int acc = 0;
         uint32_t acc_phase = 0;
         WaitClock wc;
         for (int t = unit; t < tiles; t += units) {
-            const int mt = t / n_tiles, nt = t % n_tiles;
+            const int mt = tile_m(t), nt = tile_n(t);
             const int row = mt * kRows * CG + int(rank) * kRows + r;
             const int n0 = nt * BN;
             const bool valid = row < g.rows;
@@ -448,6 +535,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (tcgen05.wait::ld waits for every outstanding load, so it comes first).
             uint32_t va[32], vb[32];
             auto convert = [&](const uint32_t(&v)[32], int c) {
+                if (S > 1) {  // split-K: this slice's partial sums go to the workspace
+                    int4* dst = reinterpret_cast<int4*>(g.ws + ((size_t(t % S) * g.ws_rows + row) * g.ws_ld + n0 + c * 32));
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        dst[j] = make_int4(int(v[4 * j]), int(v[4 * j + 1]), int(v[4 * j + 2]), int(v[4 * j + 3]));
+                    return;
+                }
                 if (g.dbg_mode & 2) {
                     words[0] = v[0];
                 } else if (EPI == FEPI_BITS) {
@@ -514,7 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     mbar_arrive(&tempty[acc]);
             }
-            if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
+            if (S > 1) {
+                split_reduce(t, mt, n0);
+            } else if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
                 const int orow = g.pool ? (row >> 2) : row;
                 uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
                 constexpr int H = (NC + 1) / 2;  // chunks per half
@@ -564,11 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (IN != FIN_F32) {
             constexpr int kPF = 3;
             using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw>::type;
-            int t_ld = unit, kb_ld = 0;  // next block to load
+            int t_ld = unit, kb_ld = unit < tiles ? kb_begin(unit) : 0;  // next block to load
+            int kb_ld_end = unit < tiles ? kb_end(unit) : 0;
             RowCtx rc;
             auto set_row = [&]() {
                 int b = 0, oy = 0, ox = 0;
-                rc.valid = t_ld < tiles && decode_row(g, (t_ld / n_tiles) * kRows * CG + row_off, b, oy, ox);
+                rc.valid = t_ld < tiles && decode_row(g, tile_m(t_ld) * kRows * CG + row_off, b, oy, ox);
                 rc.pix = b * g.H, rc.y0 = oy * g.SH, rc.x0 = ox * g.SW;
             };
             set_row();
@@ -581,16 +678,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     dst = load_pix(g, ftab, rc);
                 }
-                if (t_ld < tiles && ++kb_ld == KB) {
-                    kb_ld = 0;
+                if (t_ld < tiles && ++kb_ld == kb_ld_end) {  // per-tile divisions only at tile change
                     t_ld += units;
+                    kb_ld = t_ld < tiles ? kb_begin(t_ld) : 0;
+                    kb_ld_end = t_ld < tiles ? kb_end(t_ld) : 0;
                     set_row();
                 }
             };
 #pragma unroll
             for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
             for (int t = unit; t < tiles; t += units) {
-                for (int kb = 0; kb < KB; ++kb) {
+                const int kb1 = kb_end(t);
+                for (int kb = kb_begin(t); kb < kb1; ++kb) {
                     uint4 u;
                     if constexpr (IN == FIN_BITS)
                         u = pf[0];
@@ -621,8 +720,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             for (int t = unit; t < tiles; t += units) {
                 int b = 0, oy = 0, ox = 0;
-                const bool valid = decode_row(g, (t / n_tiles) * kRows * CG + row_off, b, oy, ox);
-                for (int kb = 0; kb < KB; ++kb) {
+                const bool valid = decode_row(g, tile_m(t) * kRows * CG + row_off, b, oy, ox);
+                const int kb1 = kb_end(t);
+                for (int kb = kb_begin(t); kb < kb1; ++kb) {
                     wc.wait(&empty[stage], phase ^ 1, 0);
                     produce_f32(g, ftab, smem_u32(sA + size_t(stage) * kRows * kKB), r, valid, b, oy, ox, kb);
                     publish(stage);
@@ -734,7 +834,11 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
         attr_set = true;
     }
     const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
-    const int tiles = m_tiles * g.n_tiles;
+    const int tiles = m_tiles * g.n_tiles * g.ksplit;
+    // split-K: the ksplit CTAs of an output tile wait for each other, so every tile needs its
+    // own co-resident CTA (one CTA per SM, grid = tiles <= SMs)
+    if (g.ksplit > 1 && tiles > num_sms() / CG)
+        return fail(BNN_E_CONFIG, "fused split-K: more tiles than SMs");
     const int grid = std::min(tiles, num_sms() / CG) * CG;
     static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
     FusedGeom gd = g;
@@ -750,13 +854,15 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CG;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = CG == 2 ? 1 : 0;
+    cfg.numAttrs = CG == 2 ? 2 : 1;
     BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
     BNN_TRY(launch_check("fused_layer_kernel"));
     if (prof) {

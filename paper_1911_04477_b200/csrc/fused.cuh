@@ -29,6 +29,10 @@ struct FusedGeom {
     int Dw;             // D / 32
     float* out_f32;     // FEPI_LOGITS: [D, ldo] (features x batch); FEPI_NCHW: [B, D, OH*OW]
     int ldo;
+    int ksplit;               // split-K factor (1: none); S > 1 needs ws/sem, CTA-local tiles, no pool
+    int* ws;                  // split-K partial sums [ksplit][ws_rows][ws_ld]
+    unsigned* sem;            // split-K counters, 2 per output tile, zero between launches
+    int ws_rows, ws_ld;
     unsigned long long* dbg;  // profiling counters (BNN_FUSED_PROFILE=1), else null
     int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math
 };

@@ -128,7 +128,7 @@ struct bnn_net {
     } graph;
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
-    bnnk::DevBuf bits[2], pix;
+    bnnk::DevBuf bits[2], pix, ws, sem;
 };
 
 namespace bnnk {
@@ -343,21 +343,36 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
 int g_forced_cg = -1, g_forced_bn = -1;  // bnn_set_fused_tiling (tests, experiments); -1: from env
 int g_tiling_epoch = 0;                   // bumped by bnn_set_fused_tiling: invalidates captured graphs
 
-void choose_tile(int D, size_t rows, int& cg, int& bn) {
+int g_forced_split = -1;  // BNN_FUSED_SPLIT / bnn_set_fused_split: 0 auto, 1 never, S forced
+
+void choose_tile(int D, size_t rows, int KB, bool pool, int& cg, int& bn, int& ks) {
     if (g_forced_cg < 0) g_forced_cg = getenv("BNN_FUSED_CG") ? atoi(getenv("BNN_FUSED_CG")) : 0;
     if (g_forced_bn < 0) g_forced_bn = getenv("BNN_FUSED_BN") ? atoi(getenv("BNN_FUSED_BN")) : 0;
+    if (g_forced_split < 0) g_forced_split = getenv("BNN_FUSED_SPLIT") ? atoi(getenv("BNN_FUSED_SPLIT")) : 0;
     const int forced_cg = g_forced_cg, forced_bn = g_forced_bn;
-    const size_t units2 = size_t(num_sms()) / 2;
     // CTA pairs measured no faster than single CTAs here (the i8 MMA runs ~128 cycles per
-    // instruction for any N <= 256 in both modes, and shared-memory bandwidth bounds both;
-    // profiles/r01_fused_cg_modes.log), so pairs are opt-in.
-    (void)units2;
+    // instruction for any N <= 256 in both modes), so pairs are opt-in.
     cg = forced_cg == 1 || forced_cg == 2 ? forced_cg : 1;
     const size_t m_tiles = ceil_div(rows, size_t(128 * cg)), units = size_t(num_sms()) / cg;
     bn = 32;
     while (bn < 256 && bn < D) bn *= 2;
-    while (bn > 32 && m_tiles * ceil_div(size_t(D), size_t(bn)) < units) bn /= 2;
-    if (forced_bn == 32 || forced_bn == 64 || forced_bn == 128 || forced_bn == 256) bn = forced_bn;
+    const bool bn_forced = forced_bn == 32 || forced_bn == 64 || forced_bn == 128 || forced_bn == 256;
+    if (bn_forced) bn = forced_bn;
+    ks = 1;
+    const size_t out_tiles = m_tiles * ceil_div(size_t(D), size_t(bn));
+    // Few, K-deep output tiles (the linear layers at small batch): an MMA costs the same for
+    // any N <= 256, so keep BN wide and split K across CTAs instead of narrowing BN.
+    const bool can_split = cg == 1 && !pool && g_forced_split != 1;
+    // The split completion (partials out, a counter, a reduction) costs ~10 us, so only deep
+    // reductions split (measured at batch 256: fc 8192->1024 gains, 1024->1024 loses).
+    if (can_split && (g_forced_split > 1 || (out_tiles * 2 <= units && KB >= 32))) {
+        const int cap = g_forced_split > 1 ? g_forced_split : 16;
+        const int kmin = g_forced_split > 1 ? 1 : 4;  // auto: at least 4 K-blocks per slice
+        // every split tile needs its own co-resident CTA (fused.cu split-K completion)
+        while (ks < cap && out_tiles * size_t(ks * 2) <= units && ks * 2 * kmin <= KB) ks *= 2;
+    }
+    if (ks == 1 && !bn_forced)
+        while (bn > 32 && m_tiles * ceil_div(size_t(D), size_t(bn)) < units) bn /= 2;
 }
 
 int box_index(int box) { return box == 16 ? 0 : box == 32 ? 1 : box == 64 ? 2 : box == 128 ? 3 : 4; }
@@ -504,9 +519,23 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         g.B = int(B);
         g.in = in;
         g.rows = int(rows);
-        int cg = 1, bn = 32;
-        choose_tile(g.D, rows, cg, bn);
+        int cg = 1, bn = 32, ks = 1;
+        choose_tile(g.D, rows, g.KB, g.pool != 0, cg, bn, ks);
         g.n_tiles = int(ceil_div(size_t(g.D), size_t(bn)));
+        g.ksplit = ks;
+        if (ks > 1) {  // split-K workspace and per-output-tile counters
+            const size_t m_tiles = ceil_div(rows, size_t(128));
+            g.ws_rows = int(m_tiles * 128), g.ws_ld = g.n_tiles * bn;
+            const size_t ws_bytes = size_t(ks) * g.ws_rows * g.ws_ld * 4;
+            const size_t sem_bytes = m_tiles * g.n_tiles * 2 * sizeof(unsigned);
+            if (net->ws.bytes < ws_bytes) BNN_TRY(net->ws.alloc(ws_bytes));
+            if (net->sem.bytes < sem_bytes) {
+                BNN_TRY(net->sem.alloc(sem_bytes));
+                BNN_CUDA(cudaMemsetAsync(net->sem.p, 0, sem_bytes, s));  // kernels leave them at 0
+            }
+            g.ws = net->ws.as<int>();
+            g.sem = net->sem.as<unsigned>();
+        }
         if (st.epi == FEPI_BITS) {
             g.out_bits = net->bits[which].as<uint32_t>();
             which ^= 1;
@@ -685,6 +714,14 @@ int bnn_net_set_graphs(bnn_net* net, int enabled) {
     net->use_graphs = enabled != 0;
     if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
     net->graph = bnn_net::Graph{};
+    return BNN_OK;
+}
+
+int bnn_set_fused_split(int split) {
+    if (split < 0 || split > 16 || (split > 1 && (split & (split - 1))))
+        return fail(BNN_E_CONFIG, "fused split: 0 (auto), 1 (off) or a power of two <= 16");
+    g_forced_split = split;
+    ++g_tiling_epoch;
     return BNN_OK;
 }
 

@@ -43,16 +43,20 @@ FUSABLE = {
 }
 
 
-@pytest.fixture(params=["auto", "smem_a", "cg1", "cg2"])
+@pytest.fixture(params=["auto", "smem_a", "cg1", "cg2", "nosplit", "split16"])
 def tiling(bnn, request):
-    """Every fused test runs with the automatic tile choice (A operand in TMEM), with the A
-    operand staged in shared memory, and with each cta_group forced."""
+    """Every fused test runs with the automatic tile choice (A operand in TMEM, split-K for the
+    small-batch linear layers), with the A operand staged in shared memory, with each
+    cta_group forced, and with split-K off / forced to 16."""
     lib = bnn.load()
-    bnn._lib.check(lib.bnn_set_fused_tiling({"auto": 0, "smem_a": 0, "cg1": 1, "cg2": 2}[request.param], 0))
-    bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if request.param == "smem_a" else 1))
-    yield request.param
+    p = request.param
+    bnn._lib.check(lib.bnn_set_fused_tiling({"cg1": 1, "cg2": 2}.get(p, 0), 0))
+    bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if p == "smem_a" else 1))
+    bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16}.get(p, 0)))
+    yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_tmem_a(1)
+    lib.bnn_set_fused_split(0)
 
 
 @pytest.fixture
