@@ -276,38 +276,63 @@ def run_ours(args):
             traffic = None
     kernel_name = lib.bnn_last_gemm_kernel().decode()
 
-    # ---- end to end through the public API: pinned host input -> H2D -> forward -> D2H logits
+    # ---- end to end through the public API: every step copies its input from pinned host memory
+    # (H2D), runs the forward, and reads its logits back (D2H). Steps are pipelined like a
+    # serving loop: two input/output buffers, the copies on their own streams, so step i+1's H2D
+    # overlaps step i's forward; the host waits for every step's logits (one step behind).
     e2e = None
     if not args.no_e2e:
         hx = x.cpu().pin_memory()
-        hy = torch.empty((world if world > 1 else 1, net.logits, B), dtype=torch.float32).pin_memory()
-        dx = torch.empty_like(x)
-        with torch.cuda.stream(st):
-            def e2e_step():
-                dx.copy_(hx, non_blocking=True)
-                net.forward_device(dx, logits, S)
-                if world > 1:
-                    dist.all_gather_into_tensor(gathered, logits)
-                    hy.copy_(gathered, non_blocking=True)
-                else:
-                    hy[0].copy_(logits, non_blocking=True)
-                st.synchronize()  # the step's result is on the host
+        nbuf = 2
+        dxs = [torch.empty_like(x) for _ in range(nbuf)]
+        outs = [torch.empty((net.logits, B), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+        gat = [torch.empty((world, net.logits, B), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+        hys = [torch.empty((world, net.logits, B), dtype=torch.float32).pin_memory() for _ in range(nbuf)]
+        s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_comp = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_out = [torch.cuda.Event() for _ in range(nbuf)]
 
-            for _ in range(3):
-                e2e_step()
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            for _ in range(args.steps):
-                e2e_step()
-            e2e_s = time.perf_counter() - t0
+        def issue(i):
+            k = i % nbuf
+            s_h2d.wait_event(ev_comp[k])  # step i-nbuf's forward is done with dxs[k]
+            with torch.cuda.stream(s_h2d):
+                dxs[k].copy_(hx, non_blocking=True)
+                ev_in[k].record(s_h2d)
+            st.wait_event(ev_in[k])
+            st.wait_event(ev_out[k])  # step i-nbuf's D2H is done with outs[k] / gat[k]
+            with torch.cuda.stream(st):
+                net.forward_device(dxs[k], outs[k], S)
+                if world > 1:
+                    dist.all_gather_into_tensor(gat[k], outs[k])
+                else:
+                    gat[k][0].copy_(outs[k])
+                ev_comp[k].record(st)
+            s_d2h.wait_event(ev_comp[k])
+            with torch.cuda.stream(s_d2h):
+                hys[k].copy_(gat[k], non_blocking=True)
+                ev_out[k].record(s_d2h)
+
+        for i in range(4):
+            issue(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            issue(i)
+            if i:
+                ev_out[(i - 1) % nbuf].synchronize()  # the host holds step i-1's logits
+        ev_out[(args.steps - 1) % nbuf].synchronize()
+        e2e_s = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": B * IMG * 4,
                "d2h_bytes_per_step": net.logits * B * 4 * world,
-               "timer": "host clock around K synchronous steps (pinned H2D + forward + D2H), max over ranks"}
+               "timer": "host clock around K pipelined steps (pinned H2D + forward + D2H of every step; "
+                        "step i+1's copy overlaps step i's forward), max over ranks"}
 
     # ---- batch sweep (BASELINE.json configs[4]), N=1: images/s at each per-GPU batch
     sweep = None

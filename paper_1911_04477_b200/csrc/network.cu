@@ -13,6 +13,7 @@
 // + K1 pack_cols(sign) + K3; maxpool / affine / htanh / sign = K4. Activations ping-pong
 // between two arena buffers sized for the largest layer at the requested batch.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <memory>
 #include <string>
@@ -118,14 +119,23 @@ struct bnn_net {
     std::vector<std::unique_ptr<bnnk::FusedStage>> stages;
     bool use_graphs = true;
     struct Graph {
+        bool key_set = false;
         const float* x = nullptr;
         size_t B = 0;
         float* logits = nullptr;
         cudaStream_t s = nullptr;
         cudaGraphExec_t exec = nullptr;
         size_t launches = 0;
-        int epoch = 0;
-    } graph;
+        int epoch = 0, arena = 0;
+    };
+    std::array<Graph, 4> graphs;
+    size_t graph_next = 0;
+    int arena_epoch = 0;  // bumped whenever an internal buffer is reallocated (graphs hold pointers)
+    void drop_graphs() {
+        for (auto& e : graphs)
+            if (e.exec) cudaGraphExecDestroy(e.exec);
+        graphs = {};
+    }
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix, ws, sem;
@@ -506,6 +516,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         BNN_TRY(net->bits[1].alloc(bytes));
         BNN_TRY(net->pix.alloc(B * net->in_h * net->in_w * 4));
         net->bits_batch = B;
+        ++net->arena_epoch;
     }
     const void* in = x;
     int which = 0;
@@ -528,8 +539,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             g.ws_rows = int(m_tiles * 128), g.ws_ld = g.n_tiles * bn;
             const size_t ws_bytes = size_t(ks) * g.ws_rows * g.ws_ld * 4;
             const size_t sem_bytes = m_tiles * g.n_tiles * 2 * sizeof(unsigned);
-            if (net->ws.bytes < ws_bytes) BNN_TRY(net->ws.alloc(ws_bytes));
+            if (net->ws.bytes < ws_bytes) {
+                BNN_TRY(net->ws.alloc(ws_bytes));
+                ++net->arena_epoch;
+            }
             if (net->sem.bytes < sem_bytes) {
+                ++net->arena_epoch;
                 BNN_TRY(net->sem.alloc(sem_bytes));
                 BNN_CUDA(cudaMemsetAsync(net->sem.p, 0, sem_bytes, s));  // kernels leave them at 0
             }
@@ -572,22 +587,29 @@ int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaS
     static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
     const bool graphable = net->use_graphs && !net->timing && !prof && s != nullptr;
     if (!graphable) return forward_fused(net, x, B, logits, s);
-    bnn_net::Graph& gc = net->graph;
-    if (gc.epoch != g_tiling_epoch) {
-        if (gc.exec) cudaGraphExecDestroy(gc.exec);
-        gc = bnn_net::Graph{};
-        gc.epoch = g_tiling_epoch;
+    // small cache: a pipelined caller alternates input/output buffers
+    bnn_net::Graph* gc = nullptr;
+    for (auto& e : net->graphs) {
+        if (e.exec && (e.epoch != g_tiling_epoch || e.arena != net->arena_epoch)) {  // stale kernels / buffers
+            cudaGraphExecDestroy(e.exec);
+            e = bnn_net::Graph{};
+        }
+        if (e.key_set && e.x == x && e.B == B && e.logits == logits && e.s == s) gc = &e;
     }
-    if (gc.exec && gc.x == x && gc.B == B && gc.logits == logits && gc.s == s) {
-        BNN_CUDA(cudaGraphLaunch(gc.exec, s));
-        net->last_launches = gc.launches;
+    if (gc && gc->exec) {
+        BNN_CUDA(cudaGraphLaunch(gc->exec, s));
+        net->last_launches = gc->launches;
         return BNN_OK;
     }
-    if (!(gc.x == x && gc.B == B && gc.logits == logits && gc.s == s)) {
+    if (!gc) {
         // first sighting: run eagerly (sizes the arena, sets kernel attributes), remember the key
-        gc.x = x, gc.B = B, gc.logits = logits, gc.s = s;
-        if (gc.exec) cudaGraphExecDestroy(gc.exec), gc.exec = nullptr;
-        return forward_fused(net, x, B, logits, s);
+        bnn_net::Graph& e = net->graphs[net->graph_next++ % net->graphs.size()];
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+        e = bnn_net::Graph{};
+        const int rc = forward_fused(net, x, B, logits, s);
+        e.key_set = true, e.x = x, e.B = B, e.logits = logits, e.s = s;
+        e.epoch = g_tiling_epoch, e.arena = net->arena_epoch;
+        return rc;
     }
     cudaGraph_t graph = nullptr;
     BNN_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -598,11 +620,12 @@ int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaS
         return rc;
     }
     BNN_CUDA(ce);
-    const cudaError_t ie = cudaGraphInstantiate(&gc.exec, graph, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&gc->exec, graph, 0);
     cudaGraphDestroy(graph);
     BNN_CUDA(ie);
-    gc.launches = net->last_launches;
-    BNN_CUDA(cudaGraphLaunch(gc.exec, s));
+    gc->launches = net->last_launches;
+    gc->epoch = g_tiling_epoch, gc->arena = net->arena_epoch;
+    BNN_CUDA(cudaGraphLaunch(gc->exec, s));
     return BNN_OK;
 }
 
@@ -685,7 +708,7 @@ void bnn_net_destroy(bnn_net* net) {
         cudaEventDestroy(p.b);
     }
     for (auto e : net->pool) cudaEventDestroy(e);
-    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
+    net->drop_graphs();
     delete net;
 }
 size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
@@ -696,8 +719,7 @@ int bnn_net_set_engine(bnn_net* net, int policy) {
     if (policy == BNN_ENGINE_FUSED && !net->fusable)
         return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
     net->engine_policy = policy;
-    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
-    net->graph = bnn_net::Graph{};
+    net->drop_graphs();
     return BNN_OK;
 }
 
@@ -712,8 +734,7 @@ int bnn_set_fused_tiling(int cta_group, int bn) {
 
 int bnn_net_set_graphs(bnn_net* net, int enabled) {
     net->use_graphs = enabled != 0;
-    if (net->graph.exec) cudaGraphExecDestroy(net->graph.exec);
-    net->graph = bnn_net::Graph{};
+    net->drop_graphs();
     return BNN_OK;
 }
 
