@@ -213,6 +213,12 @@ int bnn_set_fused_split(int split);
 /* Fused engine: keep the activation operand in TMEM (tcgen05.st + the TS-form MMA, default 1)
  * or stage it in shared memory (0). Process-wide; both are bit-exact. */
 int bnn_set_fused_tmem_a(int enabled);
+/* Fused engine: run every stage of the network in ONE persistent chained launch (1) or one
+ * launch per weighted layer (0, default). Process-wide; both are bit-exact. */
+int bnn_set_fused_chain(int enabled);
+/* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
+ * op 1 = start recording, op 2 = print the recorded launches and stop. */
+int bnn_debug_timeline(int op);
 /* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
 int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */

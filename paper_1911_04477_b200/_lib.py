@@ -104,6 +104,8 @@ _SIGS = {
     "bnn_set_fused_tiling": (_I, [_I, _I]),
     "bnn_set_fused_tmem_a": (_I, [_I]),
     "bnn_set_fused_split": (_I, [_I]),
+    "bnn_set_fused_chain": (_I, [_I]),
+    "bnn_debug_timeline": (_I, [_I]),
     "bnn_net_set_timing": (_I, [_P, _I]),
     "bnn_net_timing": (_I, [_P, _P, _P, _P]),
     "bnn_net_reset_timing": (_I, [_P]),

@@ -40,6 +40,8 @@
 //               packed words per stage (one 16-byte load), expand bit -> +-1 byte and store
 //               them in the SWIZZLE_128B K-major layout the UMMA descriptor expects.
 #include <algorithm>
+#include <string>
+#include <vector>
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
@@ -49,6 +51,13 @@
 #include "umma.cuh"
 
 namespace bnnk {
+
+// debug timeline (bnn_debug_timeline): globaltimer stamps per CTA and launch
+constexpr int kTlSlots = 64;  // launches (or chain stages) per recording
+constexpr int kTlCtas = 160;  // >= SMs
+unsigned long long* g_tl = nullptr;
+int g_tl_used = -1;  // -1: off
+std::vector<std::string> g_tl_names;
 
 using namespace umma;
 
@@ -118,14 +127,38 @@ struct RowCtx {
 // The 4 packed words (one 128-position K block) of one row. qtab[q] = {dy<<16 | dx&0xffff,
 // cw} for K word q (cw < 0: K padding). One 16-byte load when the block is one tap of
 // contiguous channels (Cw % 4 == 0), else word by word.
+// Activation loads. A single-layer launch uses the read-only path (ld.global.nc), predicated.
+// The chained kernel's activation buffers are written by other CTAs during the launch, so it
+// uses coherent loads (ld.global.ca, volatile asm: never moved across the stage hand-off's
+// acquire and barrier). The producers' ld.acquire.gpu of the stage counter invalidates the
+// SM's L1 (SASS: CCTL.IVALL), so cached loads after it see those writes. The coherent loads
+// are issued unconditionally from a clamped address (padding positions read the buffer's
+// first word and discard it): a conditional volatile load compiles to a branch per load.
+__device__ __forceinline__ uint4 ld_ca4(const uint32_t* p) {
+    uint4 v;
+    asm volatile("ld.global.ca.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_ca(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+template <bool Coherent = false>
 __device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab, const RowCtx& rc, int kb) {
     const uint32_t* act = static_cast<const uint32_t*>(g.in);
     if (!rc.valid) return make_uint4(0, 0, 0, 0);
     if ((g.Cw & 3) == 0) {
         const int2 e = qtab[4 * kb];
         const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
-        if (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
-            return __ldg(reinterpret_cast<const uint4*>(act + (size_t((rc.pix + iy) * g.W + ix)) * g.Cw + e.y));
+        const bool inb = unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W);
+        const uint32_t* src = act + (size_t((rc.pix + iy) * g.W + ix)) * g.Cw + e.y;
+        if (Coherent) {
+            const uint4 v = ld_ca4(inb ? src : act);
+            return inb ? v : make_uint4(~0u, ~0u, ~0u, ~0u);
+        }
+        if (inb) return __ldg(reinterpret_cast<const uint4*>(src));
         return make_uint4(~0u, ~0u, ~0u, ~0u);  // spatial padding: sign(0.0) = +1
     }
     uint32_t w[4];
@@ -133,10 +166,15 @@ __device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab,
     for (int i = 0; i < 4; ++i) {
         const int2 e = qtab[4 * kb + i];
         const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
-        w[i] = e.y < 0 ? 0u  // K padding: 0 bytes, and the weights are 0 there too
-               : (unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
-                   ? __ldg(act + size_t((rc.pix + iy) * g.W + ix) * g.Cw + e.y)
-                   : ~0u;
+        const bool inb = unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W);
+        const uint32_t* src = act + size_t((rc.pix + iy) * g.W + ix) * g.Cw + e.y;
+        if (Coherent) {
+            const uint32_t v = ld_ca(e.y >= 0 && inb ? src : act);
+            w[i] = e.y < 0 ? 0u : inb ? v : ~0u;
+        } else {
+            w[i] = e.y < 0 ? 0u  // K padding: 0 bytes, and the weights are 0 there too
+                   : inb ? __ldg(src) : ~0u;
+        }
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
@@ -150,6 +188,7 @@ struct PixRaw {
     uint32_t v[kMaxPixTaps];
 };
 
+template <bool Coherent = false>
 __device__ __forceinline__ PixRaw load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
     const uint32_t* pix = static_cast<const uint32_t*>(g.in);
     const int T = g.KH * g.KW;
@@ -159,9 +198,17 @@ __device__ __forceinline__ PixRaw load_pix(const FusedGeom& g, const int2* qtab,
     for (int tap = 0; tap < kMaxPixTaps; ++tap) {
         const int2 e = qtab[tap < T ? tap : 0];
         const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
+        const bool inb = rc.valid && tap < T && unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W);
+        const uint32_t* src = pix + size_t(rc.pix + iy) * g.W + ix;
         uint32_t v = cmask;  // padding: every channel +1
-        if (rc.valid && tap < T && unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W))
-            v = __ldg(pix + size_t(rc.pix + iy) * g.W + ix);
+        if (Coherent) {
+            if (tap < T) {  // T is uniform: no divergence
+                const uint32_t u = ld_ca(inb ? src : pix);
+                v = inb ? u : cmask;
+            }
+        } else if (inb) {
+            v = __ldg(src);
+        }
         raw.v[tap] = v;
     }
     return raw;
@@ -220,6 +267,12 @@ __device__ __forceinline__ long long dclock() {
 #else
     return 0;
 #endif
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 struct WaitClock {
@@ -289,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     asm volatile("griddepcontrol.launch_dependents;");  // the next layer may start its prologue
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const int unit = blockIdx.x / CG, units = gridDim.x / CG;
     const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
     const int n_tiles = g.n_tiles;
@@ -353,11 +407,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
     // Programmatic dependent launch: everything above touches only this launch's constants
     // (weights' tensor map, thresholds, tables, TMEM, barriers), so it overlaps the previous
     // layer's tail. From here on the previous layer's output is read and a buffer it may still
     // be reading is written: wait for it to complete.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 2] = gtimer();
 
     // barrier the producers / TMA / epilogue signal: the even CTA's (shared::cluster address)
     auto leader = [&](uint64_t* bar) { return CG == 2 ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
@@ -644,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         WaitClock wc;
         auto publish = [&](int st) {  // this warp's rows of stage st are written
             if (ATM) {
-                tmem_st_wait();
+                if (!(g.dbg_mode & 8)) tmem_st_wait();
                 tc_fence_before();
             } else {
                 fence_proxy_async_smem();
@@ -708,8 +764,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
                         tc_fence_after();
-                        tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) +
-                                      uint32_t(TP::kACol + stage * TP::kAStage), v);
+                        if (!(g.dbg_mode & 1))
+                            tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) +
+                                          uint32_t(TP::kACol + stage * TP::kAStage), v);
                     } else if (!(g.dbg_mode & 1)) {
                         store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
                     }
@@ -735,11 +792,530 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
     if (CG == 2) {
         cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
         if (warp == 1) tmem_dealloc_cg2<TP::kCols>(tmem_base);
     } else if (warp == 1) {
         tmem_dealloc<TP::kCols>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Chained engine: ONE persistent launch runs every fused stage of a network (conv/linear +
+// glue, as above), instead of one launch per weighted layer.
+//
+// Why: at the benchmark batch the per-layer kernels are short (10-70 us) and each paid ~10 us
+// of launch, prologue (barriers, TMEM allocation, threshold tables), pipeline fill and tail.
+// Here the roles persist across stages and their pipelines run straight through the stage
+// boundaries: the weight TMA warp streams the next stage's weights (they do not depend on
+// the activations) while the current stage's MMAs and epilogues finish, and the TMEM ring,
+// the shared-memory ring and their barrier phases carry over.
+//
+// The one cross-CTA dependency is the activation hand-off: stage s+1 reads every pixel
+// stage s wrote. Each CTA's epilogue warps publish "stage s done" (per-thread
+// __threadfence, a named barrier, one release-add on done[s]); the producer warps of every
+// CTA wait for done[s] == gridDim.x (acquire) before their first activation load of stage
+// s+1; that acquire invalidates the SM's L1, so the coherent activation loads after it see
+// no stale line of a buffer rewritten since the SM last read it. Write-after-read on the ping-pong activation
+// buffers is ordered by the same chain (stage s+1 writes only after its own producers passed
+// done[s], which follows every read of stage s-1). The grid is one CTA per SM (smem- and
+// register-limited to 1 CTA/SM), all co-resident, so the spin-waits cannot deadlock.
+//
+// Restrictions (else the per-layer launches above run): CTA-local M=128 tiles (cta_group::1),
+// A operand in TMEM, packed-bit or pixel-packed inputs (no float im2col stage), epilogues
+// writing packed bits or logits.
+//
+// TMEM (512 columns): accumulator slot a at column 256a (BN <= 128: two slots, the epilogue
+// of tile i overlaps the MMAs of tile i+1; BN = 256: slot 0 only), A stages at 384 + 32s.
+
+constexpr int kChainA = 384;
+constexpr size_t kChainSmem = 1024 + size_t(kStages) * 256 * kKB + 256 + kMaxQ * 8 + kMaxD * 4 + kMaxD / 8;
+
+// Profiling aid (ChainParams::dbg, BNN_FUSED_PROFILE=1): per stage and role, the cycles spent
+// blocked in two wait classes and the role's cycles in the stage. Slots dbg[s*16 + role*4 +
+// {0, 1, 3}]; roles 0 TMA, 1 MMA, 2 epilogue, 3 producer.
+struct StageClock {
+    long long w0 = 0, w1 = 0, t0;
+    __device__ __forceinline__ StageClock() : t0(dclock()) {}
+    __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int slot) {
+        const long long a = dclock();
+        mbar_wait(bar, parity);
+        (slot ? w1 : w0) += dclock() - a;
+    }
+    __device__ __forceinline__ void flush(unsigned long long* dbg, int s, int role, bool reporter) {
+        const long long now = dclock();
+        if (dbg && reporter) {
+            atomicAdd(dbg + s * 16 + role * 4 + 0, (unsigned long long)w0);
+            atomicAdd(dbg + s * 16 + role * 4 + 1, (unsigned long long)w1);
+            atomicAdd(dbg + s * 16 + role * 4 + 3, (unsigned long long)(now - t0));
+        }
+        w0 = w1 = 0;
+        t0 = now;
+    }
+};
+
+struct ChainTiles {
+    int S, n_tiles, tiles, KB;
+    __device__ __forceinline__ explicit ChainTiles(const FusedGeom& g) : S(g.ksplit), n_tiles(g.n_tiles), KB(g.KB) {
+        tiles = ((g.rows + kRows - 1) / kRows) * n_tiles * S;
+    }
+    __device__ __forceinline__ int kb_begin(int t) const { return (t % S) * KB / S; }
+    __device__ __forceinline__ int kb_end(int t) const { return (t % S + 1) * KB / S; }
+    __device__ __forceinline__ int n(int t) const { return (t / S) % n_tiles; }
+    __device__ __forceinline__ int m(int t) const { return (t / S) / n_tiles; }
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }   // 8 epilogue warps
+__device__ __forceinline__ void prod_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }  // 4 producer warps
+
+// Epilogue of one stage (warps 2-5 and 10-13): the same conversion as fused_layer_kernel.
+// Bit a of euse is the tfull parity of accumulator slot a (flipped at every use).
+template <int BN, int EPI>
+__device__ __forceinline__ void chain_epilogue(const FusedGeom& g, uint64_t* tfull, uint64_t* tempty,
+                                               uint32_t tmem_base, const int* tu_s, const uint32_t* flip_s,
+                                               uint32_t& euse, int warp, int lane, StageClock& sc) {
+    static_assert(EPI == FEPI_BITS || EPI == FEPI_LOGITS, "chained epilogues: bits or logits");
+    const ChainTiles ct(g);
+    const int S = ct.S;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    constexpr int NC = BN / 32;
+    constexpr int kAcc = BN <= 128 ? 2 : 1;
+    const int c_lo = warp >= 10 ? (NC + 1) / 2 : 0, c_hi = warp >= 10 ? NC : (NC + 1) / 2;
+    const int et = (warp < 6 ? warp - 2 : warp - 6) * 32 + lane;
+    int i = 0;
+    for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x, ++i) {
+        const int acc = kAcc == 2 ? (i & 1) : 0;
+        const int mt = ct.m(t), nt = ct.n(t);
+        const int row = mt * kRows + r;
+        const int n0 = nt * BN;
+        const bool valid = row < g.rows;
+        sc.wait(&tfull[acc], (euse >> acc) & 1u, 0);
+        euse ^= 1u << acc;
+        tc_fence_after();
+        uint32_t words[NC];
+        const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * 256);
+        // 16-column TMEM loads, double-buffered (32-column buffers, as in fused_layer_kernel,
+        // spill here: the chained kernel holds every role's state in one register allocation,
+        // at most 128 per thread with 14 warps)
+        uint32_t va[16], vb[16];
+        uint32_t wacc = 0;  // the 32-channel word under construction
+        auto convert = [&](const uint32_t(&v)[16], int h) {
+            const int c = h >> 1, hb = (h & 1) * 16;
+            const int col = n0 + h * 16;
+            if (S > 1) {
+                int4* dst = reinterpret_cast<int4*>(g.ws + ((size_t(t % S) * g.ws_rows + row) * g.ws_ld + col));
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    dst[j] = make_int4(int(v[4 * j]), int(v[4 * j + 1]), int(v[4 * j + 2]), int(v[4 * j + 3]));
+                return;
+            }
+            if (EPI == FEPI_BITS) {
+                const int4* t4 = reinterpret_cast<const int4*>(tu_s + col);
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const int4 th = t4[j >> 2];
+                    wacc |= ((uint32_t(int(v[j]) >= th.x) << j) | (uint32_t(int(v[j + 1]) >= th.y) << (j + 1)) |
+                             (uint32_t(int(v[j + 2]) >= th.z) << (j + 2)) | (uint32_t(int(v[j + 3]) >= th.w) << (j + 3)))
+                            << hb;
+                }
+                if (h & 1) {
+                    uint32_t w = wacc;
+                    wacc = 0;
+                    if (g.pool) {
+                        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                    }
+                    w ^= flip_s[(n0 >> 5) + c];
+#pragma unroll
+                    for (int cc = 0; cc < NC; ++cc)
+                        if (cc == c) words[cc] = w;
+                }
+            } else {
+                const int4 pl = __ldg(g.prm + n0 + c * 32 + lane);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int d = col + j;
+                    const int sd = __shfl_sync(0xffffffffu, pl.z, hb + j);
+                    const float bias = __int_as_float(__shfl_sync(0xffffffffu, pl.w, hb + j));
+                    const float y = __fadd_rn(__int2float_rn(2 * int(v[j]) - sd), bias);
+                    if (valid && d < g.D) g.out_f32[size_t(d) * g.ldo + row] = y;
+                }
+            }
+        };
+        const int h_lo = 2 * c_lo, h_hi = 2 * c_hi;  // an even number of halves
+        if (h_lo < h_hi) tmem_ld16(tbase + uint32_t(h_lo * 16), va);
+#pragma unroll 1
+        for (int h = h_lo; h < h_hi; h += 2) {
+            tmem_ld_wait();
+            tmem_ld16(tbase + uint32_t((h + 1) * 16), vb);
+            convert(va, h);
+            tmem_ld_wait();
+            if (h + 2 < h_hi) tmem_ld16(tbase + uint32_t((h + 2) * 16), va);
+            convert(vb, h + 1);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (S > 1) {
+            // split-K completion, as in fused_layer_kernel: meet at the tile's counter, each
+            // K-slice CTA reduces 128/S rows, the last one out resets the counters
+            const int u = t / S, ks = t % S;
+            __threadfence();
+            epi_bar();
+            if (warp == 2 && lane == 0) {
+                atomicAdd(g.sem + 2 * u, 1u);
+                unsigned seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.sem + 2 * u) : "memory");
+                } while (seen < unsigned(S));
+                __threadfence();
+            }
+            __syncwarp();
+            epi_bar();
+            const int rp = kRows / S;
+            constexpr int C4 = BN / 4;
+            for (int i0 = 0; i0 < rp * C4; i0 += 256) {
+                const int ii = i0 + et;
+                const bool live = ii < rp * C4;
+                const int row2 = mt * kRows + ks * rp + (live ? ii / C4 : 0), c4 = ii % C4;
+                const int n = n0 + 4 * c4;
+                int4 sum = make_int4(0, 0, 0, 0);
+                if (live) {
+                    const int4* src = reinterpret_cast<const int4*>(g.ws + size_t(row2) * g.ws_ld + n);
+                    const size_t slice = size_t(g.ws_rows) * g.ws_ld / 4;
+#pragma unroll 4
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        const int4 v4 = __ldcg(src + s2 * slice);
+                        sum.x += v4.x, sum.y += v4.y, sum.z += v4.z, sum.w += v4.w;
+                    }
+                }
+                const bool out = live && row2 < g.rows && n < g.D;
+                if (EPI == FEPI_BITS) {
+                    uint32_t w = 0;
+                    if (live) {
+                        const int4 t4 = *reinterpret_cast<const int4*>(tu_s + n);
+                        w = (uint32_t(sum.x >= t4.x) | (uint32_t(sum.y >= t4.y) << 1) | (uint32_t(sum.z >= t4.z) << 2) |
+                             (uint32_t(sum.w >= t4.w) << 3))
+                            << (4 * (c4 & 7));
+                    }
+                    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+                    if (out && (c4 & 7) == 0) g.out_bits[size_t(row2) * g.Dw + (n >> 5)] = w ^ flip_s[n >> 5];
+                } else if (out) {
+                    const int sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int d = n + j;
+                        if (d >= g.D) break;
+                        const int4 pd = __ldg(g.prm + d);
+                        g.out_f32[size_t(d) * g.ldo + row2] = __fadd_rn(__int2float_rn(2 * sv[j] - pd.z), __int_as_float(pd.w));
+                    }
+                }
+            }
+            epi_bar();
+            if (warp == 2 && lane == 0 && atomicAdd(g.sem + 2 * u + 1, 1u) == unsigned(S - 1)) {
+                g.sem[2 * u] = 0;
+                g.sem[2 * u + 1] = 0;
+            }
+        } else if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
+            const int orow = g.pool ? (row >> 2) : row;
+            uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
+            constexpr int H = (NC + 1) / 2;
+            if (H % 4 == 0 && (g.Dw & 3) == 0 && n0 + BN <= g.D) {
+#pragma unroll
+                for (int c = 0; c < NC; c += 4)
+                    if (c >= c_lo && c < c_hi)
+                        *reinterpret_cast<uint4*>(dst + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (c >= c_lo && c < c_hi && n0 + 32 * c < g.D) dst[c] = words[c];
+            }
+        }
+    }
+}
+
+// Activation producers of one stage (warps 6-9), A operand into TMEM; same as the ATM path
+// of fused_layer_kernel, with coherent loads. stage/phase: the shared ring position.
+template <int IN>
+__device__ __forceinline__ void chain_produce(const FusedGeom& g, const int2* ftab, uint64_t* full, uint64_t* empty,
+                                              uint32_t tmem_base, int& stage, uint32_t& phase, int warp, int lane,
+                                              StageClock& sc) {
+    const ChainTiles ct(g);
+    const int tiles = ct.tiles, unit = blockIdx.x, units = gridDim.x;
+    const int r = 32 * (warp & 3) + lane;
+    constexpr int kPF = 3;
+    using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw>::type;
+    int t_ld = unit, kb_ld = unit < tiles ? ct.kb_begin(unit) : 0;
+    int kb_ld_end = unit < tiles ? ct.kb_end(unit) : 0;
+    RowCtx rc;
+    auto set_row = [&]() {
+        int b = 0, oy = 0, ox = 0;
+        rc.valid = t_ld < tiles && decode_row(g, ct.m(t_ld) * kRows + r, b, oy, ox);
+        rc.pix = b * g.H, rc.y0 = oy * g.SH, rc.x0 = ox * g.SW;
+    };
+    set_row();
+    Raw pf[kPF];
+    bool pv[kPF];
+    auto next_load = [&](Raw& dst, bool& v) {
+        v = rc.valid;
+        if constexpr (IN == FIN_BITS) {
+            dst = t_ld < tiles ? load_bits<true>(g, ftab, rc, kb_ld) : make_uint4(0, 0, 0, 0);
+        } else {
+            dst = load_pix<false>(g, ftab, rc);  // the pixel encoder's output: read-only in this launch
+        }
+        if (t_ld < tiles && ++kb_ld == kb_ld_end) {
+            t_ld += units;
+            kb_ld = t_ld < tiles ? ct.kb_begin(t_ld) : 0;
+            kb_ld_end = t_ld < tiles ? ct.kb_end(t_ld) : 0;
+            set_row();
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
+    for (int t = unit; t < tiles; t += units) {
+        const int kb1 = ct.kb_end(t);
+        for (int kb = ct.kb_begin(t); kb < kb1; ++kb) {
+            uint4 u;
+            if constexpr (IN == FIN_BITS)
+                u = pf[0];
+            else
+                u = gather_pix(g, pf[0], pv[0]);
+#pragma unroll
+            for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1], pv[i] = pv[i + 1];
+            next_load(pf[kPF - 1], pv[kPF - 1]);
+            sc.wait(&empty[stage], phase ^ 1, 0);
+            uint32_t v[32];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
+            tc_fence_after();
+            tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(kChainA + stage * 32), v);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+            if (++stage == kStages) stage = 0, phase ^= 1;
+        }
+    }
+}
+
+__device__ __forceinline__ void chain_epilogue_bn(const ChainStage& cs, uint64_t* tfull, uint64_t* tempty,
+                                                  uint32_t tmem_base, const int* tu_s, const uint32_t* flip_s,
+                                                  uint32_t& euse, int warp, int lane, StageClock& sc) {
+    const FusedGeom& g = cs.g;
+#define BNN_CHAIN_EPI(BN, EPI) chain_epilogue<BN, EPI>(g, tfull, tempty, tmem_base, tu_s, flip_s, euse, warp, lane, sc)
+    if (cs.epi == FEPI_BITS) {
+        switch (cs.bn) {
+            case 32: BNN_CHAIN_EPI(32, FEPI_BITS); break;
+            case 64: BNN_CHAIN_EPI(64, FEPI_BITS); break;
+            case 128: BNN_CHAIN_EPI(128, FEPI_BITS); break;
+            default: BNN_CHAIN_EPI(256, FEPI_BITS); break;
+        }
+    } else {
+        switch (cs.bn) {
+            case 32: BNN_CHAIN_EPI(32, FEPI_LOGITS); break;
+            case 64: BNN_CHAIN_EPI(64, FEPI_LOGITS); break;
+            case 128: BNN_CHAIN_EPI(128, FEPI_LOGITS); break;
+            default: BNN_CHAIN_EPI(256, FEPI_LOGITS); break;
+        }
+    }
+#undef BNN_CHAIN_EPI
+}
+
+__global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_constant__ ChainParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sB = smem_raw + (base - raw);  // [kStages][256 * 128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kStages) * 256 * kKB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int2* ftab = reinterpret_cast<int2*>(bars + 32);
+    int* tu_s = reinterpret_cast<int*>(ftab + kMaxQ);
+    uint32_t* flip_s = reinterpret_cast<uint32_t*>(tu_s + kMaxD);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = P.n;
+    // timeline stamp k of stage s: 0 producers passed the hand-off, 1 kernel entry (s = 0),
+    // 2 epilogue finished the stage, 3 TMA issued the stage's last load
+    auto stamp = [&](int s, int k) {
+        if (P.tl) P.tl[(size_t(s) * gridDim.x + blockIdx.x) * 4 + k] = gtimer();
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (threadIdx.x == 0) stamp(0, 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 4 + 1);  // four producer warps + the TMA thread
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0)
+        for (int s = 0; s < n; ++s) tma_prefetch(&P.st[s].tm);
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ weight TMA, all stages
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            StageClock sc;
+            for (int s = 0; s < n; ++s) {
+                const ChainStage& cs = P.st[s];
+                const ChainTiles ct(cs.g);
+                const uint32_t bytes = uint32_t(cs.bn) * kKB;
+                for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x) {
+                    const int nt = ct.n(t), kb1 = ct.kb_end(t);
+                    for (int kb = ct.kb_begin(t); kb < kb1; ++kb) {
+                        sc.wait(&empty[stage], phase ^ 1, 0);
+                        mbar_arrive_expect_tx(&full[stage], bytes);
+                        tma_load_2d(&cs.tm, &full[stage], sB + size_t(stage) * 256 * kKB, kb * kKB, nt * cs.bn);
+                        if (++stage == kStages) stage = 0, phase ^= 1;
+                    }
+                }
+                sc.flush(P.dbg, s, 0, true);
+                stamp(s, 3);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ UMMA issuer, all stages
+        int stage = 0;
+        uint32_t phase = 0;
+        uint32_t ause = 0;  // bit a: tempty parity of accumulator slot a
+        StageClock sc;
+        for (int s = 0; s < n; ++s) {
+            const ChainStage& cs = P.st[s];
+            const ChainTiles ct(cs.g);
+            const uint32_t idesc = idesc_i8(kRows, cs.bn);
+            const int kAcc = cs.bn <= 128 ? 2 : 1;
+            int i = 0;
+            for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x, ++i) {
+                const int acc = kAcc == 2 ? (i & 1) : 0;
+                sc.wait(&tempty[acc], ((ause >> acc) & 1u) ^ 1u, 0);
+                ause ^= 1u << acc;
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
+                const int kb0 = ct.kb_begin(t), kb1 = ct.kb_end(t);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    sc.wait(&full[stage], phase, 1);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t b0 = smem_u32(sB + size_t(stage) * 256 * kKB);
+#pragma unroll
+                        for (int k = 0; k < kKB / 32; ++k)
+                            mma_i8_ts(d_tmem, tmem_base + uint32_t(kChainA + stage * 32 + 8 * k), sdesc_k_sw128(b0 + 32 * k),
+                                      idesc, (kb != kb0 || k != 0));
+                        mma_commit(&empty[stage]);
+                        if (kb == kb1 - 1) mma_commit(&tfull[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+            sc.flush(P.dbg, s, 1, lane == 0);
+        }
+    } else if (warp < 6 || warp >= 10) {
+        // ------------------------------------------------------ epilogue, all stages
+        const int ew = warp < 6 ? warp - 2 : warp - 6;  // 0..7
+        const int et = ew * 32 + lane;
+        uint32_t euse = 0;
+        StageClock sc;
+        for (int s = 0; s < n; ++s) {
+            const ChainStage& cs = P.st[s];
+            const FusedGeom& g = cs.g;
+            const long long tb = dclock();
+            epi_bar();  // every epilogue warp is done with the previous stage's tables
+            if (cs.epi == FEPI_BITS) {
+                const int dp = g.n_tiles * cs.bn;
+                for (int d = et; d < dp; d += 256) tu_s[d] = __ldg(g.prm + d).x;
+                for (int d0 = ew * 32; d0 < dp; d0 += 256) {
+                    const uint32_t f = __ballot_sync(0xffffffffu, __ldg(g.prm + d0 + lane).y != 0);
+                    if (lane == 0) flip_s[d0 >> 5] = f;
+                }
+            }
+            epi_bar();
+            sc.w1 += dclock() - tb;
+            chain_epilogue_bn(cs, tfull, tempty, tmem_base, tu_s, flip_s, euse, warp, lane, sc);
+            if (s + 1 < n) {  // publish: this CTA's outputs of stage s are written
+                __threadfence();
+                epi_bar();
+                if (ew == 0 && lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.done + s) : "memory");
+            }
+            sc.flush(P.dbg, s, 2, ew == 0 && lane == 0);
+            if (ew == 0 && lane == 0) stamp(s, 2);
+        }
+    } else {
+        // ------------------------------------------------------ activation producers, all stages
+        int stage = 0;
+        uint32_t phase = 0;
+        const int pt = threadIdx.x - 6 * 32;  // 0..127
+        StageClock sc;
+        for (int s = 0; s < n; ++s) {
+            const ChainStage& cs = P.st[s];
+            const FusedGeom& g = cs.g;
+            const long long tb = dclock();
+            if (s == 0) {
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // the input encoder's output
+            } else if (pt == 0) {
+                unsigned seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(P.done + s - 1) : "memory");
+                } while (seen < gridDim.x);
+            }
+            prod_bar();  // the previous stage's producers are done with ftab; stage s-1 is complete
+            sc.w1 += dclock() - tb;
+            if (pt == 0) stamp(s, 0);
+            if (cs.in_mode == FIN_BITS) {
+                const int kw_total = g.K >> 5;
+                for (int q = pt; q < 4 * g.KB; q += 128) {
+                    int2 e = make_int2(0, -1);
+                    if (q < kw_total) {
+                        const int tap = q / g.Cw, cw = q - tap * g.Cw, ky = tap / g.KW, kx = tap - ky * g.KW;
+                        e = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), cw);
+                    }
+                    ftab[q] = e;
+                }
+            } else {
+                for (int tap = pt; tap < g.KH * g.KW; tap += 128) {
+                    const int ky = tap / g.KW, kx = tap - ky * g.KW;
+                    ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
+                }
+            }
+            prod_bar();
+            if (cs.in_mode == FIN_BITS)
+                chain_produce<FIN_BITS>(g, ftab, full, empty, tmem_base, stage, phase, warp, lane, sc);
+            else
+                chain_produce<FIN_PIX>(g, ftab, full, empty, tmem_base, stage, phase, warp, lane, sc);
+            sc.flush(P.dbg, s, 3, pt == 0);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem_base);
+    if (threadIdx.x == 0) {  // the last CTA out re-arms the stage counters for the next launch
+        __threadfence();
+        if (atomicAdd(P.done + kChainMaxStages, 1u) == gridDim.x - 1) {
+            for (int s = 0; s <= kChainMaxStages; ++s) P.done[s] = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -842,12 +1418,14 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms() / CG) * CG;
     static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
     FusedGeom gd = g;
+    gd.tl = fused_timeline_slot(1);
+    if (gd.tl) g_tl_names.push_back("layer BN=" + std::to_string(BN) + " D=" + std::to_string(g.D) + " KB=" + std::to_string(g.KB));
     unsigned long long* dbg = nullptr;
     if (prof) {
         BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
         BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
         gd.dbg = dbg;
-        gd.dbg_mode = prof >> 1;  // 2: producer skips its stores, 4: epilogue skips its math
+        gd.dbg_mode = prof >> 1;  // 3: producer skips its stores, 5: epilogue skips its math, 17: no wait::st
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
@@ -937,7 +1515,108 @@ int fused_set_tmem_a(int enabled) {
     return BNN_OK;
 }
 
-int fused_tmem_a() { return g_atmem != 0; }
+int fused_tmem_a() {
+    if (g_atmem < 0) g_atmem = getenv("BNN_FUSED_TMEM_A") ? atoi(getenv("BNN_FUSED_TMEM_A")) : 1;
+    return g_atmem != 0;
+}
+
+unsigned long long* fused_timeline_slot(int slots) {
+    if (g_tl_used < 0 || g_tl_used + slots > kTlSlots) return nullptr;
+    unsigned long long* p = g_tl + size_t(g_tl_used) * kTlCtas * 4;
+    g_tl_used += slots;
+    return p;
+}
+
+int fused_timeline(int op) {
+    if (op == 1) {
+        if (!g_tl) BNN_CUDA(cudaMalloc(&g_tl, size_t(kTlSlots) * kTlCtas * 4 * sizeof(unsigned long long)));
+        BNN_CUDA(cudaMemset(g_tl, 0, size_t(kTlSlots) * kTlCtas * 4 * sizeof(unsigned long long)));
+        g_tl_used = 0;
+        g_tl_names.clear();
+        return BNN_OK;
+    }
+    if (g_tl_used < 0) return BNN_OK;
+    BNN_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(size_t(kTlSlots) * kTlCtas * 4);
+    BNN_CUDA(cudaMemcpy(h.data(), g_tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (auto v : h)
+        if (v && v < t0) t0 = v;
+    for (int sl = 0; sl < g_tl_used; ++sl) {
+        double mn[4], md[4], mx[4];
+        for (int k = 0; k < 4; ++k) {
+            std::vector<double> v;
+            for (int c = 0; c < kTlCtas; ++c) {
+                const unsigned long long x = h[(size_t(sl) * kTlCtas + c) * 4 + k];
+                if (x) v.push_back((x - t0) * 1e-3);
+            }
+            std::sort(v.begin(), v.end());
+            mn[k] = v.empty() ? -1 : v.front();
+            md[k] = v.empty() ? -1 : v[v.size() / 2];
+            mx[k] = v.empty() ? -1 : v.back();
+        }
+        fprintf(stderr, "[timeline %2d %-28s] us: k0 %7.1f/%7.1f/%7.1f | k1 %7.1f/%7.1f/%7.1f | k2 %7.1f/%7.1f/%7.1f | k3 %7.1f/%7.1f/%7.1f\n",
+                sl, sl < int(g_tl_names.size()) ? g_tl_names[sl].c_str() : "", mn[0], md[0], mx[0], mn[1], md[1], mx[1],
+                mn[2], md[2], mx[2], mn[3], md[3], mx[3]);
+    }
+    g_tl_used = -1;
+    return BNN_OK;
+}
+
+static int launch_chain_impl(const ChainParams& p, cudaStream_t s);
+
+int launch_chain(const ChainParams& p0, cudaStream_t s) {
+    ChainParams p = p0;
+    p.tl = fused_timeline_slot(p.n);
+    for (int i = 0; p.tl && i < p.n; ++i) g_tl_names.push_back("chain stage " + std::to_string(i));
+    return launch_chain_impl(p, s);
+}
+
+static int launch_chain_impl(const ChainParams& p, cudaStream_t s) {
+    static_assert(sizeof(ChainParams) <= 4096, "kernel parameter space");
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(fused_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
+        attr_set = true;
+    }
+    set_last_gemm("fused_chain_umma_i8");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(num_sms()));  // one CTA per SM, all co-resident (stage hand-off spins)
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kChainSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
+    if (!prof) {
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, fused_chain_kernel, p));
+        return launch_check("fused_chain_kernel");
+    }
+    ChainParams q = p;
+    const size_t nd = size_t(kChainMaxStages) * 16;
+    BNN_CUDA(cudaMalloc(&q.dbg, nd * sizeof(unsigned long long)));
+    BNN_CUDA(cudaMemset(q.dbg, 0, nd * sizeof(unsigned long long)));
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, fused_chain_kernel, q));
+    BNN_TRY(launch_check("fused_chain_kernel"));
+    std::vector<unsigned long long> h(nd);
+    BNN_CUDA(cudaMemcpy(h.data(), q.dbg, nd * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    cudaFree(q.dbg);
+    const double g = double(num_sms());
+    for (int s = 0; s < p.n; ++s) {
+        const unsigned long long* d = h.data() + s * 16;
+        fprintf(stderr,
+                "[chain stage %d BN=%d in=%d epi=%d rows=%d D=%d KB=%d S=%d] per-CTA kcycles: tma %.1f (wait %.1f) | "
+                "mma %.1f (wait-acc %.1f wait-full %.1f) | epi %.1f (wait-acc %.1f tables %.1f) | prod %.1f (wait-slot %.1f "
+                "wait-dep %.1f)\n",
+                s, p.st[s].bn, p.st[s].in_mode, p.st[s].epi, p.st[s].g.rows, p.st[s].g.D, p.st[s].g.KB, p.st[s].g.ksplit,
+                d[3] / g / 1e3, d[0] / g / 1e3, d[7] / g / 1e3, d[4] / g / 1e3, d[5] / g / 1e3, d[11] / g / 1e3,
+                d[8] / g / 1e3, d[9] / g / 1e3, d[15] / g / 1e3, d[12] / g / 1e3, d[13] / g / 1e3);
+    }
+    return BNN_OK;
+}
 
 int launch_fused(int cg, int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;

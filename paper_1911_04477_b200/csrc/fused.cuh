@@ -34,8 +34,28 @@ struct FusedGeom {
     unsigned* sem;            // split-K counters, 2 per output tile, zero between launches
     int ws_rows, ws_ld;
     unsigned long long* dbg;  // profiling counters (BNN_FUSED_PROFILE=1), else null
-    int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math
+    int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math, 8 no wait::st
+    unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
 };
+
+// Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.
+constexpr int kChainMaxStages = 10;
+struct ChainStage {
+    CUtensorMap tm;  // weight map with box rows = bn
+    FusedGeom g;
+    int bn, in_mode, epi, pad;
+};
+struct ChainParams {
+    ChainStage st[kChainMaxStages];
+    int n;
+    unsigned* done;  // [kChainMaxStages + 1] stage-completion counters, zero between launches
+    unsigned long long* dbg;  // per-stage role clocks (BNN_FUSED_PROFILE=1), else null
+    unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [n][grid][4], else null
+};
+// Debug timeline (globaltimer stamps per CTA and launch): op 1 enable + reset, 2 print + disable.
+int fused_timeline(int op);
+unsigned long long* fused_timeline_slot(int slots);
+int launch_chain(const ChainParams& p, cudaStream_t s);
 
 int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
                        int Kpad, int8_t* out, cudaStream_t s);
@@ -43,6 +63,7 @@ int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const fl
                       const float* shift, int4* prm, int* bad_dev, cudaStream_t s);
 int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN);
 int fused_set_tmem_a(int enabled);
+int fused_tmem_a();
 int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s);
 // cg = 1: CTA-local M=128 tiles; cg = 2: CTA pairs with cta_group::2 M=256 tiles. tm must be
 // the weight map whose box has BN / cg rows.

@@ -20,6 +20,8 @@
 #include <vector>
 
 #include "bnn_common.cuh"
+#include <cstring>
+
 #include "fused.cuh"
 
 namespace bnnk {
@@ -139,6 +141,7 @@ struct bnn_net {
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix, ws, sem;
+    bnnk::DevBuf chain_done;  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
 };
 
 namespace bnnk {
@@ -509,6 +512,13 @@ int forward_generic(bnn_net* net, const float* x, size_t B, float* logits, cudaS
 }
 
 
+// bnn_set_fused_chain / BNN_FUSED_CHAIN: 1 one chained launch, 0 (default) one launch per
+// weighted layer. The chained kernel removes the ~3-4 us launch boundaries but its stages run
+// slower (one register allocation for all roles and stage shapes, 128 per thread), so at
+// the measured batches the per-layer launches win (profiles/r01_chain_*).
+int g_chain = -1;
+int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -518,9 +528,19 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         net->bits_batch = B;
         ++net->arena_epoch;
     }
+    if (g_chain < 0) g_chain = getenv("BNN_FUSED_CHAIN") ? atoi(getenv("BNN_FUSED_CHAIN")) : 0;
+    if (g_chain_tail < 0) g_chain_tail = getenv("BNN_FUSED_CHAIN_TAIL") ? atoi(getenv("BNN_FUSED_CHAIN_TAIL")) : 0;
+    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
+    // per-stage launch geometry (batch-dependent fields, tiling, buffers)
+    struct Plan {
+        FusedGeom g;
+        int cg, bn;
+    };
+    std::vector<Plan> plans;
     const void* in = x;
     int which = 0;
-    size_t launches = 0;
+    (void)prof;
+    const bool chain_ok = !net->timing && fused_tmem_a();
     for (auto& stp : net->stages) {
         FusedStage& st = *stp;
         FusedGeom g = st.g;
@@ -558,18 +578,65 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             g.out_f32 = logits;
             g.ldo = int(B);
         }
+        if (st.in_mode == FIN_PIX) g.in = net->pix.as<uint32_t>();
+        plans.push_back({g, cg, bn});
+        in = g.out_bits;
+    }
+    // Chained tail: stages [first_chained, n) run in ONE persistent launch (fused_chain_kernel),
+    // the ones before it one launch each. g_chain = 1 chains every stage; g_chain_tail = 1 only
+    // the trailing run of linear stages (short, launch-latency-bound at inference batches).
+    // Both are off by default: measured slower than one launch per layer.
+    auto chain_stage_ok = [&](size_t i) {
+        const FusedStage& st = *net->stages[i];
+        return chain_ok && plans[i].cg == 1 && st.in_mode != FIN_F32 && st.epi != FEPI_NCHW;
+    };
+    size_t first_chained = plans.size();
+    while (first_chained > 0 && chain_stage_ok(first_chained - 1) &&
+           (g_chain != 0 || net->layers[net->stages[first_chained - 1]->layer]->spec.kind == BNN_LAYER_LINEAR) &&
+           plans.size() - first_chained < size_t(kChainMaxStages))
+        --first_chained;
+    if (g_chain_tail == 0 && g_chain == 0) first_chained = plans.size();
+    if (plans.size() - first_chained < 2 && g_chain == 0) first_chained = plans.size();  // nothing to save
+    size_t launches = 0;
+    for (size_t i = 0; i < first_chained; ++i) {
+        FusedStage& st = *net->stages[i];
+        const FusedGeom& g = plans[i].g;
         EventPair layer_ev(net, st.layer, 0, s);
         if (st.in_mode == FIN_PIX) {  // first-layer sign bits, one word per pixel
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
-            g.in = net->pix.as<uint32_t>();
             ++launches;
         }
         EventPair gemm_ev(net, st.layer, 1, s);
-        BNN_TRY(launch_fused(cg, bn, st.in_mode, st.epi, st.tm[box_index(bn / cg)], g, s));
+        BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
         gemm_ev.close();
         layer_ev.close();
         ++launches;
-        in = g.out_bits;
+    }
+    if (first_chained < plans.size()) {
+        if (!net->chain_done.p) {
+            BNN_TRY(net->chain_done.alloc((kChainMaxStages + 1) * sizeof(unsigned)));
+            BNN_CUDA(cudaMemsetAsync(net->chain_done.p, 0, (kChainMaxStages + 1) * sizeof(unsigned), s));
+        }
+        const FusedStage& first = *net->stages[first_chained];
+        if (first.in_mode == FIN_PIX) {
+            BNN_TRY(launch_pack_pixels(x, B, first.g.C, size_t(first.g.H) * first.g.W, net->pix.as<uint32_t>(), s));
+            ++launches;
+        }
+        ChainParams cp;
+        memset(&cp, 0, sizeof cp);
+        cp.n = int(plans.size() - first_chained);
+        cp.done = net->chain_done.as<unsigned>();
+        for (size_t i = first_chained; i < plans.size(); ++i) {
+            const FusedStage& st = *net->stages[i];
+            ChainStage& c = cp.st[i - first_chained];
+            c.tm = st.tm[box_index(plans[i].bn)];
+            c.g = plans[i].g;
+            c.bn = plans[i].bn;
+            c.in_mode = st.in_mode;
+            c.epi = st.epi;
+        }
+        BNN_TRY(launch_chain(cp, s));
+        ++launches;
     }
     net->last_launches = launches;
     return BNN_OK;
@@ -743,6 +810,14 @@ int bnn_set_fused_split(int split) {
         return fail(BNN_E_CONFIG, "fused split: 0 (auto), 1 (off) or a power of two <= 16");
     g_forced_split = split;
     ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_debug_timeline(int op) { return fused_timeline(op); }
+
+int bnn_set_fused_chain(int enabled) {
+    g_chain = enabled ? 1 : 0;
+    ++g_tiling_epoch;  // captured graphs hold the other launch sequence
     return BNN_OK;
 }
 

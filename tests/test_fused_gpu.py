@@ -43,20 +43,29 @@ FUSABLE = {
 }
 
 
-@pytest.fixture(params=["auto", "smem_a", "cg1", "cg2", "nosplit", "split16"])
+# tilings that run all stages in one chained launch (the others: one launch per weighted layer)
+CHAINED = {"chain", "chain_nosplit", "chain_split16"}
+
+
+@pytest.fixture(params=["auto", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+                        "chain_split16"])
 def tiling(bnn, request):
-    """Every fused test runs with the automatic tile choice (A operand in TMEM, split-K for the
-    small-batch linear layers), with the A operand staged in shared memory, with each
-    cta_group forced, and with split-K off / forced to 16."""
+    """Every fused test runs with the automatic tile choice (one launch per weighted layer,
+    A operand in TMEM, split-K for the small-batch linear layers), with all stages chained in
+    one persistent launch, with the A operand staged in shared memory, with each cta_group
+    forced, and with split-K off / forced to 16 (per-layer and chained)."""
     lib = bnn.load()
     p = request.param
     bnn._lib.check(lib.bnn_set_fused_tiling({"cg1": 1, "cg2": 2}.get(p, 0), 0))
     bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if p == "smem_a" else 1))
-    bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16}.get(p, 0)))
+    bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16, "chain_nosplit": 1,
+                                            "chain_split16": 16}.get(p, 0)))
+    bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_tmem_a(1)
     lib.bnn_set_fused_split(0)
+    lib.bnn_set_fused_chain(0)
 
 
 @pytest.fixture
@@ -70,15 +79,16 @@ def fused(bnn, tiling):
 
 
 @pytest.mark.parametrize("batch", [1, 2, 3, 5, 33, 128, 129])
-def test_default_network_fused_vs_oracle(bnn, orc, fused, batch):
+def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     net = fused()
     x = orc.fill_random((batch, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     got = net.forward(x)
-    assert net.last_launches() == 10  # first-layer pixel encoder + one launch per weighted layer
+    # first-layer pixel encoder + one launch per weighted layer (10), or + one chained launch (2)
+    assert net.last_launches() == (2 if tiling in CHAINED else 10)
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 
-@pytest.mark.parametrize("mode", ["cg1_tmem", "cg1_smem", "cg2"])
+@pytest.mark.parametrize("mode", ["chain", "cg1_tmem", "cg1_smem", "cg2"])
 @pytest.mark.parametrize("bn", [32, 64, 128, 256])
 def test_forced_tile_shapes_vs_oracle(bnn, orc, mode, bn):
     lib = bnn.load()
@@ -88,10 +98,12 @@ def test_forced_tile_shapes_vs_oracle(bnn, orc, mode, bn):
     try:
         bnn._lib.check(lib.bnn_set_fused_tiling(2 if mode == "cg2" else 1, bn))
         bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if mode == "cg1_smem" else 1))
+        bnn._lib.check(lib.bnn_set_fused_chain(1 if mode == "chain" else 0))
         got = net.forward(x)
     finally:
         lib.bnn_set_fused_tiling(0, 0)
         lib.bnn_set_fused_tmem_a(1)
+        lib.bnn_set_fused_chain(0)
     assert np.array_equal(got, orc.net(seed=1).forward(x)), (mode, bn)
 
 

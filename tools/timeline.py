@@ -1,0 +1,34 @@
+"""Launch timeline of the fused engine (bnn_debug_timeline): per launch / chain stage, the
+min/median/max over CTAs of four globaltimer stamps, in us from the first stamp.
+
+    python tools/timeline.py [B] [chain 0|1]
+Per-layer launches: k0 entry, k1 setup done, k2 griddepcontrol.wait returned, k3 exit.
+Chain stages: k0 producers passed the hand-off, k1 kernel entry, k2 epilogue done, k3 TMA done.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1911_04477_b200 as bnn  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+lib = bnn.load()
+if len(sys.argv) > 2:
+    lib.bnn_set_fused_chain(int(sys.argv[2]))
+net = bnn.Network(seed=1)
+s = torch.cuda.current_stream().cuda_stream  # legacy stream: eager launches (no graph)
+x = torch.empty((B, 3, 32, 32), dtype=torch.float32, device="cuda")
+bnn._lib.check(lib.bnn_fill_random_f32(bnn.mix64(1, 0x696E707574), 0, x.numel(), x.data_ptr(), s))
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+for _ in range(3):
+    net.forward_device(x)
+torch.cuda.synchronize()
+flush.fill_(1.0)
+torch.cuda.synchronize()
+lib.bnn_debug_timeline(1)
+net.forward_device(x)
+lib.bnn_debug_timeline(2)
+torch.cuda.synchronize()
+print("ok", B, net.engine, lib.bnn_last_gemm_kernel().decode())
