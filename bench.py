@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--sweep", default="1,64,1024,4096,16384", help="batch sweep (N=1 only)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config section (cfg1/2/4, K1/K2)")
     return ap.parse_args()
 
 
@@ -166,6 +167,210 @@ def int8_tensor_peak(dev):
             return 2 * pk["bf16_tflops"], f"2 x MEASURED_PEAKS bf16_tflops (int8 GEMM probe failed: {e})"
         except Exception:
             return 2 * 1590.0, "2 x fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------ per-config section (N=1)
+
+FC_STACK = [{"kind": "linear", "out_features": 4096}, {"kind": "linear", "out_features": 4096},
+            {"kind": "linear", "out_features": 1000}]  # BASELINE.json configs[3]
+
+
+def _dev_time(fn, st, flush, iters):
+    """Mean ms of fn() over iters runs on stream st, each timed with CUDA events and preceded by
+    an L2 flush (a 256 MiB write outside the events)."""
+    import torch
+
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            fn()
+        st.synchronize()
+        tot = 0.0
+        for i in range(iters):
+            flush.fill_(float(i))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            st.synchronize()
+            tot += e0.elapsed_time(e1)
+    return tot / iters
+
+
+def measure_configs(lib, dev, st, flush, seed, peak, cpu):
+    """BASELINE.json's other named shapes on this GPU (device-resident inputs, L2 flushed before
+    every timed call), the HBM-bound encoders' achieved bandwidth, and the K3 pipe probes; with
+    the unmodified reference CPU path timed on the same shapes when cpu is set."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_1911_04477_b200 as bnn
+    from paper_1911_04477_b200 import _lib
+
+    S = st.cuda_stream
+    out = {}
+    hbm = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        hbm, hbm_src = 7700.0, "fallback 7.7 TB/s (B200_PROFILING.md)"
+
+    def fill(shape, sd):
+        t = torch.empty(shape, dtype=torch.float32, device=dev)
+        _lib.check(lib.bnn_fill_random_f32(sd, 0, t.numel(), t.data_ptr(), S))
+        return t
+
+    def packed_rows(M, K, sd):
+        w = fill((M, K), sd)
+        wpl = (K + 31) // 32
+        pw = torch.empty((M, wpl), dtype=torch.int32, device=dev)
+        _lib.check(lib.bnn_sign_pack_rows_f32(w.data_ptr(), M, K, pw.data_ptr(), wpl, S))
+        return pw, wpl
+
+    ref = None
+    if cpu:
+        try:
+            from oracle import RefLib
+
+            ref = RefLib()
+        except Exception as e:
+            out["cpu_reference"] = f"unavailable: {e}"
+    cores = os.cpu_count() or 1
+
+    def cpu_ms(fn, reps=3):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return 1e3 * (time.perf_counter() - t0) / reps
+
+    # cfg1: single binary linear layer, encode + xnor GEMM (+ bias), M = N = K = 1024
+    M = N = K = 1024
+    x = fill((K, N), bnn.mix64(seed, 11))
+    pw, wpl = packed_rows(M, K, bnn.mix64(seed, 12))
+    bias = fill((M,), bnn.mix64(seed, 13))
+    y = torch.empty((M, N), dtype=torch.float32, device=dev)
+    lines = torch.empty((N, wpl), dtype=torch.int32, device=dev)
+    acc = torch.empty((M, N), dtype=torch.int32, device=dev)
+    f_lin = lambda: _lib.check(lib.bnn_linear_forward_packed_f32(x.data_ptr(), K, N, pw.data_ptr(), wpl, M,
+                                                                 bias.data_ptr(), y.data_ptr(), S))
+    f_enc = lambda: _lib.check(lib.bnn_sign_pack_cols_f32(x.data_ptr(), K, N, lines.data_ptr(), wpl, S))
+    f_gemm = lambda: _lib.check(lib.bnn_xnor_gemm_s32(pw.data_ptr(), wpl, lines.data_ptr(), wpl, M, N, K,
+                                                      acc.data_ptr(), N, S))
+    ms = _dev_time(f_lin, st, flush, 20)
+    gemm_kernel = lib.bnn_last_gemm_kernel().decode()
+    ms_enc = _dev_time(f_enc, st, flush, 20)
+    ms_gemm = _dev_time(f_gemm, st, flush, 20)
+    bops = 2.0 * M * N * K
+    c1 = {"shape": "linear_forward_packed x[1024,1024] f32, W 1024x1024 packed (BASELINE configs[0])",
+          "ms": ms, "binary_tops": bops / (ms * 1e-3) / 1e12, "gemm_kernel": gemm_kernel,
+          "encode_ms": ms_enc, "xnor_gemm_ms": ms_gemm, "xnor_gemm_tops": bops / (ms_gemm * 1e-3) / 1e12,
+          "xnor_gemm_frac_of_int8_peak": (bops / (ms_gemm * 1e-3) / 1e12) / peak if peak else None}
+    if ref is not None:
+        xh = x.cpu().numpy()
+        ph = pw.cpu().numpy().view(np.uint32)
+        bh = bias.cpu().numpy()
+        c1["cpu_reference_ms"] = cpu_ms(lambda: ref.linear_forward_packed(xh, ph, bh, threads=cores))
+        c1["cpu_reference_threads"] = cores
+        c1["parity_vs_reference"] = bool(np.array_equal(y.cpu().numpy(), ref.linear_forward_packed(xh, ph, bh)))
+    out["cfg1_linear_1024"] = c1
+
+    # cfg2: binary 3x3 conv 64 -> 64 on 32x32, batch 1 (encode + im2col + xnor GEMM + epilogue)
+    g = _lib.ConvGeom(3, 3, 1, 1, 1, 1, 64, 64)
+    xc = fill((1, 64, 32, 32), bnn.mix64(seed, 21))
+    pwc, wplc = packed_rows(64, 576, bnn.mix64(seed, 22))
+    bc = fill((64,), bnn.mix64(seed, 23))
+    yc = torch.empty((1, 64, 32, 32), dtype=torch.float32, device=dev)
+    f_conv = lambda: _lib.check(lib.bnn_conv_forward_binary_f32(xc.data_ptr(), 1, 64, 32, 32, pwc.data_ptr(), wplc,
+                                                                bc.data_ptr(), C.byref(g), yc.data_ptr(), S))
+    ms = _dev_time(f_conv, st, flush, 30)
+    c2 = {"shape": "conv_forward_binary x[1,64,32,32], 3x3 pad 1, D=64 (BASELINE configs[1])", "ms": ms,
+          "binary_tops": 2.0 * 64 * 576 * 1024 / (ms * 1e-3) / 1e12, "gemm_kernel": lib.bnn_last_gemm_kernel().decode(),
+          "note": "75.5 M bops: launch-latency bound"}
+    if ref is not None:
+        xh, ph, bh = xc.cpu().numpy(), pwc.cpu().numpy().view(np.uint32), bc.cpu().numpy()
+        geo = [3, 3, 1, 1, 1, 1, 64, 64]
+        c2["cpu_reference_ms"] = cpu_ms(lambda: ref.conv_forward_binary(xh, ph, bh, geo, threads=cores), reps=10)
+        c2["cpu_reference_threads"] = cores
+        c2["parity_vs_reference"] = bool(np.array_equal(yc.cpu().numpy(), ref.conv_forward_binary(xh, ph, bh, geo)))
+    out["cfg2_conv_64_32x32_b1"] = c2
+
+    # cfg4: AlexNet-sized binary FC stack 9216 -> 4096 -> 4096 -> 1000, batch 1024
+    Bf = 1024
+    net = bnn.Network(FC_STACK, (9216, 1, 1), seed)
+    xf = fill((Bf, 9216, 1, 1), bnn.mix64(seed, INPUT_STREAM))
+    yf = torch.empty((1000, Bf), dtype=torch.float32, device=dev)
+    ms = _dev_time(lambda: net.forward_device(xf, yf, S), st, flush, 20)
+    fc_bops = 2.0 * Bf * (9216 * 4096 + 4096 * 4096 + 4096 * 1000)
+    c4 = {"shape": "NetworkSpec [1024, 9216, 1, 1] -> linear 4096 -> 4096 -> 1000 (BASELINE configs[3])",
+          "ms": ms, "images_per_s": Bf / (ms * 1e-3), "binary_tops": fc_bops / (ms * 1e-3) / 1e12,
+          "frac_of_int8_peak": (fc_bops / (ms * 1e-3) / 1e12) / peak if peak else None,
+          "engine": net.engine, "launches": net.last_launches()}
+    if ref is not None:
+        import tempfile
+
+        spec = {"input_shape": [1, 9216, 1, 1], "seed": seed, "binarize_weights": False, "kernel": "binary",
+                "layers": FC_STACK}
+        with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as fh:
+            json.dump(spec, fh)
+            path = fh.name
+        try:
+            rnet = ref.net_file(path)
+            nb = 64  # bounded sample: the reference's linear layers cost the same per image
+            xh = xf[:nb].cpu().numpy()
+            t0 = time.perf_counter()
+            want = rnet.forward(xh, threads=cores)
+            dt = time.perf_counter() - t0
+            c4["cpu_reference_images_per_s"] = nb / dt
+            c4["cpu_reference_threads"] = cores
+            c4["cpu_reference_sample"] = f"{nb} images"
+            c4["parity_vs_reference"] = bool(np.array_equal(yf[:, :nb].cpu().numpy(), want))
+        finally:
+            os.unlink(path)
+    out["cfg4_fc_stack_b1024"] = c4
+    del xf, yf, net
+
+    # K1 encoder, HBM-bound: pack_cols(sign(X)) of a 1 GiB float matrix (> L2)
+    Lk, Nk = 16384, 16384
+    xe = torch.empty((Lk, Nk), dtype=torch.float32, device=dev)
+    _lib.check(lib.bnn_fill_random_f32(bnn.mix64(seed, 31), 0, xe.numel(), xe.data_ptr(), S))
+    wple = Lk // 32
+    le = torch.empty((Nk, wple), dtype=torch.int32, device=dev)
+    ms = _dev_time(lambda: _lib.check(lib.bnn_sign_pack_cols_f32(xe.data_ptr(), Lk, Nk, le.data_ptr(), wple, S)),
+                   st, flush, 5)
+    byt = Lk * Nk * 4 + Nk * wple * 4
+    msr = _dev_time(lambda: _lib.check(lib.bnn_sign_pack_rows_f32(xe.data_ptr(), Lk, Nk, le.data_ptr(), wple, S)),
+                    st, flush, 5)
+    out["k1_sign_pack"] = {"shape": "float [16384, 16384] (1 GiB) -> packed", "bytes": byt,
+                           "cols_ms": ms, "cols_gbs": byt / (ms * 1e-3) / 1e9, "cols_frac_hbm": byt / (ms * 1e-3) / 1e9 / hbm,
+                           "rows_ms": msr, "rows_gbs": byt / (msr * 1e-3) / 1e9,
+                           "rows_frac_hbm": byt / (msr * 1e-3) / 1e9 / hbm, "hbm_peak_gbs": hbm, "peak_source": hbm_src}
+    del xe, le
+
+    # K2 binary im2col: x [256, 128, 32, 32] (128 MiB, > L2) -> packed K = 1152 lines
+    g2 = _lib.ConvGeom(3, 3, 1, 1, 1, 1, 128, 128)
+    xi = torch.empty((256, 128, 32, 32), dtype=torch.float32, device=dev)
+    _lib.check(lib.bnn_fill_random_f32(bnn.mix64(seed, 41), 0, xi.numel(), xi.data_ptr(), S))
+    li = torch.empty((256 * 1024, 36), dtype=torch.int32, device=dev)
+    ms = _dev_time(lambda: _lib.check(lib.bnn_im2col_sign_pack_f32(xi.data_ptr(), 256, 128, 32, 32, C.byref(g2),
+                                                                   li.data_ptr(), 36, S)), st, flush, 5)
+    byt = xi.numel() * 4 + li.numel() * 4
+    out["k2_im2col_sign_pack"] = {"shape": "x [256,128,32,32] f32 -> 262144 lines x 36 words", "bytes": byt, "ms": ms,
+                                  "gbs": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / hbm,
+                                  "note": "algorithmic bytes = input once + packed output"}
+    del xi, li
+
+    # K3 pipe candidates (SURVEY.md §7 hard part 1): LOP3+POPC vs emulated b1 mma.sync vs int8 UMMA
+    a, b = C.c_double(), C.c_double()
+    _lib.check(lib.bnn_probe_popc_peak(C.byref(a), C.byref(b), S))
+    popc = a.value / 1e12
+    _lib.check(lib.bnn_probe_bmma_peak(C.byref(a), C.byref(b), S))
+    bmma = a.value / 1e12
+    out["k3_pipes_tbops"] = {"popc_lop3": popc, "b1_mma_sync_emulated": bmma, "int8_tcgen05_cublaslt": peak,
+                             "chosen": "int8 tcgen05 (kind::i8) for the fused engine and large xnor_gemm"}
+    return out
 
 
 # ---------------------------------------------------------------------- ours
@@ -370,6 +575,13 @@ def run_ours(args):
         except Exception as e:  # the checker must never break the benchmark line
             parity = f"oracle unavailable: {e}"
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            configs = measure_configs(lib, dev, st, flush, args.seed, peak, not args.no_cpu_baseline)
+        except Exception as e:  # never lose the headline line to the side section
+            configs = {"error": f"{type(e).__name__}: {e}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -416,6 +628,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "batch_sweep_images_per_s": sweep,
+            "configs": configs,
             "parity_vs_oracle": parity,
         }
         print(json.dumps(line), flush=True)

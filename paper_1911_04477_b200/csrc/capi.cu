@@ -40,6 +40,16 @@ int probe(int dev) {
         if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return -1;
         g_sms[dev] = p.multiProcessorCount;
         g_arch_ok[dev] = (p.major == 10 && p.minor == 0) ? 1 : -1;
+        if (g_arch_ok[dev] == 1) {
+            // Stream-ordered scratch (Scratch: im2col lines, unpacked operands) comes from the
+            // device's default memory pool. Its default release threshold (0) hands the memory
+            // back at every synchronize, so the next cudaMallocAsync remaps it (~ms). Keep it.
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        }
     }
     return g_arch_ok[dev];
 }
@@ -88,12 +98,13 @@ namespace {
 int g_policy = BNN_GEMM_AUTO;
 
 // Size rule: the tensor-core path pays an unpack pass
-// (1 bit -> 1 byte per operand element) and a ~4-6 us launch floor; below ~2^27 bit-MACs the
-// single-launch integer-pipe kernel finishes first.
+// (1 bit -> 1 byte per operand element, two launches) and a ~18 us floor; below ~2^31
+// bit-MACs the single-launch integer-pipe kernel finishes first (profiles/r01_gemm_crossover:
+// 1024^3 popc 14.9 us vs 20.7; 1000x1024x4096 popc 41 us vs 29).
 bool use_umma(size_t M, size_t N, size_t L) {
     if (g_policy == BNN_GEMM_POPC) return false;
     if (g_policy == BNN_GEMM_UMMA) return true;
-    return double(M) * double(N) * double(L) >= double(1u << 27);
+    return double(M) * double(N) * double(L) >= 2147483648.0;
 }
 
 // Unpack both packed operands to int8 rows (stride round_up(L, 32)) in stream-ordered scratch.

@@ -93,6 +93,58 @@ __global__ void __launch_bounds__(256) pack_cols_kernel(const float* __restrict_
     if (j0 + line < N && k0 + kk < wpl) words[(j0 + line) * ld + k0 + kk] = tile[line][kk];
 }
 
+// pack_cols with 16-byte loads: lane owns 4 adjacent columns, so one warp load covers 512
+// contiguous bytes of a row (4x the bytes per request of the scalar kernel, which is what
+// keeps this access pattern — 32 rows per word, each row a different DRAM page — near the
+// HBM roofline). Needs N % 4 == 0 and a 16-byte aligned x. Block: 128 columns x 8 words.
+template <bool STRICT>
+__global__ void __launch_bounds__(256) pack_cols4_kernel(const float* __restrict__ x, size_t L,
+                                                         size_t N, uint32_t* __restrict__ words,
+                                                         size_t ld, size_t wpl,
+                                                         unsigned long long* first_bad) {
+    __shared__ uint32_t tile[128][kColsWordsPerBlock + 1];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const size_t j0 = size_t(blockIdx.x) * 128;
+    const size_t k0 = size_t(blockIdx.y) * kColsWordsPerBlock;
+    const size_t col = j0 + 4 * tx;
+    const size_t word = k0 + ty;
+    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+    if (col < N && word < wpl) {
+        const size_t r0 = word * 32;
+        const float4* src = reinterpret_cast<const float4*>(x + r0 * N + col);
+        const size_t stride = N / 4;
+#pragma unroll 8
+        for (int b = 0; b < 32; ++b) {
+            if (r0 + b < L) {
+                const float4 v = __ldg(src + b * stride);
+                if (STRICT) {
+                    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (!(e[i] == 1.0f || e[i] == -1.0f))
+                            atomicMin(first_bad, (unsigned long long)((r0 + b) * N + col + i));
+                    w0 |= uint32_t(v.x == 1.0f) << b, w1 |= uint32_t(v.y == 1.0f) << b;
+                    w2 |= uint32_t(v.z == 1.0f) << b, w3 |= uint32_t(v.w == 1.0f) << b;
+                } else {
+                    w0 |= uint32_t(v.x >= 0.0f) << b, w1 |= uint32_t(v.y >= 0.0f) << b;
+                    w2 |= uint32_t(v.z >= 0.0f) << b, w3 |= uint32_t(v.w >= 0.0f) << b;
+                }
+            }
+        }
+    }
+    tile[4 * tx + 0][ty] = w0;
+    tile[4 * tx + 1][ty] = w1;
+    tile[4 * tx + 2][ty] = w2;
+    tile[4 * tx + 3][ty] = w3;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int t = i * 256 + ty * 32 + tx;
+        const int line = t / kColsWordsPerBlock, kk = t % kColsWordsPerBlock;
+        if (j0 + line < N && k0 + kk < wpl) words[(j0 + line) * ld + k0 + kk] = tile[line][kk];
+    }
+}
+
 __global__ void unpack_kernel(const uint32_t* __restrict__ words, size_t ld, size_t rows,
                               size_t cols, int col_packed, float* __restrict__ out) {
     const size_t n = rows * cols;
@@ -151,8 +203,19 @@ int launch_pack_cols(const float* x, size_t L, size_t N, uint32_t* words, size_t
     if (L == 0 || N == 0) return fail(BNN_E_SHAPE, "pack_cols: extents must be >= 1");
     BNN_TRY(check_ld(ld, L));
     const size_t wpl = wpl_of(L);
-    dim3 grid(unsigned(ceil_div(N, 32)), unsigned(ceil_div(wpl, kColsWordsPerBlock)));
     dim3 block(32, kColsWordsPerBlock);
+    // 16-byte kernel when it still fills the GPU (>= 2 blocks per SM); small matrices take the
+    // scalar kernel's 4x more blocks
+    const bool wide_grid = ceil_div(N, 128) * ceil_div(wpl, kColsWordsPerBlock) >= size_t(2 * num_sms());
+    if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && wide_grid) {
+        dim3 grid4(unsigned(ceil_div(N, 128)), unsigned(ceil_div(wpl, kColsWordsPerBlock)));
+        if (first_bad)
+            pack_cols4_kernel<true><<<grid4, block, 0, s>>>(x, L, N, words, ld, wpl, first_bad);
+        else
+            pack_cols4_kernel<false><<<grid4, block, 0, s>>>(x, L, N, words, ld, wpl, nullptr);
+        return launch_check("pack_cols4_kernel");
+    }
+    dim3 grid(unsigned(ceil_div(N, 32)), unsigned(ceil_div(wpl, kColsWordsPerBlock)));
     if (first_bad)
         pack_cols_kernel<true><<<grid, block, 0, s>>>(x, L, N, words, ld, wpl, first_bad);
     else

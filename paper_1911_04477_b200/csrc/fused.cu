@@ -71,7 +71,7 @@ constexpr int kKB = 128;     // K bytes per stage
 
 constexpr int kMaxF32K = 1024;  // float-input layers: K <= this (im2col offset table in smem)
 constexpr int kMaxQ = 1024;     // K words per layer (bits mode), entries of the offset table
-constexpr int kMaxD = 2048;     // output channels of a bits-epilogue launch (threshold table)
+constexpr int kMaxD = 4096;     // output channels of a bits-epilogue launch (threshold table)
 constexpr int kMaxPixTaps = 16; // pixel-packed first layer: taps (and taps*C <= 64)
 
 template <int BN, int CG, int ATM>
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
-    asm volatile("griddepcontrol.launch_dependents;");  // the next layer may start its prologue
+    if (!g.pdl_late) asm volatile("griddepcontrol.launch_dependents;");  // the next layer may start its prologue
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const int unit = blockIdx.x / CG, units = gridDim.x / CG;
     const int m_tiles = (g.rows + kRows * CG - 1) / (kRows * CG);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ftab[k] = make_int2(c * g.H * g.W + ky * g.W + kx, (ky << 16) | kx);
         }
     } else if (IN == FIN_BITS) {  // K word q -> (tap offset, channel word); all divisions here
-        const int kw_total = g.K >> 5;
+        const int kw_total = (g.K + 31) >> 5;  // a partial last word holds zero pad bits
         for (int q = threadIdx.x; q < 4 * KB; q += blockDim.x) {
             int2 e = make_int2(0, -1);
             if (q < kw_total) {
@@ -793,6 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
+    if (g.pdl_late) asm volatile("griddepcontrol.launch_dependents;");
     if (CG == 2) {
         cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
         if (warp == 1) tmem_dealloc_cg2<TP::kCols>(tmem_base);
@@ -1283,7 +1284,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_c
             sc.w1 += dclock() - tb;
             if (pt == 0) stamp(s, 0);
             if (cs.in_mode == FIN_BITS) {
-                const int kw_total = g.K >> 5;
+                const int kw_total = (g.K + 31) >> 5;  // a partial last word holds zero pad bits
                 for (int q = pt; q < 4 * g.KB; q += 128) {
                     int2 e = make_int2(0, -1);
                     if (q < kw_total) {
@@ -1418,6 +1419,8 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms() / CG) * CG;
     static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
     FusedGeom gd = g;
+    static const int pdl = getenv("BNN_PDL") ? atoi(getenv("BNN_PDL")) : 0;  // 0 early, 1 late, 2 off
+    gd.pdl_late = pdl == 1;
     gd.tl = fused_timeline_slot(1);
     if (gd.tl) g_tl_names.push_back("layer BN=" + std::to_string(BN) + " D=" + std::to_string(g.D) + " KB=" + std::to_string(g.KB));
     unsigned long long* dbg = nullptr;
@@ -1439,8 +1442,8 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     attr[1].val.clusterDim.x = CG;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = CG == 2 ? 2 : 1;
+    cfg.attrs = pdl == 2 ? attr + 1 : attr;
+    cfg.numAttrs = (CG == 2 ? 2 : 1) - (pdl == 2 ? 1 : 0);
     BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
     BNN_TRY(launch_check("fused_layer_kernel"));
     if (prof) {

@@ -36,6 +36,7 @@ struct FusedGeom {
     unsigned long long* dbg;  // profiling counters (BNN_FUSED_PROFILE=1), else null
     int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math, 8 no wait::st
     unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
+    int pdl_late;             // trigger dependent launch at the end of the CTA (else at entry)
 };
 
 // Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.

@@ -89,6 +89,7 @@ struct FusedStage {
     int in_mode = FIN_BITS, epi = FEPI_BITS;
     FusedGeom g{};               // batch-independent fields
     int Dpad = 0, Kpad = 0;
+    bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
     DevBuf w8, prm;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
     CUtensorMap tm[5];           // weight tile maps, box rows 16, 32, 64, 128, 256 (= BN / cta_group)
     size_t out_words_per_image = 0;
@@ -264,7 +265,6 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         if (kind != BNN_LAYER_CONV && kind != BNN_LAYER_LINEAR)
             return no("layer " + std::to_string(i) + " is glue without a preceding weighted layer");
         const bool first = i == 0;
-        if (first && kind != BNN_LAYER_CONV) return no("first layer is not a conv");
         auto st = std::make_unique<FusedStage>();
         st->layer = i;
         st->in_mode = FIN_BITS;
@@ -286,10 +286,17 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         } else {
             g.C = int(L.cols), g.H = g.W = 1, g.KH = g.KW = g.SH = g.SW = 1, g.PH = g.PW = 0;
             g.OH = g.OW = 1;
-            if (L.cols % 32) return no("linear input features not a multiple of 32");
-            if (!L.in_flat) T = int(L.in_h * L.in_w), Cperm = int(L.in_c);  // NHWC flatten order
+            if (first) {
+                // float input: flatten_to_columns order (network.cpp:177-184) is each image's
+                // memory order, so K1 pack_rows over [B, F] yields the stage's input bits in the
+                // reference K order (T = 1, no weight permutation); pad bits are 0 on both sides
+                st->pre_encode = true;
+            } else {
+                if (L.cols % 32) return no("linear input features not a multiple of 32");
+                if (!L.in_flat) T = int(L.in_h * L.in_w), Cperm = int(L.in_c);  // NHWC flatten order
+            }
         }
-        g.Cw = g.C / 32;
+        g.Cw = int((size_t(g.C) + 31) / 32);
         g.K = int(L.cols);
         g.D = int(L.rows);
         size_t j = i + 1;
@@ -312,7 +319,7 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
                 return no("unsupported glue sequence after layer " + std::to_string(i));
             if (L.rows % 32) return no("output channels not a multiple of 32");
             st->epi = FEPI_BITS;
-            if (round_up(L.rows, 256) > 2048) return no("more than 2048 output channels");
+            if (round_up(L.rows, 256) > 4096) return no("more than 4096 output channels");
         }
         g.pool = pool ? 1 : 0;
         g.Dw = g.D / 32;
@@ -524,7 +531,8 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
         BNN_TRY(net->bits[0].alloc(bytes));
         BNN_TRY(net->bits[1].alloc(bytes));
-        BNN_TRY(net->pix.alloc(B * net->in_h * net->in_w * 4));
+        const size_t pre_words = net->stages.front()->pre_encode ? wpl_of(net->in_c * net->in_h * net->in_w) : 0;
+        BNN_TRY(net->pix.alloc(B * std::max(net->in_h * net->in_w, pre_words) * 4));
         net->bits_batch = B;
         ++net->arena_epoch;
     }
@@ -578,7 +586,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             g.out_f32 = logits;
             g.ldo = int(B);
         }
-        if (st.in_mode == FIN_PIX) g.in = net->pix.as<uint32_t>();
+        if (st.in_mode == FIN_PIX || st.pre_encode) g.in = net->pix.as<uint32_t>();
         plans.push_back({g, cg, bn});
         in = g.out_bits;
     }
@@ -606,6 +614,10 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
             ++launches;
         }
+        if (st.pre_encode) {  // K1: pack_rows(sign(x)) over [B, F]
+            BNN_TRY(launch_pack_rows(x, B, size_t(g.C), net->pix.as<uint32_t>(), size_t(g.Cw), nullptr, s));
+            ++launches;
+        }
         EventPair gemm_ev(net, st.layer, 1, s);
         BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
         gemm_ev.close();
@@ -620,6 +632,10 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         const FusedStage& first = *net->stages[first_chained];
         if (first.in_mode == FIN_PIX) {
             BNN_TRY(launch_pack_pixels(x, B, first.g.C, size_t(first.g.H) * first.g.W, net->pix.as<uint32_t>(), s));
+            ++launches;
+        }
+        if (first.pre_encode) {
+            BNN_TRY(launch_pack_rows(x, B, size_t(first.g.C), net->pix.as<uint32_t>(), size_t(first.g.Cw), nullptr, s));
             ++launches;
         }
         ChainParams cp;

@@ -40,6 +40,11 @@ FUSABLE = {
     # C = 256 / 512 fast path with pooling down to 1x1, then a single logits layer
     "wide": {"input_shape": [1, 3, 8, 8], "seed": 3,
              "layers": [conv(256)] + POOL + G + [conv(512)] + POOL + G + [conv(256)] + POOL + G + [lin(33)]},
+    # linear-first stacks (BASELINE cfg1 / cfg4 shape class): K1 pack_rows of the float input,
+    # linear -> linear with no glue (sign of float(a) + bias), a 4096-wide hidden layer
+    "fc_stack": {"input_shape": [1, 288, 1, 1], "seed": 5, "layers": [lin(4096), lin(96), lin(10)]},
+    # tensor input flattened (F = 100: a partial last word), glue between the linears
+    "fc_tensor_in": {"input_shape": [1, 4, 5, 5], "seed": 9, "layers": [lin(64)] + G + [lin(10)]},
 }
 
 

@@ -104,7 +104,12 @@ def test_device_encoder_with_padded_leading_dimension(bnn, orc):
 GEOMS = [((2, 3, 6, 6), (3, 3, 1, 1, 1, 1, 3, 5)), ((1, 64, 32, 32), (3, 3, 1, 1, 1, 1, 64, 64)),
          ((3, 5, 9, 7), (3, 2, 2, 1, 1, 0, 5, 7)), ((2, 4, 8, 8), (5, 5, 1, 1, 2, 2, 4, 3)),
          ((1, 1, 4, 4), (1, 1, 1, 1, 0, 0, 1, 1)), ((4, 7, 5, 11), (2, 3, 1, 2, 0, 1, 7, 2)),
-         ((2, 128, 16, 16), (3, 3, 1, 1, 1, 1, 128, 8))]
+         ((2, 128, 16, 16), (3, 3, 1, 1, 1, 1, 128, 8)),
+         # batch x output rows >= SM count: the row-bits kernel (W <= 32), incl. kW = 1 runs,
+         # stride 2, 5x5 / pad 2, a partial last word and rectangular kernels
+         ((6, 64, 32, 32), (3, 3, 1, 1, 1, 1, 64, 64)), ((40, 3, 8, 8), (5, 5, 1, 1, 2, 2, 3, 4)),
+         ((80, 5, 9, 7), (3, 2, 2, 1, 1, 0, 5, 7)), ((160, 33, 4, 4), (1, 1, 1, 1, 0, 0, 33, 2)),
+         ((150, 7, 5, 11), (2, 3, 1, 2, 0, 1, 7, 2)), ((3, 16, 64, 20), (3, 3, 1, 1, 1, 1, 16, 8))]
 
 
 @pytest.mark.parametrize("shape,g", GEOMS)

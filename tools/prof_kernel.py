@@ -1,0 +1,34 @@
+"""Run one K1/K2 launch at the bench shapes (for ncu captures).
+
+    python tools/prof_kernel.py im2col|pack_cols|pack_rows
+"""
+import ctypes as C
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1911_04477_b200 as bnn  # noqa: E402
+from paper_1911_04477_b200 import _lib  # noqa: E402
+
+lib = bnn.load()
+S = torch.cuda.current_stream().cuda_stream
+what = sys.argv[1]
+if what == "im2col":
+    g = _lib.ConvGeom(3, 3, 1, 1, 1, 1, 128, 128)
+    x = torch.empty((256, 128, 32, 32), dtype=torch.float32, device="cuda")
+    _lib.check(lib.bnn_fill_random_f32(7, 0, x.numel(), x.data_ptr(), S))
+    out = torch.empty((256 * 1024, 36), dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        _lib.check(lib.bnn_im2col_sign_pack_f32(x.data_ptr(), 256, 128, 32, 32, C.byref(g), out.data_ptr(), 36, S))
+else:
+    L = N = 16384
+    x = torch.empty((L, N), dtype=torch.float32, device="cuda")
+    _lib.check(lib.bnn_fill_random_f32(7, 0, x.numel(), x.data_ptr(), S))
+    out = torch.empty((N, L // 32), dtype=torch.int32, device="cuda")
+    fn = lib.bnn_sign_pack_cols_f32 if what == "pack_cols" else lib.bnn_sign_pack_rows_f32
+    for _ in range(2):
+        _lib.check(fn(x.data_ptr(), L, N, out.data_ptr(), L // 32, S))
+torch.cuda.synchronize()
+print("ok", what)
