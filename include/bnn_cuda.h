@@ -216,6 +216,10 @@ int bnn_set_fused_tmem_a(int enabled);
 /* Fused engine: run every stage of the network in ONE persistent chained launch (1) or one
  * launch per weighted layer (0, default). Process-wide; both are bit-exact. */
 int bnn_set_fused_chain(int enabled);
+/* Fused engine: conv layers with a packed-bit output use the swapped-operand kernel (output
+ * channels on the tensor-core M, positions on N: full rate for 128-channel layers): 1 (default)
+ * for layers of <= 128 channels, 2 for all, 0 never. Process-wide; all are bit-exact. */
+int bnn_set_fused_swap(int enabled);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */
 int bnn_debug_timeline(int op);

@@ -83,20 +83,18 @@ constexpr size_t fused_smem() {
 
 __device__ __forceinline__ bool decode_row(const FusedGeom& g, int row, int& b, int& oy, int& ox) {
     if (row >= g.rows) return false;
-    if (g.pool) {
+    if (g.pool) {  // dv0 = OW/2, dv1 = OH/2
         const int s = row & 3, win = row >> 2;
-        const int pw = g.OW >> 1, ph = g.OH >> 1;
-        const int px = win % pw, t = win / pw;
-        const int py = t % ph;
-        b = t / ph;
+        const int t = g.dv0.div(win), px = win - t * int(g.dv0.d);
+        b = g.dv1.div(t);
+        const int py = t - b * int(g.dv1.d);
         oy = 2 * py + (s >> 1);
         ox = 2 * px + (s & 1);
-    } else {
-        const int P = g.OH * g.OW;
-        b = row / P;
-        const int p = row - b * P;
-        oy = p / g.OW;
-        ox = p - oy * g.OW;
+    } else {  // dv0 = OH*OW, dv1 = OW
+        b = g.dv0.div(row);
+        const int p = row - b * int(g.dv0.d);
+        oy = g.dv1.div(p);
+        ox = p - oy * int(g.dv1.d);
     }
     return true;
 }
@@ -184,18 +182,21 @@ __device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab,
 // tap-major / channel-minor (K <= 64: one K block). qtab[tap] = {dy<<16 | dx&0xffff, 0}.
 // load_pix() only issues the loads (their values are consumed kPF blocks later by
 // gather_pix(), so the L2 latency is hidden like the bits path's).
+// NT: compile-time tap count (9 for the 3x3 first layer: no dead iterations), else kMaxPixTaps
+// with the runtime T <= NT.
+template <int NT = kMaxPixTaps>
 struct PixRaw {
-    uint32_t v[kMaxPixTaps];
+    uint32_t v[NT];
 };
 
-template <bool Coherent = false>
-__device__ __forceinline__ PixRaw load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
+template <bool Coherent = false, int NT = kMaxPixTaps>
+__device__ __forceinline__ PixRaw<NT> load_pix(const FusedGeom& g, const int2* qtab, const RowCtx& rc) {
     const uint32_t* pix = static_cast<const uint32_t*>(g.in);
-    const int T = g.KH * g.KW;
+    const int T = NT == kMaxPixTaps ? g.KH * g.KW : NT;
     const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
-    PixRaw raw;
+    PixRaw<NT> raw;
 #pragma unroll
-    for (int tap = 0; tap < kMaxPixTaps; ++tap) {
+    for (int tap = 0; tap < NT; ++tap) {
         const int2 e = qtab[tap < T ? tap : 0];
         const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
         const bool inb = rc.valid && tap < T && unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W);
@@ -214,12 +215,13 @@ __device__ __forceinline__ PixRaw load_pix(const FusedGeom& g, const int2* qtab,
     return raw;
 }
 
-__device__ __forceinline__ uint4 gather_pix(const FusedGeom& g, const PixRaw& raw, bool valid) {
+template <int NT>
+__device__ __forceinline__ uint4 gather_pix(const FusedGeom& g, const PixRaw<NT>& raw, bool valid) {
     if (!valid) return make_uint4(0, 0, 0, 0);
-    const int T = g.KH * g.KW;
+    const int T = NT == kMaxPixTaps ? g.KH * g.KW : NT;
     uint64_t acc = 0;
 #pragma unroll
-    for (int tap = 0; tap < kMaxPixTaps; ++tap)
+    for (int tap = 0; tap < NT; ++tap)
         if (tap < T) acc |= uint64_t(raw.v[tap]) << (tap * g.C);
     return make_uint4(uint32_t(acc), uint32_t(acc >> 32), 0u, 0u);
 }
@@ -315,7 +317,7 @@ struct TmemPlan {
     static_assert(kUsed <= 512, "TMEM budget");
 };
 
-template <int BN, int IN, int EPI, int CG, int ATM>
+template <int BN, int IN, int EPI, int CG, int ATM, int PT = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     fused_layer_kernel(const __grid_constant__ CUtensorMap tmW, const FusedGeom g) {
     static_assert(!(ATM && (CG == 2 || IN == FIN_F32)), "TMEM A operand: CTA-local, bits/pixel input");
@@ -462,8 +464,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) {
                         const uint32_t a0 = smem_u32(sA + size_t(stage) * kRows * kKB);
                         const uint32_t b0 = smem_u32(sB + size_t(stage) * BH * kKB);
+                        // K steps past the layer's K in its last block multiply zeros: skip them
+                        const int nk = kb == KB - 1 ? g.kq_last : kKB / 32;
 #pragma unroll
                         for (int k = 0; k < kKB / 32; ++k) {
+                            if (k >= nk) break;
                             if (ATM)
                                 mma_i8_ts(d_tmem, tmem_base + uint32_t(TP::kACol + stage * TP::kAStage + 8 * k),
                                           sdesc_k_sw128(b0 + 32 * k), idesc, (kb != kb0 || k != 0));
@@ -715,7 +720,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         if (IN != FIN_F32) {
             constexpr int kPF = 3;
-            using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw>::type;
+            constexpr int NT = PT ? PT : kMaxPixTaps;
+            using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw<NT>>::type;
             int t_ld = unit, kb_ld = unit < tiles ? kb_begin(unit) : 0;  // next block to load
             int kb_ld_end = unit < tiles ? kb_end(unit) : 0;
             RowCtx rc;
@@ -732,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (IN == FIN_BITS) {
                     dst = t_ld < tiles ? load_bits(g, ftab, rc, kb_ld) : make_uint4(0, 0, 0, 0);
                 } else {
-                    dst = load_pix(g, ftab, rc);
+                    dst = load_pix<false, NT>(g, ftab, rc);
                 }
                 if (t_ld < tiles && ++kb_ld == kb_ld_end) {  // per-tile divisions only at tile change
                     t_ld += units;
@@ -757,16 +763,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     wc.wait(&empty[stage], phase ^ 1, 0);
                     if (ATM) {
                         // bytes 4s..4s+3 of word i's 32-byte segment = column 8i + s (put_word's order)
-                        uint32_t v[32];
-                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-#pragma unroll
-                            for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
+                        const uint32_t taddr = tmem_base + (uint32_t(32 * (warp & 3)) << 16) +
+                                               uint32_t(TP::kACol + stage * TP::kAStage);
                         tc_fence_after();
-                        if (!(g.dbg_mode & 1))
-                            tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) +
-                                          uint32_t(TP::kACol + stage * TP::kAStage), v);
+                        if (g.KB == 1 && g.kq_last == 1) {  // one K step (e.g. a 27-bit first layer)
+                            uint32_t v[8];
+#pragma unroll
+                            for (int s8 = 0; s8 < 8; ++s8) v[s8] = (u.x >> s8) & 0x01010101u;
+                            if (!(g.dbg_mode & 1)) tmem_st8(taddr, v);
+                        } else {
+                            uint32_t v[32];
+                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                                for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
+                            if (!(g.dbg_mode & 1)) tmem_st32(taddr, v);
+                        }
                     } else if (!(g.dbg_mode & 1)) {
                         store_bits(smem_u32(sA + size_t(stage) * kRows * kKB), r, u);
                     }
@@ -1049,7 +1062,7 @@ __device__ __forceinline__ void chain_produce(const FusedGeom& g, const int2* ft
     const int tiles = ct.tiles, unit = blockIdx.x, units = gridDim.x;
     const int r = 32 * (warp & 3) + lane;
     constexpr int kPF = 3;
-    using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw>::type;
+    using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw<>>::type;
     int t_ld = unit, kb_ld = unit < tiles ? ct.kb_begin(unit) : 0;
     int kb_ld_end = unit < tiles ? ct.kb_end(unit) : 0;
     RowCtx rc;
@@ -1320,6 +1333,288 @@ __global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_c
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Swapped-operand fused conv: tiles of 128 output channels (UMMA M, the weights, TMA-loaded
+// into shared memory) x 256 output positions (UMMA N, the activations, expanded by the
+// producer warps into shared memory).
+//
+// Why: a kind::i8 M=128 instruction costs the same ~128-150 cycles for any N <= 256
+// (profiles/r01_fused_v3_bn_sweep.log), so the position-major tiles above (positions on M,
+// channels on N) run layers with 128 output channels at half the tensor rate. Putting the
+// positions on N fills the instruction for every layer. Both operands now come from shared
+// memory (A may only come from TMEM, and 2 x 256 accumulator columns fill TMEM), so each
+// 4-instruction stage moves 96 KB through shared memory (TMA 16 KB + producer 32 KB written,
+// 48 KB read by the MMA): ~128 B/clk bounds it near the MMA rate. Two accumulator slots of
+// 256 columns let the epilogue of tile i overlap the MMAs of tile i+1 at every width.
+//
+// Epilogue: TMEM lane = output channel, column = position. Each thread tests its channel's
+// threshold (Tu, flip: prep_params_kernel) against 32 positions; __ballot_sync over the warp
+// turns 32 channels into the packed output word of each position; pooled layers OR the 4
+// words of a window (pool-major positions: 4 adjacent columns).
+constexpr int kSwN = 256;  // positions per tile
+constexpr size_t kSwSmem = 1024 + size_t(kStages) * (kRows + kSwN) * kKB + 256 + kMaxQ * 8;
+
+template <int IN, int PT>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_swap_kernel(const __grid_constant__ CUtensorMap tmW, const FusedGeom g) {
+    static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sW = smem_raw + (base - raw);                 // [kStages][128 * 128] weights (A)
+    uint8_t* sX = sW + size_t(kStages) * kRows * kKB;      // [kStages][256 * 128] activations (B)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(kStages) * kSwN * kKB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int2* ftab = reinterpret_cast<int2*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int units = gridDim.x, unit = blockIdx.x;
+    const int m_tiles = (g.D + kRows - 1) / kRows;
+    const int n_tiles = (g.rows + kSwN - 1) / kSwN;
+    const int tiles = m_tiles * n_tiles;  // t -> (channel tile t % m_tiles, position tile t / m_tiles)
+    const int KB = g.KB;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmW);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 4 + 1);  // four producer warps + the TMA thread
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        fence_mbar_init();
+    }
+    if (IN == FIN_BITS) {
+        const int kw_total = (g.K + 31) >> 5;
+        for (int q = threadIdx.x; q < 4 * KB; q += blockDim.x) {
+            int2 e = make_int2(0, -1);
+            if (q < kw_total) {
+                const int tap = q / g.Cw, cw = q - tap * g.Cw, ky = tap / g.KW, kx = tap - ky * g.KW;
+                e = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), cw);
+            }
+            ftab[q] = e;
+        }
+    } else {
+        for (int tap = threadIdx.x; tap < g.KH * g.KW; tap += blockDim.x) {
+            const int ky = tap / g.KW, kx = tap - ky * g.KW;
+            ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
+        }
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ weight TMA (A)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = unit; t < tiles; t += units) {
+                const int mt = t % m_tiles;
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], kRows * kKB);
+                    tma_load_2d(&tmW, &full[stage], sW + size_t(stage) * kRows * kKB, kb * kKB, mt * kRows);
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ UMMA issuer
+        constexpr uint32_t idesc = idesc_i8(kRows, kSwN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int i = 0;
+        for (int t = unit; t < tiles; t += units, ++i) {
+            const int acc = i & 1;
+            mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + uint32_t(acc * kSwN);
+            for (int kb = 0; kb < KB; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
+                    const uint32_t b0 = smem_u32(sX + size_t(stage) * kSwN * kKB);
+                    const int nk = kb == KB - 1 ? g.kq_last : kKB / 32;  // K steps past K: zeros
+#pragma unroll
+                    for (int k = 0; k < kKB / 32; ++k) {
+                        if (k >= nk) break;
+                        mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                               (kb != 0 || k != 0));
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == kStages) stage = 0, phase ^= 1;
+            }
+        }
+    } else if (warp < 6 || warp >= 10) {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;                       // TMEM lane quarter: channels q*32 + lane
+        const int col0 = warp >= 10 ? kSwN / 2 : 0;   // this warp's half of the positions
+        int i = 0;
+        for (int t = unit; t < tiles; t += units, ++i) {
+            const int acc = i & 1;
+            const int mt = t % m_tiles, nt = t / m_tiles;
+            const int c = mt * kRows + q * 32 + lane;
+            const bool wvalid = mt * kRows + q * 32 < g.D;  // D % 32 == 0: whole words
+            const int4 pc = wvalid ? __ldg(g.prm + c) : make_int4(0x7fffffff, 0, 0, 0);
+            const int Tu = pc.x;
+            const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
+            const int oword = mt * (kRows / 32) + q;
+            mbar_wait(&tfull[acc], (i >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kSwN + col0);
+            uint32_t va[32], vb[32];
+            auto emit = [&](const uint32_t(&v)[32], int cc) {
+                uint32_t mine = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t w = __ballot_sync(0xffffffffu, int(v[j]) >= Tu) ^ flipw;
+                    if (lane == j) mine = w;
+                }
+                const int pos = nt * kSwN + col0 + cc * 32 + lane;
+                if (g.pool) {
+                    mine |= __shfl_xor_sync(0xffffffffu, mine, 1);
+                    mine |= __shfl_xor_sync(0xffffffffu, mine, 2);
+                    if (wvalid && (lane & 3) == 0 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
+                } else if (wvalid && pos < g.rows) {
+                    g.out_bits[size_t(pos) * g.Dw + oword] = mine;
+                }
+            };
+            tmem_ld32(tbase, va);
+            tmem_ld_wait();
+            tmem_ld32(tbase + 32, vb);
+            emit(va, 0);
+            tmem_ld_wait();
+            tmem_ld32(tbase + 64, va);
+            emit(vb, 1);
+            tmem_ld_wait();
+            tmem_ld32(tbase + 96, vb);
+            emit(va, 2);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator free before the last words
+            emit(vb, 3);
+        }
+    } else {
+        // ------------------------------------------------------------ activation producers (B)
+        // thread pt owns tile rows pt and pt + 128 (two positions); loads kPF blocks ahead
+        const int pt = threadIdx.x - 6 * 32;
+        constexpr int NT = PT ? PT : kMaxPixTaps;
+        using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw<NT>>::type;
+        constexpr int kPF = 2;
+        int stage = 0;
+        uint32_t phase = 0;
+        int t_ld = unit, kb_ld = 0;
+        RowCtx rc[2];
+        auto set_rows = [&]() {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                int b = 0, oy = 0, ox = 0;
+                rc[h].valid = t_ld < tiles && decode_row(g, (t_ld / m_tiles) * kSwN + pt + 128 * h, b, oy, ox);
+                rc[h].pix = b * g.H, rc[h].y0 = oy * g.SH, rc[h].x0 = ox * g.SW;
+            }
+        };
+        set_rows();
+        Raw pf[kPF][2];
+        bool pv[kPF][2];
+        auto next_load = [&](Raw (&dst)[2], bool (&v)[2]) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                v[h] = rc[h].valid;
+                if constexpr (IN == FIN_BITS)
+                    dst[h] = t_ld < tiles ? load_bits(g, ftab, rc[h], kb_ld) : make_uint4(0, 0, 0, 0);
+                else
+                    dst[h] = load_pix<false, NT>(g, ftab, rc[h]);
+            }
+            if (t_ld < tiles && ++kb_ld == KB) {
+                t_ld += units;
+                kb_ld = 0;
+                set_rows();
+            }
+        };
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
+        const bool one_step = KB == 1 && g.kq_last == 1;  // e.g. the 27-bit first layer: 32 bytes per row
+        for (int t = unit; t < tiles; t += units) {
+            for (int kb = 0; kb < KB; ++kb) {
+                uint4 u[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if constexpr (IN == FIN_BITS)
+                        u[h] = pf[0][h];
+                    else
+                        u[h] = gather_pix(g, pf[0][h], pv[0][h]);
+                }
+#pragma unroll
+                for (int i = 0; i < kPF - 1; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) pf[i][h] = pf[i + 1][h], pv[i][h] = pv[i + 1][h];
+                next_load(pf[kPF - 1], pv[kPF - 1]);
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t tile = smem_u32(sX + size_t(stage) * kSwN * kKB);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (one_step)
+                        put_word(tile, pt + 128 * h, 0, u[h].x);  // the MMA reads the first 32 bytes only
+                    else
+                        store_bits(tile, pt + 128 * h, u[h]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[stage]);
+                if (++stage == kStages) stage = 0, phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem_base);
+}
+
+template <int IN, int PT>
+int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    auto kern = fused_swap_kernel<IN, PT>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSwSmem)));
+        attr_set = true;
+    }
+    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows)) * ceil_div(size_t(g.rows), size_t(kSwN)));
+    const int grid = std::min(tiles, num_sms());
+    static const int pdl = getenv("BNN_PDL") ? atoi(getenv("BNN_PDL")) : 0;
+    FusedGeom gd = g;
+    gd.tl = fused_timeline_slot(1);
+    if (gd.tl) g_tl_names.push_back("swap D=" + std::to_string(g.D) + " KB=" + std::to_string(g.KB));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSwSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl == 2 ? 0 : 1;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
+    return launch_check("fused_swap_kernel");
+}
+
 // Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),
 // K order r) -> int8 +-1 rows [Dpad, Kpad] in the engine's K order. With T > 1 the engine
 // order is tap-major (k' = tap*C + c) and the reference order is channel-major
@@ -1401,9 +1696,9 @@ __global__ void pack_pixels_kernel(const float* __restrict__ x, int C, size_t HW
     }
 }
 
-template <int BN, int IN, int EPI, int CG, int ATM>
+template <int BN, int IN, int EPI, int CG, int ATM, int PT = 0>
 int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_layer_kernel<BN, IN, EPI, CG, ATM>;
+    auto kern = fused_layer_kernel<BN, IN, EPI, CG, ATM, PT>;
     constexpr size_t smem = fused_smem<BN, CG, ATM>();
     static bool attr_set = false;  // per instantiation; the attribute is per function
     if (!attr_set) {
@@ -1460,13 +1755,13 @@ int launch_fused_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     return BNN_OK;
 }
 
-template <int IN, int EPI, int CG, int ATM>
+template <int IN, int EPI, int CG, int ATM, int PT = 0>
 int launch_fused_bn(int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     switch (BN) {
-        case 32: return launch_fused_t<32, IN, EPI, CG, ATM>(tm, g, s);
-        case 64: return launch_fused_t<64, IN, EPI, CG, ATM>(tm, g, s);
-        case 128: return launch_fused_t<128, IN, EPI, CG, ATM>(tm, g, s);
-        case 256: return launch_fused_t<256, IN, EPI, CG, ATM>(tm, g, s);
+        case 32: return launch_fused_t<32, IN, EPI, CG, ATM, PT>(tm, g, s);
+        case 64: return launch_fused_t<64, IN, EPI, CG, ATM, PT>(tm, g, s);
+        case 128: return launch_fused_t<128, IN, EPI, CG, ATM, PT>(tm, g, s);
+        case 256: return launch_fused_t<256, IN, EPI, CG, ATM, PT>(tm, g, s);
         default: return fail(BNN_E_CONFIG, "fused layer: unsupported BN " + std::to_string(BN));
     }
 }
@@ -1477,6 +1772,8 @@ template <int IN, int EPI>
 int launch_fused_cg(int cg, int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (cg == 2) return launch_fused_bn<IN, EPI, 2, 0>(BN, tm, g, s);
     if (g_atmem < 0) g_atmem = getenv("BNN_FUSED_TMEM_A") ? atoi(getenv("BNN_FUSED_TMEM_A")) : 1;
+    if constexpr (IN == FIN_PIX)  // 3x3 first layer: the 9-tap pixel gather
+        if (g_atmem && g.KH * g.KW == 9) return launch_fused_bn<IN, EPI, 1, 1, 9>(BN, tm, g, s);
     if constexpr (IN != FIN_F32)
         if (g_atmem) return launch_fused_bn<IN, EPI, 1, 1>(BN, tm, g, s);
     return launch_fused_bn<IN, EPI, 1, 0>(BN, tm, g, s);
@@ -1567,6 +1864,17 @@ int fused_timeline(int op) {
 }
 
 static int launch_chain_impl(const ChainParams& p, cudaStream_t s);
+
+int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    if (g.rows <= 0) return BNN_OK;
+    set_last_gemm("fused_swap_umma_i8");
+    if (in_mode == FIN_PIX) {
+        if (g.KH * g.KW == 9) return launch_swap_t<FIN_PIX, 9>(tm, g, s);
+        return launch_swap_t<FIN_PIX, 0>(tm, g, s);
+    }
+    if (in_mode == FIN_BITS) return launch_swap_t<FIN_BITS, 0>(tm, g, s);
+    return fail(BNN_E_CONFIG, "swapped fused layer: packed-bit or pixel input only");
+}
 
 int launch_chain(const ChainParams& p0, cudaStream_t s) {
     ChainParams p = p0;

@@ -13,6 +13,24 @@ namespace bnnk {
 enum { FIN_BITS = 0, FIN_F32 = 1, FIN_PIX = 2 };
 enum { FEPI_BITS = 0, FEPI_LOGITS = 1, FEPI_NCHW = 2 };  // epilogue output
 
+// Division by a launch constant without the ~20-instruction integer divide: for n < 2^31,
+// n / d = (umulhi(n, mul) + n) >> shift (Granlund-Montgomery, round-up multiplier).
+struct FastDiv {
+    uint32_t d, mul, shift;
+    static FastDiv make(uint32_t d) {
+        if (d == 0) d = 1;  // unused divisor
+        uint32_t l = 0;
+        while ((uint64_t(1) << l) < d) ++l;
+        const uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1;
+        return FastDiv{d, uint32_t(m), l};
+    }
+#ifdef __CUDACC__
+    __device__ __forceinline__ int div(int n) const {
+        return int((__umulhi(uint32_t(n), mul) + uint32_t(n)) >> shift);
+    }
+#endif
+};
+
 struct FusedGeom {
     const void* in;  // FIN_BITS: u32 [B, H, W, Cw] packed NHWC; FIN_F32: float [B, C, H, W]
     int B, H, W, C, Cw;
@@ -37,6 +55,8 @@ struct FusedGeom {
     int dbg_mode;             // profiling experiments (results invalid): 1 no A stores, 2 no epilogue math, 8 no wait::st
     unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
     int pdl_late;             // trigger dependent launch at the end of the CTA (else at entry)
+    int kq_last;              // 32-byte K steps that carry data in the last K block (1..4)
+    FastDiv dv0, dv1;         // decode_row divisors: pool (OW/2, OH/2) or (OH*OW, OW)
 };
 
 // Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.
@@ -57,6 +77,9 @@ struct ChainParams {
 int fused_timeline(int op);
 unsigned long long* fused_timeline_slot(int slots);
 int launch_chain(const ChainParams& p, cudaStream_t s);
+// Swapped-operand conv (fused_swap_kernel): 128 channels x 256 positions per tile, bits
+// epilogue, CTA-local; tm must be the weight map with box rows 128.
+int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
 
 int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
                        int Kpad, int8_t* out, cudaStream_t s);

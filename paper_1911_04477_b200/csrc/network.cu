@@ -327,6 +327,9 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         st->Kpad = int(round_up(size_t(g.K), 128));
         st->Dpad = int(round_up(size_t(g.D), 32));
         g.KB = st->Kpad / 128;
+        g.kq_last = (g.K - 128 * (g.KB - 1) + 31) / 32;
+        g.dv0 = FastDiv::make(uint32_t(pool ? g.OW / 2 : g.OH * g.OW));
+        g.dv1 = FastDiv::make(uint32_t(pool ? g.OH / 2 : g.OW));
         if (st->in_mode == FIN_F32 && g.K > 1024) return no("first conv reduction length > 1024");
         if (st->in_mode == FIN_BITS && st->Kpad / 32 > 1024) return no("reduction length > 32768");
         const size_t prm_n = round_up(size_t(g.D), 256);
@@ -526,6 +529,21 @@ int forward_generic(bnn_net* net, const float* x, size_t B, float* logits, cudaS
 int g_chain = -1;
 int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
 
+// Swapped-operand conv kernel (fused_swap_kernel: channels on the MMA's M, positions on N)
+// for conv layers with a packed-bit epilogue. BNN_FUSED_SWAP / bnn_set_fused_swap: 1 (default)
+// for layers of <= 128 output channels, where the position-major kernel runs the MMA at half
+// rate (measured at batch 256: conv 128->128 70.5 -> 58.7 us); 2 for every such conv layer
+// (wider layers measured slower: the swapped stage is shared-memory-bandwidth bound); 0 off.
+// Forced tilings (bnn_set_fused_tiling) keep the position-major kernel.
+int g_swap = -1;
+
+bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
+    if (g_swap < 0) g_swap = getenv("BNN_FUSED_SWAP") ? atoi(getenv("BNN_FUSED_SWAP")) : 1;
+    return g_swap != 0 && g_forced_cg <= 0 && g_forced_bn <= 0 && cg == 1 &&
+           net->layers[st.layer]->spec.kind == BNN_LAYER_CONV && st.epi == FEPI_BITS && st.in_mode != FIN_F32 &&
+           (g_swap == 2 || st.g.D <= 128);
+}
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -619,7 +637,10 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             ++launches;
         }
         EventPair gemm_ev(net, st.layer, 1, s);
-        BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
+        if (use_swap(net, st, plans[i].cg))
+            BNN_TRY(launch_swap(st.in_mode, st.tm[box_index(128)], g, s));
+        else
+            BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
         gemm_ev.close();
         layer_ev.close();
         ++launches;
@@ -830,6 +851,13 @@ int bnn_set_fused_split(int split) {
 }
 
 int bnn_debug_timeline(int op) { return fused_timeline(op); }
+
+int bnn_set_fused_swap(int enabled) {
+    if (enabled < 0 || enabled > 2) return fail(BNN_E_CONFIG, "fused swap: 0 (off), 1 (<= 128 channels) or 2 (all)");
+    g_swap = enabled;
+    ++g_tiling_epoch;  // captured graphs hold the other kernels
+    return BNN_OK;
+}
 
 int bnn_set_fused_chain(int enabled) {
     g_chain = enabled ? 1 : 0;

@@ -52,11 +52,12 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "noswap", "swapall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
-    A operand in TMEM, split-K for the small-batch linear layers), with all stages chained in
+    swapped-operand conv kernels, A operand in TMEM and split-K for the small-batch linear
+    layers), with the position-major conv kernel (noswap), with all stages chained in
     one persistent launch, with the A operand staged in shared memory, with each cta_group
     forced, and with split-K off / forced to 16 (per-layer and chained)."""
     lib = bnn.load()
@@ -66,11 +67,13 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16, "chain_nosplit": 1,
                                             "chain_split16": 16}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
+    bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_tmem_a(1)
     lib.bnn_set_fused_split(0)
     lib.bnn_set_fused_chain(0)
+    lib.bnn_set_fused_swap(1)
 
 
 @pytest.fixture
