@@ -271,9 +271,11 @@ __device__ __forceinline__ long long dclock() {
 #endif
 }
 
+// "memory" clobber: the read must not move across the barriers it brackets (a volatile asm
+// without it can be scheduled ahead of __syncthreads)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     return t;
 }
 
@@ -404,12 +406,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
             tmem_alloc<TP::kCols>(tmem_slot);
     }
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
+    // (stamp 1 is written at the very end, after the TMEM dealloc)
     // Programmatic dependent launch: everything above touches only this launch's constants
     // (weights' tensor map, thresholds, tables, TMEM, barriers), so it overlaps the previous
     // layer's tail. From here on the previous layer's output is read and a buffer it may still
@@ -493,6 +496,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == kAcc) acc = 0, acc_phase ^= 1;
             }
             if (lane == 0) wc.flush(g.dbg, 1);
+            if (CG == 1) {
+                // Free TMEM as soon as the epilogue has read the last accumulators (wait for the
+                // release of every slot, as if kAcc more tiles followed) instead of after the
+                // final __syncthreads, so the dealloc overlaps the epilogue's last stores.
+                for (int k = 0; k < kAcc; ++k) {
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    if (++acc == kAcc) acc = 0, acc_phase ^= 1;
+                }
+                tc_fence_after();
+                tmem_dealloc<TP::kCols>(tmem_base);
+            }
         }
     } else if (warp < 6 || warp >= 10) {
         // -------------------------------------------------------------- epilogue
@@ -803,6 +817,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r == 0) wc.flush(g.dbg, 3);
     }
 
+    if (g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
+    __syncwarp();  // reconverge role-divergent lanes before the CTA barrier
     tc_fence_before();
     __syncthreads();
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
@@ -810,9 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CG == 2) {
         cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
         if (warp == 1) tmem_dealloc_cg2<TP::kCols>(tmem_base);
-    } else if (warp == 1) {
-        tmem_dealloc<TP::kCols>(tmem_base);
-    }
+    }  // CG == 1: the MMA warp deallocated already
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1180,6 +1194,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_c
     if (warp == 0 && lane == 0)
         for (int s = 0; s < n; ++s) tma_prefetch(&P.st[s].tm);
     if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1321,6 +1336,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_c
         }
     }
 
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem_base);
@@ -1408,6 +1424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1419,15 +1436,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            WaitClock wc;
             for (int t = unit; t < tiles; t += units) {
                 const int mt = t % m_tiles;
                 for (int kb = 0; kb < KB; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    wc.wait(&empty[stage], phase ^ 1, 0);
                     mbar_arrive_expect_tx(&full[stage], kRows * kKB);
                     tma_load_2d(&tmW, &full[stage], sW + size_t(stage) * kRows * kKB, kb * kKB, mt * kRows);
                     if (++stage == kStages) stage = 0, phase ^= 1;
                 }
             }
+            wc.flush(g.dbg, 0);
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ UMMA issuer
@@ -1435,13 +1454,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int i = 0;
+        WaitClock wc;
         for (int t = unit; t < tiles; t += units, ++i) {
             const int acc = i & 1;
-            mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+            wc.wait(&tempty[acc], ((i >> 1) & 1) ^ 1, 0);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + uint32_t(acc * kSwN);
             for (int kb = 0; kb < KB; ++kb) {
-                mbar_wait(&full[stage], phase);
+                wc.wait(&full[stage], phase, 1);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
@@ -1460,8 +1480,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++stage == kStages) stage = 0, phase ^= 1;
             }
         }
+        if (lane == 0) wc.flush(g.dbg, 1);
+        // early TMEM release (see fused_layer_kernel): wait until both slots are read
+        for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
     } else if (warp < 6 || warp >= 10) {
         // ------------------------------------------------------------ epilogue
+        WaitClock wc;
         const int q = warp & 3;                       // TMEM lane quarter: channels q*32 + lane
         const int col0 = warp >= 10 ? kSwN / 2 : 0;   // this warp's half of the positions
         int i = 0;
@@ -1474,7 +1500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int Tu = pc.x;
             const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
             const int oword = mt * (kRows / 32) + q;
-            mbar_wait(&tfull[acc], (i >> 1) & 1);
+            wc.wait(&tfull[acc], (i >> 1) & 1, 0);
             tc_fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kSwN + col0);
             uint32_t va[32], vb[32];
@@ -1510,6 +1536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator free before the last words
             emit(vb, 3);
         }
+        if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
     } else {
         // ------------------------------------------------------------ activation producers (B)
         // thread pt owns tile rows pt and pt + 128 (two positions); loads kPF blocks ahead
@@ -1550,6 +1577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
         const bool one_step = KB == 1 && g.kq_last == 1;  // e.g. the 27-bit first layer: 32 bytes per row
+        WaitClock wc;
         for (int t = unit; t < tiles; t += units) {
             for (int kb = 0; kb < KB; ++kb) {
                 uint4 u[2];
@@ -1565,26 +1593,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) pf[i][h] = pf[i + 1][h], pv[i][h] = pv[i + 1][h];
                 next_load(pf[kPF - 1], pv[kPF - 1]);
-                mbar_wait(&empty[stage], phase ^ 1);
+                wc.wait(&empty[stage], phase ^ 1, 0);
                 const uint32_t tile = smem_u32(sX + size_t(stage) * kSwN * kKB);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    if (g.dbg_mode & 1) break;  // profiling: no stores (results invalid)
                     if (one_step)
                         put_word(tile, pt + 128 * h, 0, u[h].x);  // the MMA reads the first 32 bytes only
                     else
                         store_bits(tile, pt + 128 * h, u[h]);
                 }
-                fence_proxy_async_smem();
+                if (!(g.dbg_mode & 8)) fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[stage]);
                 if (++stage == kStages) stage = 0, phase ^= 1;
             }
         }
+        if (pt == 0) wc.flush(g.dbg, 3);
     }
 
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem_base);
+    __syncthreads();  // (TMEM: deallocated by the MMA warp)
 }
 
 template <int IN, int PT>
@@ -1611,8 +1641,28 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl == 2 ? 0 : 1;
+    static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
+    unsigned long long* dbg = nullptr;
+    if (prof) {
+        BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+        BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
+        gd.dbg = dbg;
+        gd.dbg_mode = prof >> 1;
+    }
     BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
-    return launch_check("fused_swap_kernel");
+    BNN_TRY(launch_check("fused_swap_kernel"));
+    if (prof) {
+        unsigned long long h[16];
+        BNN_CUDA(cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost));
+        cudaFree(dbg);
+        const double n = double(grid);
+        fprintf(stderr,
+                "[swap in=%d rows=%d D=%d KB=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | mma wait-acc %.1f "
+                "wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
+                IN, g.rows, g.D, g.KB, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
+                h[8] / n / 1e3, h[12] / n / 1e3);
+    }
+    return BNN_OK;
 }
 
 // Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
+    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<2 * BN>(tmem_base);

@@ -2,7 +2,7 @@
 min/median/max over CTAs of four globaltimer stamps, in us from the first stamp.
 
     python tools/timeline.py [B] [chain 0|1]
-Per-layer launches: k0 entry, k1 setup done, k2 griddepcontrol.wait returned, k3 exit.
+Per-layer launches: k0 entry, k1 after the TMEM dealloc (last), k2 griddepcontrol.wait returned, k3 roles done.
 Chain stages: k0 producers passed the hand-off, k1 kernel entry, k2 epilogue done, k3 TMA done.
 """
 import os
