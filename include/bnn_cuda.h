@@ -220,6 +220,9 @@ int bnn_set_fused_chain(int enabled);
  * channels on the tensor-core M, positions on N: full rate for 128-channel layers): 1 (default)
  * for layers of <= 128 channels, 2 for all, 0 never. Process-wide; all are bit-exact. */
 int bnn_set_fused_swap(int enabled);
+/* Fused engine: a final layer of <= 64 logits runs as a CUDA-core xnor-popcount kernel (1,
+ * default) or on the tensor cores like the other layers (0). Bit-exact either way. */
+int bnn_set_fused_small_logits(int enabled);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */
 int bnn_debug_timeline(int op);

@@ -107,6 +107,7 @@ _SIGS = {
     "bnn_set_fused_chain": (_I, [_I]),
     "bnn_debug_timeline": (_I, [_I]),
     "bnn_set_fused_swap": (_I, [_I]),
+    "bnn_set_fused_small_logits": (_I, [_I]),
     "bnn_net_set_timing": (_I, [_P, _I]),
     "bnn_net_timing": (_I, [_P, _P, _P, _P]),
     "bnn_net_reset_timing": (_I, [_P]),

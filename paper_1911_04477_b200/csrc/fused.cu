@@ -1665,6 +1665,47 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     return BNN_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tiny final layers (a handful of logits, e.g. 1024 -> 10): one CUDA-core thread per logit,
+// xnor-popcount over the packed input row, instead of a tensor-core launch whose fixed
+// pipeline latency (TMA, expansion, 8 dependent K blocks on 2 CTAs) dominates: the layer
+// is ~1 M bit-MACs. a = K - 2 popc(w ^ x) (kernels.hpp:46-54: pad bits are 0 on both sides),
+// logit = float(a) + bias (kernels.cpp:90-107), written [D, ldo] (features x batch).
+__global__ void logits_popc_kernel(const uint32_t* __restrict__ act, int Kw, int K, const uint32_t* __restrict__ wbits,
+                                   const int4* __restrict__ prm, int D, int B, float* __restrict__ out, int ldo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= D * B) return;
+    const int d = i / B, b = i - d * B;  // consecutive threads: consecutive images (coalesced logits)
+    const uint4* x4 = reinterpret_cast<const uint4*>(act + size_t(b) * Kw);
+    const uint4* w4 = reinterpret_cast<const uint4*>(wbits + size_t(d) * Kw);
+    int acc = 0;
+    if ((Kw & 3) == 0) {
+        for (int q = 0; q < Kw / 4; ++q) {
+            const uint4 x = __ldg(x4 + q), w = __ldg(w4 + q);
+            acc += __popc(x.x ^ w.x) + __popc(x.y ^ w.y) + __popc(x.z ^ w.z) + __popc(x.w ^ w.w);
+        }
+    } else {
+        for (int q = 0; q < Kw; ++q) acc += __popc(__ldg(act + size_t(b) * Kw + q) ^ __ldg(wbits + size_t(d) * Kw + q));
+    }
+    out[size_t(d) * ldo + b] = __fadd_rn(__int2float_rn(K - 2 * acc), __int_as_float(__ldg(&prm[d].w)));
+}
+
+// The engine's int8 weights back to sign bits in the activation bit order (word q bit j = K
+// position 32q + j). prep_weights_kernel's within-word byte order: byte 4s + j holds position
+// 8j + s, so position j of a 32-group sits at byte 4 (j % 8) + j / 8. Positions >= K: 0.
+__global__ void weights_to_bits_kernel(const int8_t* __restrict__ w8, int Kpad, int K, int D, int Kw,
+                                       uint32_t* __restrict__ wbits) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= D * Kw) return;
+    const int d = i / Kw, q = i - d * Kw;
+    uint32_t w = 0;
+    for (int j = 0; j < 32; ++j) {
+        const int k = 32 * q + j;
+        if (k < K && w8[size_t(d) * Kpad + 32 * q + 4 * (j % 8) + j / 8] > 0) w |= 1u << j;
+    }
+    wbits[i] = w;
+}
+
 // Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),
 // K order r) -> int8 +-1 rows [Dpad, Kpad] in the engine's K order. With T > 1 the engine
 // order is tap-major (k' = tap*C + c) and the reference order is channel-major
@@ -1914,6 +1955,21 @@ int fused_timeline(int op) {
 }
 
 static int launch_chain_impl(const ChainParams& p, cudaStream_t s);
+
+int prep_logit_bits(const int8_t* w8, int Kpad, int K, int D, int Kw, uint32_t* wbits, cudaStream_t s) {
+    const int n = D * Kw;
+    weights_to_bits_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(w8, Kpad, K, D, Kw, wbits);
+    return launch_check("weights_to_bits_kernel");
+}
+
+int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s) {
+    const int n = g.D * g.rows;
+    if (n == 0) return BNN_OK;
+    set_last_gemm("logits_popc");
+    logits_popc_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(static_cast<const uint32_t*>(g.in), g.Cw, g.K, wbits,
+                                                                 g.prm, g.D, g.rows, g.out_f32, g.ldo);
+    return launch_check("logits_popc_kernel");
+}
 
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;

@@ -80,6 +80,9 @@ int launch_chain(const ChainParams& p, cudaStream_t s);
 // Swapped-operand conv (fused_swap_kernel): 128 channels x 256 positions per tile, bits
 // epilogue, CTA-local; tm must be the weight map with box rows 128.
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
+// Tiny final logits layer on the CUDA cores (logits_popc_kernel); wbits from prep_logit_bits.
+int prep_logit_bits(const int8_t* w8, int Kpad, int K, int D, int Kw, uint32_t* wbits, cudaStream_t s);
+int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s);
 
 int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
                        int Kpad, int8_t* out, cudaStream_t s);

@@ -90,7 +90,8 @@ struct FusedStage {
     FusedGeom g{};               // batch-independent fields
     int Dpad = 0, Kpad = 0;
     bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
-    DevBuf w8, prm;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
+    bool small_logits = false;   // tiny final layer: CUDA-core popcount kernel (wbits)
+    DevBuf w8, prm, wbits;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
     CUtensorMap tm[5];           // weight tile maps, box rows 16, 32, 64, 128, 256 (= BN / cta_group)
     size_t out_words_per_image = 0;
 };
@@ -344,6 +345,11 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         const int bns[5] = {16, 32, 64, 128, 256};
         for (int b = 0; b < 5; ++b)
             BNN_TRY(fused_make_tmap(&st->tm[b], st->w8.as<int8_t>(), st->Dpad, st->Kpad, bns[b]));
+        if (st->epi == FEPI_LOGITS && kind == BNN_LAYER_LINEAR && g.D <= 64) {
+            st->small_logits = true;
+            BNN_TRY(st->wbits.alloc(size_t(g.D) * g.Cw * sizeof(uint32_t)));
+            BNN_TRY(prep_logit_bits(st->w8.as<int8_t>(), st->Kpad, g.K, g.D, g.Cw, st->wbits.as<uint32_t>(), s));
+        }
         if (st->epi == FEPI_BITS) {
             const size_t pos = kind == BNN_LAYER_CONV ? size_t(g.OH) * g.OW / (pool ? 4 : 1) : 1;
             st->out_words_per_image = pos * g.Dw;
@@ -536,6 +542,7 @@ int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stage
 // (wider layers measured slower: the swapped stage is shared-memory-bandwidth bound); 0 off.
 // Forced tilings (bnn_set_fused_tiling) keep the position-major kernel.
 int g_swap = -1;
+int g_small_logits = 1;  // bnn_set_fused_small_logits: tiny final layers on the CUDA cores
 
 bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
     if (g_swap < 0) g_swap = getenv("BNN_FUSED_SWAP") ? atoi(getenv("BNN_FUSED_SWAP")) : 1;
@@ -637,7 +644,9 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             ++launches;
         }
         EventPair gemm_ev(net, st.layer, 1, s);
-        if (use_swap(net, st, plans[i].cg))
+        if (st.small_logits && g_small_logits)
+            BNN_TRY(launch_logits_popc(g, st.wbits.as<uint32_t>(), s));
+        else if (use_swap(net, st, plans[i].cg))
             BNN_TRY(launch_swap(st.in_mode, st.tm[box_index(128)], g, s));
         else
             BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
@@ -851,6 +860,12 @@ int bnn_set_fused_split(int split) {
 }
 
 int bnn_debug_timeline(int op) { return fused_timeline(op); }
+
+int bnn_set_fused_small_logits(int enabled) {
+    g_small_logits = enabled ? 1 : 0;
+    ++g_tiling_epoch;
+    return BNN_OK;
+}
 
 int bnn_set_fused_swap(int enabled) {
     if (enabled < 0 || enabled > 2) return fail(BNN_E_CONFIG, "fused swap: 0 (off), 1 (<= 128 channels) or 2 (all)");

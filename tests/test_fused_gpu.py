@@ -52,7 +52,7 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "noswap", "swapall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "noswap", "swapall", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -68,12 +68,14 @@ def tiling(bnn, request):
                                             "chain_split16": 16}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
     bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
+    bnn._lib.check(lib.bnn_set_fused_small_logits(0 if p == "nosmall" else 1))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_tmem_a(1)
     lib.bnn_set_fused_split(0)
     lib.bnn_set_fused_chain(0)
     lib.bnn_set_fused_swap(1)
+    lib.bnn_set_fused_small_logits(1)
 
 
 @pytest.fixture
