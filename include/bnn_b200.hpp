@@ -174,6 +174,7 @@ struct LayerSpec {
     std::size_t out_features = 0;
     KernelChoice kernel = KernelChoice::Float;
     std::optional<std::uint64_t> seed;
+    std::string weights_blob;  // tensor blob path; empty -> seeded weights (network.hpp:36)
 };
 
 struct NetworkSpec {
@@ -192,6 +193,8 @@ NetworkSpec build_default_network(KernelChoice kernel, std::uint64_t seed);
 class DeviceNetwork {
 public:
     explicit DeviceNetwork(const NetworkSpec& spec);
+    // load_network_spec (network.cpp:487-536) + build_network: a NetworkSpec JSON file.
+    static DeviceNetwork from_spec_file(const std::string& path);
     ~DeviceNetwork();
     DeviceNetwork(const DeviceNetwork&) = delete;
     DeviceNetwork& operator=(const DeviceNetwork&) = delete;
@@ -201,9 +204,20 @@ public:
     bnn_net* handle() const { return net_; }
 
 private:
+    DeviceNetwork() = default;
     bnn_net* net_ = nullptr;
     std::array<std::size_t, 3> in_chw_{};
+
+public:
+    DeviceNetwork(DeviceNetwork&& o) noexcept : net_(o.net_), in_chw_(o.in_chw_) { o.net_ = nullptr; }
 };
+
+// ------------------------------------------------------- on-disk formats (binarize.hpp:28-32,
+// tensor.hpp:129-133): byte-identical to the reference's files, same IoError messages.
+void save_packed_blob(const PackedBitMatrix& p, const std::string& path);
+PackedBitMatrix load_packed_blob(const std::string& path);
+void save_tensor_blob(const FloatTensor& t, const std::string& path);
+FloatTensor load_tensor_blob(const std::string& path);
 
 FloatMatrix network_forward(DeviceNetwork& net, const FloatTensor& x);
 

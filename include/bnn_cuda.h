@@ -155,12 +155,13 @@ int bnn_fnv1a_f32(const float* x, size_t n, uint64_t* hash, bnn_stream_t s);
 enum { BNN_LAYER_CONV = 0, BNN_LAYER_LINEAR = 1, BNN_LAYER_MAXPOOL = 2, BNN_LAYER_AFFINE = 3,
        BNN_LAYER_SIGN = 4, BNN_LAYER_HTANH = 5 }; /* LayerKind order, network.hpp:15 */
 
-typedef struct { /* LayerSpec (network.hpp:23-39), binary kernel, seeded weights */
+typedef struct { /* LayerSpec (network.hpp:23-39), binary kernel */
     uint32_t kind;
     uint32_t has_seed;
     uint64_t seed;
     uint64_t out_channels, kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w;
     uint64_t out_features;
+    const char* weights_blob; /* tensor blob path of the float weights; NULL -> seeded weights */
 } bnn_layer_spec;
 
 typedef struct bnn_net bnn_net;
@@ -223,6 +224,22 @@ int bnn_set_fused_swap(int enabled);
 /* Fused engine: a final layer of <= 64 logits runs as a CUDA-core xnor-popcount kernel (1,
  * default) or on the tensor cores like the other layers (0). Bit-exact either way. */
 int bnn_set_fused_small_logits(int enabled);
+/* ------------------------------------------------------- on-disk formats (host side)
+ * packed blob (binarize.cpp:116-148): orientation byte, rows and cols (u64 LE), words (u32 LE).
+ * tensor blob (tensor.cpp:123-150): batch, channels, height, width (u64 LE), floats (f32 LE).
+ * Loaders with a NULL output pointer return the header only. Errors: BNN_E_IO with the
+ * reference's IoError messages ("packed blob size mismatch: <path>", ...). */
+int bnn_save_packed_blob(const char* path, int orientation, uint64_t rows, uint64_t cols,
+                         const uint32_t* words);
+int bnn_load_packed_blob(const char* path, int* orientation, uint64_t* rows, uint64_t* cols,
+                         uint32_t* words, size_t cap_words);
+int bnn_save_tensor_blob(const char* path, const uint64_t shape[4], const float* data);
+int bnn_load_tensor_blob(const char* path, uint64_t shape[4], float* data, size_t cap);
+/* load_network_spec (network.cpp:487-536) + build_network: a NetworkSpec JSON file (layers
+ * may name a weights_blob tensor blob). binarize_override -1 keeps the spec's flag. */
+int bnn_net_create_from_spec(const char* path, int binarize_override, bnn_net** out);
+int bnn_spec_info(const char* path, uint64_t input_shape[4], size_t* n_layers);
+
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */
 int bnn_debug_timeline(int op);

@@ -341,6 +341,10 @@ class RefLib:
         L.bnnref_net_build_file.restype = _P
         L.bnnref_net_build_file.argtypes = [C.c_char_p, C.c_int]
         L.bnnref_net_free.argtypes = [_P]
+        L.bnnref_save_packed_blob.argtypes = [C.c_char_p, C.c_int, _SZ, _SZ, _P]
+        L.bnnref_load_packed_blob.argtypes = [C.c_char_p, _P, _P]
+        L.bnnref_save_tensor_blob.argtypes = [C.c_char_p, _P, _P]
+        L.bnnref_load_tensor_blob.argtypes = [C.c_char_p, _P, _P]
         L.bnnref_net_info.argtypes = [_P, _P]
         L.bnnref_net_layer_info.argtypes = [_P, _SZ, _P]
         L.bnnref_net_layer_params.argtypes = [_P, _SZ, _P, _P, _P, _P]
@@ -461,6 +465,32 @@ class RefLib:
     def fnv1a(self, x):
         x = np.ascontiguousarray(x, np.float32)
         return int(self.lib.bnnref_fnv1a(x.ctypes.data, x.size))
+
+    def save_packed_blob(self, path, orientation, rows, cols, words):
+        w = np.ascontiguousarray(words, np.uint32)
+        self._check(self.lib.bnnref_save_packed_blob(str(path).encode(), int(orientation), rows, cols, w.ctypes.data))
+
+    def load_packed_blob(self, path):
+        """-> (orientation 0/1, rows, cols, words [lines, wpl])"""
+        d = np.zeros(3, np.uint64)
+        self._check(self.lib.bnnref_load_packed_blob(str(path).encode(), d.ctypes.data, None))
+        o, r, c = (int(v) for v in d)
+        lines, extent = (r, c) if o == 0 else (c, r)
+        w = np.zeros((lines, words_per_line(extent)), np.uint32)
+        self._check(self.lib.bnnref_load_packed_blob(str(path).encode(), d.ctypes.data, w.ctypes.data))
+        return o, r, c, w
+
+    def save_tensor_blob(self, path, x):
+        x = np.ascontiguousarray(x, np.float32)
+        shape = np.asarray(x.shape, np.uint64)
+        self._check(self.lib.bnnref_save_tensor_blob(str(path).encode(), shape.ctypes.data, x.ctypes.data))
+
+    def load_tensor_blob(self, path):
+        shape = np.zeros(4, np.uint64)
+        self._check(self.lib.bnnref_load_tensor_blob(str(path).encode(), shape.ctypes.data, None))
+        out = np.zeros(tuple(int(v) for v in shape), np.float32)
+        self._check(self.lib.bnnref_load_tensor_blob(str(path).encode(), shape.ctypes.data, out.ctypes.data))
+        return out
 
     def net_default(self, seed=1, binarize=False):
         h = self.lib.bnnref_net_build_default(seed, int(binarize))

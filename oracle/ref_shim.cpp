@@ -252,6 +252,40 @@ void* bnnref_net_build_file(const char* path, int binarize_weights) {
 
 void bnnref_net_free(void* h) { delete static_cast<RefNet*>(h); }
 
+// save_packed_blob / load_packed_blob (binarize.cpp:116-148)
+int bnnref_save_packed_blob(const char* path, int orientation, std::size_t rows, std::size_t cols,
+                            const std::uint32_t* words) {
+    return guarded([&] {
+        PackedBitMatrix p = PackedBitMatrix::make(rows, cols, static_cast<PackOrientation>(orientation));
+        std::memcpy(p.words.data(), words, p.words.size() * 4);
+        save_packed_blob(p, path);
+    });
+}
+
+// dims[0] = orientation, dims[1] = rows, dims[2] = cols; words NULL: header only
+int bnnref_load_packed_blob(const char* path, std::size_t dims[3], std::uint32_t* words) {
+    return guarded([&] {
+        PackedBitMatrix p = load_packed_blob(path);
+        dims[0] = static_cast<std::size_t>(p.orientation);
+        dims[1] = p.logical_rows;
+        dims[2] = p.logical_cols;
+        if (words) std::memcpy(words, p.words.data(), p.words.size() * 4);
+    });
+}
+
+// save_tensor_blob / load_tensor_blob (tensor.cpp:123-150)
+int bnnref_save_tensor_blob(const char* path, const std::size_t shape[4], const float* data) {
+    return guarded([&] { save_tensor_blob(make_tensor(data, shape[0], shape[1], shape[2], shape[3]), path); });
+}
+
+int bnnref_load_tensor_blob(const char* path, std::size_t shape[4], float* data) {
+    return guarded([&] {
+        FloatTensor t = load_tensor_blob(path);
+        shape[0] = t.batch, shape[1] = t.channels, shape[2] = t.height, shape[3] = t.width;
+        if (data) std::memcpy(data, t.data.data(), t.data.size() * 4);
+    });
+}
+
 // dims[0..3] = default input shape (B, C, H, W), dims[4] = logits, dims[5] = layer count
 void bnnref_net_info(void* h, std::size_t dims[6]) {
     const Network& n = static_cast<RefNet*>(h)->net;

@@ -10,6 +10,6 @@ from ._lib import (BnnError, ConfigError, CudaError, EncodingError, IoError, Sha
 from .api import (COL_PACKED, ROW_PACKED, ConvGeometry, Network, PackedBitMatrix,  # noqa: F401
                   affine_norm, bias_add, conv_forward_binary, default_layers, fill_random,
                   flatten_to_columns, fnv1a_hash, htanh, im2col_sign_pack, linear_forward,
-                  linear_forward_packed, maxpool2, mix64, output_dims, pack_cols, pack_rows,
-                  sign, sign_pack_cols, sign_pack_rows, to_float, unpack, words_per_line,
-                  xnor_gemm)
+                  linear_forward_packed, load_packed_blob, load_tensor_blob, maxpool2, mix64,
+                  output_dims, pack_cols, pack_rows, save_packed_blob, save_tensor_blob, sign,
+                  sign_pack_cols, sign_pack_rows, to_float, unpack, words_per_line, xnor_gemm)

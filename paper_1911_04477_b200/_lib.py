@@ -60,7 +60,7 @@ class LayerSpec(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("has_seed", C.c_uint32), ("seed", _U64),
                 ("out_channels", _U64), ("kernel_h", _U64), ("kernel_w", _U64),
                 ("stride_h", _U64), ("stride_w", _U64), ("pad_h", _U64), ("pad_w", _U64),
-                ("out_features", _U64)]
+                ("out_features", _U64), ("weights_blob", C.c_char_p)]
 
 
 _SIGS = {
@@ -108,6 +108,12 @@ _SIGS = {
     "bnn_debug_timeline": (_I, [_I]),
     "bnn_set_fused_swap": (_I, [_I]),
     "bnn_set_fused_small_logits": (_I, [_I]),
+    "bnn_save_packed_blob": (_I, [C.c_char_p, _I, _U64, _U64, _P]),
+    "bnn_load_packed_blob": (_I, [C.c_char_p, C.POINTER(_I), C.POINTER(_U64), C.POINTER(_U64), _P, _SZ]),
+    "bnn_save_tensor_blob": (_I, [C.c_char_p, _P, _P]),
+    "bnn_load_tensor_blob": (_I, [C.c_char_p, _P, _P, _SZ]),
+    "bnn_net_create_from_spec": (_I, [C.c_char_p, _I, _P]),
+    "bnn_spec_info": (_I, [C.c_char_p, _P, C.POINTER(_SZ)]),
     "bnn_net_set_timing": (_I, [_P, _I]),
     "bnn_net_timing": (_I, [_P, _P, _P, _P]),
     "bnn_net_reset_timing": (_I, [_P]),

@@ -408,6 +408,8 @@ def layer_specs(layers) -> "C.Array":
             arr[i].pad_h, arr[i].pad_w = _pair(l.get("pad"), 0)
         elif k == "linear":
             arr[i].out_features = int(l["out_features"])
+        if k in ("conv", "linear") and l.get("weights_blob"):
+            arr[i].weights_blob = str(l["weights_blob"]).encode()  # the array keeps the bytes alive
     return arr
 
 
@@ -427,6 +429,45 @@ def default_layers() -> list[dict]:
     return out
 
 
+# ------------------------------------------------------------------ on-disk formats (csrc/io.cpp)
+
+
+def save_packed_blob(p: PackedBitMatrix, path) -> None:
+    """save_packed_blob (binarize.cpp:116-127)."""
+    o = 0 if p.orientation == ROW_PACKED else 1
+    w = np.ascontiguousarray(p.words, np.uint32)
+    check(load().bnn_save_packed_blob(str(path).encode(), o, p.logical_rows, p.logical_cols, _p(w)))
+
+
+def load_packed_blob(path) -> PackedBitMatrix:
+    """load_packed_blob (binarize.cpp:129-148): IoError on a truncated / mismatched / dirty blob."""
+    lib = load()
+    o, r, c = C.c_int(), C.c_uint64(), C.c_uint64()
+    check(lib.bnn_load_packed_blob(str(path).encode(), C.byref(o), C.byref(r), C.byref(c), None, 0))
+    p = PackedBitMatrix.make(r.value, c.value, ROW_PACKED if o.value == 0 else COL_PACKED)
+    check(lib.bnn_load_packed_blob(str(path).encode(), C.byref(o), C.byref(r), C.byref(c), _p(p.words), p.words.size))
+    return p
+
+
+def save_tensor_blob(x, path) -> None:
+    """save_tensor_blob (tensor.cpp:123-134): x is [batch, channels, height, width]."""
+    x = _f32(x)
+    if x.ndim != 4:
+        raise ShapeError("tensor blob needs a 4-d [batch, channels, height, width] array")
+    shape = np.asarray(x.shape, np.uint64)
+    check(load().bnn_save_tensor_blob(str(path).encode(), _p(shape), _p(x)))
+
+
+def load_tensor_blob(path) -> np.ndarray:
+    """load_tensor_blob (tensor.cpp:136-150)."""
+    lib = load()
+    shape = np.zeros(4, np.uint64)
+    check(lib.bnn_load_tensor_blob(str(path).encode(), _p(shape), None, 0))
+    out = np.zeros(tuple(int(v) for v in shape), np.float32)
+    check(lib.bnn_load_tensor_blob(str(path).encode(), _p(shape), _p(out), out.size))
+    return out
+
+
 class Network:
     """build_network + network_forward(ExecKernel::Binary) on the current CUDA device."""
 
@@ -441,6 +482,27 @@ class Network:
         self._h = h
         self.input_chw = tuple(input_chw)
         self.logits = int(lib.bnn_net_logits(h))
+
+    @classmethod
+    def from_spec_file(cls, path, binarize_weights=None) -> "Network":
+        """load_network_spec (network.cpp:487-536) + build_network: a NetworkSpec JSON file,
+        layers may take their float weights from a ``weights_blob`` tensor blob."""
+        import json as _json
+
+        lib = load()
+        h = C.c_void_p()
+        check(lib.bnn_net_create_from_spec(str(path).encode(), -1 if binarize_weights is None else int(binarize_weights),
+                                           C.byref(h)))
+        self = cls.__new__(cls)
+        spec = _json.load(open(path))
+        self.layers = spec["layers"]
+        shape = np.zeros(4, np.uint64)
+        n = C.c_size_t()
+        check(lib.bnn_spec_info(str(path).encode(), _p(shape), C.byref(n)))
+        self._h = h
+        self.input_chw = tuple(int(v) for v in shape[1:])
+        self.logits = int(lib.bnn_net_logits(h))
+        return self
 
     @classmethod
     def from_spec(cls, spec: dict) -> "Network":

@@ -28,8 +28,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hid
 
 CXX = os.environ.get("CXX", "g++")
 # the C++ reference-signature API (cpp_api.cpp) is C++20 like the reference (std::span)
+# nlohmann/json (NetworkSpec JSON, csrc/io.cpp): the reference's own JSON library (network.cpp:6),
+# used from the copy that ships inside the image's Python environment
+JSON_INC = os.environ.get("BNN_JSON_INC", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-fvisibility=hidden", "-Wall", f"-I{os.path.join(ROOT, 'include')}",
-            "-I/usr/local/cuda/include"]
+            "-I/usr/local/cuda/include", f"-I{JSON_INC}"]
 
 
 def _compile(src: str) -> str:

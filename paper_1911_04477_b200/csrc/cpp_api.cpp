@@ -361,6 +361,7 @@ DeviceNetwork::DeviceNetwork(const NetworkSpec& spec) {
         c.stride_h = l.stride_h, c.stride_w = l.stride_w;
         c.pad_h = l.pad_h, c.pad_w = l.pad_w;
         c.out_features = l.out_features;
+        c.weights_blob = l.weights_blob.empty() ? nullptr : l.weights_blob.c_str();
         layers.push_back(c);
     }
     in_chw_ = {spec.input_shape[1], spec.input_shape[2], spec.input_shape[3]};
@@ -368,7 +369,44 @@ DeviceNetwork::DeviceNetwork(const NetworkSpec& spec) {
                          spec.binarize_weights ? 1 : 0, &net_));
 }
 
-DeviceNetwork::~DeviceNetwork() { bnn_net_destroy(net_); }
+DeviceNetwork DeviceNetwork::from_spec_file(const std::string& path) {
+    DeviceNetwork n;
+    std::uint64_t shape[4];
+    check(bnn_spec_info(path.c_str(), shape, nullptr));
+    n.in_chw_ = {shape[1], shape[2], shape[3]};
+    check(bnn_net_create_from_spec(path.c_str(), -1, &n.net_));
+    return n;
+}
+
+DeviceNetwork::~DeviceNetwork() {
+    if (net_) bnn_net_destroy(net_);
+}
+
+void save_packed_blob(const PackedBitMatrix& p, const std::string& path) {  // binarize.cpp:116-127
+    check(bnn_save_packed_blob(path.c_str(), int(p.orientation), p.logical_rows, p.logical_cols, p.words.data()));
+}
+
+PackedBitMatrix load_packed_blob(const std::string& path) {  // binarize.cpp:129-148
+    int o = 0;
+    std::uint64_t r = 0, c = 0;
+    check(bnn_load_packed_blob(path.c_str(), &o, &r, &c, nullptr, 0));
+    PackedBitMatrix p = PackedBitMatrix::make(r, c, static_cast<PackOrientation>(o));
+    check(bnn_load_packed_blob(path.c_str(), &o, &r, &c, p.words.data(), p.words.size()));
+    return p;
+}
+
+void save_tensor_blob(const FloatTensor& t, const std::string& path) {  // tensor.cpp:123-134
+    const std::uint64_t shape[4] = {t.batch, t.channels, t.height, t.width};
+    check(bnn_save_tensor_blob(path.c_str(), shape, t.data.data()));
+}
+
+FloatTensor load_tensor_blob(const std::string& path) {  // tensor.cpp:136-150
+    std::uint64_t shape[4];
+    check(bnn_load_tensor_blob(path.c_str(), shape, nullptr, 0));
+    FloatTensor t(shape[0], shape[1], shape[2], shape[3]);
+    check(bnn_load_tensor_blob(path.c_str(), shape, t.data.data(), t.data.size()));
+    return t;
+}
 
 std::size_t DeviceNetwork::logits() const { return bnn_net_logits(net_); }
 

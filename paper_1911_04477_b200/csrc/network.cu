@@ -218,11 +218,28 @@ int build(bnn_net* net, const bnn_layer_spec* specs, size_t n, uint64_t seed, cu
             default:
                 return fail(BNN_E_CONFIG, "unknown layer kind " + std::to_string(specs[i].kind));
         }
-        if (L->rows) {  // weighted layer: generate, binarize, pack once
+        if (L->rows) {  // weighted layer: generate (or load), binarize, pack once
             L->wpl = wpl_of(L->cols);
             const size_t nw = L->rows * L->cols;
             if (tmp.bytes < nw * 4) BNN_TRY(tmp.alloc(nw * 4));
-            BNN_TRY(fill(tmp.as<float>(), nw, mix64(base, 1), s));
+            if (specs[i].weights_blob) {  // network.cpp:233-241 / 258-266
+                uint64_t shp[4];
+                BNN_TRY(bnn_load_tensor_blob(specs[i].weights_blob, shp, nullptr, 0));
+                const bool conv = specs[i].kind == BNN_LAYER_CONV;
+                const bool ok = conv ? (shp[0] == L->rows && shp[1] == L->in_c && shp[2] == specs[i].kernel_h &&
+                                        shp[3] == specs[i].kernel_w)
+                                     : (shp[0] == L->rows && shp[1] == L->cols && shp[2] == 1 && shp[3] == 1);
+                if (!ok)
+                    return chain_error(conv ? "weights blob shape does not match [D, C, kH, kW]"
+                                            : "weights blob shape does not match [out, in, 1, 1]");
+                std::vector<float> hw(nw);
+                BNN_TRY(bnn_load_tensor_blob(specs[i].weights_blob, shp, hw.data(), nw));
+                // flatten_weights is the identity on [D, C, kH, kW] memory (lowering.cpp:97-102)
+                BNN_CUDA(cudaMemcpyAsync(tmp.p, hw.data(), nw * 4, cudaMemcpyHostToDevice, s));
+                BNN_CUDA(cudaStreamSynchronize(s));  // hw is released on scope exit
+            } else {
+                BNN_TRY(fill(tmp.as<float>(), nw, mix64(base, 1), s));
+            }
             BNN_TRY(L->packed.alloc(L->rows * L->wpl * 4));
             BNN_TRY(launch_pack_rows(tmp.as<float>(), L->rows, L->cols, L->packed.as<uint32_t>(),
                                      L->wpl, nullptr, s));

@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <unistd.h>
 #include <functional>
 #include <string>
 
@@ -193,12 +195,27 @@ void test_network() {
     const auto wrong = bnn::fill_random(1, 3, 16, 16, 1);
     CHECK(throws_with<bnn::ShapeError>([&] { net.forward(wrong); }, "network expects"));
 }
+void test_io() {  // on-disk formats: round trips and the reference's IoError messages
+    const std::string dir = "/tmp/bnn_cpp_io_" + std::to_string(::getpid());
+    std::system(("mkdir -p " + dir).c_str());
+    bnn::FloatMatrix w = bnn::fill_random_matrix(5, 40, 3);
+    const auto p = bnn::sign_pack_rows(w);
+    bnn::save_packed_blob(p, dir + "/w.pbm");
+    const auto q = bnn::load_packed_blob(dir + "/w.pbm");
+    CHECK(q.logical_rows == 5 && q.logical_cols == 40 && q.orientation == p.orientation && q.words == p.words);
+    const auto t = bnn::fill_random(2, 3, 4, 5, 9);
+    bnn::save_tensor_blob(t, dir + "/t.tb");
+    const auto u = bnn::load_tensor_blob(dir + "/t.tb");
+    CHECK(u.batch == 2 && u.channels == 3 && u.height == 4 && u.width == 5 && u.data == t.data);
+    CHECK(throws_with<bnn::IoError>([&] { bnn::load_tensor_blob(dir + "/missing.tb"); }, "cannot open for reading"));
+    std::system(("rm -rf " + dir).c_str());
+}
 }  // namespace
 
 int main() {
     const std::pair<const char*, void (*)()> suites[] = {{"tensor", test_tensor},   {"binarize", test_binarize},
                                                         {"gemm", test_gemm},       {"layers", test_layers},
-                                                        {"network", test_network}};
+                                                        {"network", test_network}, {"io", test_io}};
     for (const auto& [name, fn] : suites) {
         try {
             fn();
