@@ -332,6 +332,23 @@ def measure_configs(lib, dev, st, flush, seed, peak, cpu):
     out["cfg4_fc_stack_b1024"] = c4
     del xf, yf, net
 
+    # The paper's comparison: the binary network vs the float control group
+    # (ExecKernel::Float, CUDA-core FP32 without vendor libraries, csrc/control.cu) on this GPU
+    Bc = 256
+    netf = bnn.Network(seed=seed)
+    netf.set_engine("float")
+    xc2 = fill((Bc, 3, 32, 32), bnn.mix64(seed, INPUT_STREAM))
+    yc2 = torch.empty((10, Bc), dtype=torch.float32, device=dev)
+    ms_f = _dev_time(lambda: netf.forward_device(xc2, yc2, S), st, flush, 3)
+    netb = bnn.Network(seed=seed)
+    ms_b = _dev_time(lambda: netb.forward_device(xc2, yc2, S), st, flush, 20)
+    out["control_group_vgg_b256"] = {
+        "shape": "default network (cfg3) batch 256: binary fused engine vs float control group",
+        "float_ms": ms_f, "float_images_per_s": Bc / (ms_f * 1e-3), "binary_ms": ms_b,
+        "binary_images_per_s": Bc / (ms_b * 1e-3), "binary_over_float": ms_f / ms_b,
+        "paper": "GTX 1080 Ti: binary 3.57 s vs control 11.23 s per 10k images (3.1x), PAPER.md:193-197"}
+    del netf, netb, xc2, yc2
+
     # K1 encoder, HBM-bound: pack_cols(sign(X)) of a 1 GiB float matrix (> L2)
     Lk, Nk = 16384, 16384
     xe = torch.empty((Lk, Nk), dtype=torch.float32, device=dev)

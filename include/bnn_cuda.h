@@ -198,7 +198,10 @@ int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]);
  * activations; available when the topology matches conv {[maxpool][affine][htanh][sign]
  * conv|linear}* linear (the default network does). GENERIC: one kernel per reference op.
  * AUTO (default) = FUSED when available. Both are bit-exact with the reference. */
-enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2 };
+/* BNN_ENGINE_FLOAT: the paper's float control group (ExecKernel::Float: conv_forward_float /
+ * linear_forward Float on the float weights, control.cu), bit-exact with the reference's
+ * FMA-contracted float_gemm. */
+enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2, BNN_ENGINE_FLOAT = 3 };
 int bnn_net_set_engine(bnn_net* net, int policy);
 /* Fused-engine tile shape override, process-wide (tests / experiments): cta_group 1 (M=128
  * per CTA) or 2 (CTA pairs, M=256, tcgen05 cta_group::2), bn = MMA N in {32,64,128,256};
@@ -224,6 +227,15 @@ int bnn_set_fused_swap(int enabled);
 /* Fused engine: a final layer of <= 64 logits runs as a CUDA-core xnor-popcount kernel (1,
  * default) or on the tensor cores like the other layers (0). Bit-exact either way. */
 int bnn_set_fused_small_logits(int enabled);
+/* ------------------------------------------------- the float control group (control.cu)
+ * float_gemm (kernels.cpp:33-51): w [M, K] x [K, N], k-ascending FMA chain per output, then
+ * + bias (may be NULL) with the reshape epilogue of bnn_xnor_gemm_bias_f32 (P = 0: P = N). */
+int bnn_float_gemm_f32(const float* w, size_t M, size_t K, const float* x, size_t N, const float* bias,
+                       size_t P, float* out, bnn_stream_t s);
+/* conv_forward_float (network.cpp:50-63). */
+int bnn_conv_forward_float_f32(const float* x, size_t B, size_t C, size_t H, size_t W, const float* w_flat,
+                               const float* bias, const bnn_conv_geom* g, float* out, bnn_stream_t s);
+
 /* ------------------------------------------------------- on-disk formats (host side)
  * packed blob (binarize.cpp:116-148): orientation byte, rows and cols (u64 LE), words (u32 LE).
  * tensor blob (tensor.cpp:123-150): batch, channels, height, width (u64 LE), floats (f32 LE).

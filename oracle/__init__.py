@@ -539,7 +539,7 @@ class RefNet:
     def forward(self, x, exec_kind="binary", threads=1, batch_threads=1):
         x = np.ascontiguousarray(x, np.float32)
         out = np.empty((self.logits, x.shape[0]), np.float32)
-        ek = {"binary": 2, "binary_reference": 4}[exec_kind]
+        ek = {"float": 1, "binary": 2, "binary_reference": 4}[exec_kind]  # ExecKernel (network.hpp:91)
         self.ref._check(self.ref.lib.bnnref_net_forward(self.h, x.ctypes.data, x.shape[0], ek,
                                                         threads, batch_threads, out.ctypes.data))
         return out

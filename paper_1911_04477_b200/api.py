@@ -538,7 +538,7 @@ class Network:
         check(load().bnn_net_forward(self._h, x.data_ptr(), B, out.data_ptr(), st))
         return out
 
-    ENGINES = {"auto": 0, "generic": 1, "fused": 2}
+    ENGINES = {"auto": 0, "generic": 1, "fused": 2, "float": 3}
 
     def set_engine(self, name: str) -> None:
         """Select the device engine: "fused" (one tcgen05 launch per weighted layer, packed-bit
@@ -548,7 +548,7 @@ class Network:
 
     @property
     def engine(self) -> str:
-        return {1: "generic", 2: "fused"}[int(load().bnn_net_engine(self._h))]
+        return {1: "generic", 2: "fused", 3: "float"}[int(load().bnn_net_engine(self._h))]
 
     def last_launches(self) -> int:
         return int(load().bnn_net_last_launches(self._h))

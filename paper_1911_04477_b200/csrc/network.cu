@@ -41,6 +41,8 @@ int launch_transpose(const float*, size_t, size_t, float*, cudaStream_t);
 int launch_fill_random(uint64_t, uint64_t, size_t, float*, cudaStream_t);
 int launch_affine_scale(float*, size_t, cudaStream_t);
 int launch_unary(int, const float*, size_t, float*, cudaStream_t);
+int launch_float_gemm(const float*, const float*, size_t, size_t, size_t, const float*, size_t, float*, cudaStream_t);
+int launch_im2col_f32(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*, float*, cudaStream_t);
 
 namespace {
 
@@ -75,6 +77,7 @@ struct Layer {
     bnn_layer_spec spec{};
     bnn_conv_geom geom{};
     size_t rows = 0, cols = 0, wpl = 0;  // packed weights: rows lines x wpl words, L = cols
+    DevBuf wf;                           // float weights [rows, cols] (the float control group)
     DevBuf packed, bias, scale, shift;
     size_t n_affine = 0;
     size_t in_c = 0, in_h = 0, in_w = 0;  // input shape (per image)
@@ -143,7 +146,8 @@ struct bnn_net {
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix, ws, sem;
-    bnnk::DevBuf chain_done;  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
+    bnnk::DevBuf chain_done;
+    bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
 };
 
 namespace bnnk {
@@ -240,6 +244,8 @@ int build(bnn_net* net, const bnn_layer_spec* specs, size_t n, uint64_t seed, cu
             } else {
                 BNN_TRY(fill(tmp.as<float>(), nw, mix64(base, 1), s));
             }
+            BNN_TRY(L->wf.alloc(nw * 4));  // network.cpp:246,269: layer.weights, kept for ExecKernel::Float
+            BNN_CUDA(cudaMemcpyAsync(L->wf.p, tmp.p, nw * 4, cudaMemcpyDeviceToDevice, s));
             BNN_TRY(L->packed.alloc(L->rows * L->wpl * 4));
             BNN_TRY(launch_pack_rows(tmp.as<float>(), L->rows, L->cols, L->packed.as<uint32_t>(),
                                      L->wpl, nullptr, s));
@@ -552,6 +558,85 @@ int forward_generic(bnn_net* net, const float* x, size_t B, float* logits, cudaS
 int g_chain = -1;
 int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
 
+// The float control group (network_forward with ExecKernel::Float, network.cpp:350-420): the
+// same graph with conv_forward_float / linear_forward(Float) on the float weights (control.cu).
+int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+    BNN_TRY(ensure_arena(net, B));
+    size_t launches = 0;
+    const float* cur = x;
+    int which = 0;
+    auto next = [&]() { float* o = net->act[which].as<float>(); which ^= 1; return o; };
+    for (size_t li = 0; li < net->layers.size(); ++li) {
+        Layer& L = *net->layers[li];
+        EventPair layer_ev(net, li, 0, s);
+        switch (L.spec.kind) {
+            case BNN_LAYER_CONV: {
+                float* out = next();
+                const size_t N = B * L.out_h * L.out_w;
+                if (net->fcols.bytes < L.cols * N * 4) BNN_TRY(net->fcols.alloc(L.cols * N * 4));
+                BNN_TRY(launch_im2col_f32(cur, B, L.in_c, L.in_h, L.in_w, &L.geom, net->fcols.as<float>(), s));
+                EventPair gemm_ev(net, li, 1, s);
+                BNN_TRY(launch_float_gemm(L.wf.as<float>(), net->fcols.as<float>(), L.rows, N, L.cols,
+                                          L.bias.as<float>(), L.out_h * L.out_w, out, s));
+                gemm_ev.close();
+                launches += 2;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_LINEAR: {
+                if (!L.in_flat) {  // flatten_to_columns: [B, F] -> [F, B]
+                    float* t = next();
+                    BNN_TRY(launch_transpose(cur, B, L.cols, t, s));
+                    ++launches;
+                    cur = t;
+                }
+                float* out = next();
+                EventPair gemm_ev(net, li, 1, s);
+                BNN_TRY(launch_float_gemm(L.wf.as<float>(), cur, L.rows, B, L.cols, L.bias.as<float>(), B, out, s));
+                gemm_ev.close();
+                ++launches;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_MAXPOOL: {
+                float* out = next();
+                BNN_TRY(launch_maxpool2(cur, B, L.in_c, L.in_h, L.in_w, out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_AFFINE: {
+                float* out = next();
+                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
+                const size_t plane = L.in_flat ? B : L.in_h * L.in_w;
+                BNN_TRY(launch_affine(cur, n, L.in_c, plane, L.scale.as<float>(), L.shift.as<float>(), out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+            case BNN_LAYER_SIGN:
+            case BNN_LAYER_HTANH: {
+                float* out = next();
+                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
+                BNN_TRY(launch_unary(L.spec.kind == BNN_LAYER_SIGN ? 0 : 1, cur, n, out, s));
+                ++launches;
+                cur = out;
+                break;
+            }
+        }
+        layer_ev.close();
+    }
+    const Layer& last = *net->layers.back();
+    if (last.out_flat) {
+        BNN_CUDA(cudaMemcpyAsync(logits, cur, net->logits * B * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+        BNN_TRY(launch_transpose(cur, B, net->logits, logits, s));
+        ++launches;
+    }
+    net->last_launches = launches;
+    return BNN_OK;
+}
+
 // Swapped-operand conv kernel (fused_swap_kernel: channels on the MMA's M, positions on N)
 // for conv layers with a packed-bit epilogue. BNN_FUSED_SWAP / bnn_set_fused_swap: 1 (default)
 // for layers of <= 128 output channels, where the position-major kernel runs the MMA at half
@@ -761,6 +846,7 @@ int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaS
 
 int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
+    if (net->engine_policy == BNN_ENGINE_FLOAT) return forward_float(net, x, B, logits, s);
     if (use_fused(net)) return forward_graphed(net, x, B, logits, s);
     return forward_generic(net, x, B, logits, s);
 }
@@ -844,7 +930,7 @@ void bnn_net_destroy(bnn_net* net) {
 size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
 
 int bnn_net_set_engine(bnn_net* net, int policy) {
-    if (policy < BNN_ENGINE_AUTO || policy > BNN_ENGINE_FUSED)
+    if (policy < BNN_ENGINE_AUTO || policy > BNN_ENGINE_FLOAT)
         return fail(BNN_E_CONFIG, "bad engine policy");
     if (policy == BNN_ENGINE_FUSED && !net->fusable)
         return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
@@ -902,7 +988,10 @@ int bnn_set_fused_tmem_a(int enabled) {
     return fused_set_tmem_a(enabled);
 }
 
-int bnn_net_engine(const bnn_net* net) { return use_fused(net) ? BNN_ENGINE_FUSED : BNN_ENGINE_GENERIC; }
+int bnn_net_engine(const bnn_net* net) {
+    if (net->engine_policy == BNN_ENGINE_FLOAT) return BNN_ENGINE_FLOAT;
+    return use_fused(net) ? BNN_ENGINE_FUSED : BNN_ENGINE_GENERIC;
+}
 size_t bnn_net_num_layers(const bnn_net* net) { return net->layers.size(); }
 size_t bnn_net_last_launches(const bnn_net* net) { return net->last_launches; }
 
