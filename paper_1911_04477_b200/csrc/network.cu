@@ -672,6 +672,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         int cg, bn;
     };
     std::vector<Plan> plans;
+    size_t ws_need = 0, sem_need = 0;  // the largest split-K workspace of any stage
     const void* in = x;
     int which = 0;
     (void)prof;
@@ -689,22 +690,11 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         choose_tile(g.D, rows, g.KB, g.pool != 0, cg, bn, ks);
         g.n_tiles = int(ceil_div(size_t(g.D), size_t(bn)));
         g.ksplit = ks;
-        if (ks > 1) {  // split-K workspace and per-output-tile counters
+        if (ks > 1) {  // split-K workspace and per-output-tile counters (pointers set below)
             const size_t m_tiles = ceil_div(rows, size_t(128));
             g.ws_rows = int(m_tiles * 128), g.ws_ld = g.n_tiles * bn;
-            const size_t ws_bytes = size_t(ks) * g.ws_rows * g.ws_ld * 4;
-            const size_t sem_bytes = m_tiles * g.n_tiles * 2 * sizeof(unsigned);
-            if (net->ws.bytes < ws_bytes) {
-                BNN_TRY(net->ws.alloc(ws_bytes));
-                ++net->arena_epoch;
-            }
-            if (net->sem.bytes < sem_bytes) {
-                ++net->arena_epoch;
-                BNN_TRY(net->sem.alloc(sem_bytes));
-                BNN_CUDA(cudaMemsetAsync(net->sem.p, 0, sem_bytes, s));  // kernels leave them at 0
-            }
-            g.ws = net->ws.as<int>();
-            g.sem = net->sem.as<unsigned>();
+            ws_need = std::max(ws_need, size_t(ks) * g.ws_rows * g.ws_ld * 4);
+            sem_need = std::max(sem_need, m_tiles * g.n_tiles * 2 * sizeof(unsigned));
         }
         if (st.epi == FEPI_BITS) {
             g.out_bits = net->bits[which].as<uint32_t>();
@@ -732,6 +722,20 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         --first_chained;
     if (g_chain_tail == 0 && g_chain == 0) first_chained = plans.size();
     if (plans.size() - first_chained < 2 && g_chain == 0) first_chained = plans.size();  // nothing to save
+    // one split-K workspace shared by the stages (they run one after another), sized for the
+    // largest before any pointer is handed out: growing it between stages would leave the
+    // earlier stages' plans pointing at freed memory
+    if (net->ws.bytes < ws_need) {
+        BNN_TRY(net->ws.alloc(ws_need));
+        ++net->arena_epoch;
+    }
+    if (net->sem.bytes < sem_need) {
+        ++net->arena_epoch;
+        BNN_TRY(net->sem.alloc(sem_need));
+        BNN_CUDA(cudaMemsetAsync(net->sem.p, 0, sem_need, s));  // kernels leave them at 0
+    }
+    for (auto& pl : plans)
+        if (pl.g.ksplit > 1) pl.g.ws = net->ws.as<int>(), pl.g.sem = net->sem.as<unsigned>();
     size_t launches = 0;
     for (size_t i = 0; i < first_chained; ++i) {
         FusedStage& st = *net->stages[i];

@@ -1,0 +1,31 @@
+"""compute-sanitizer driver: one forward of the default network per engine setting and batch,
+each checked against the oracle (run under `compute-sanitizer --tool memcheck`)."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_1911_04477_b200 as bnn  # noqa: E402
+from oracle import Oracle  # noqa: E402
+
+orc = Oracle()
+lib = bnn.load()
+SETTINGS = {"default": {}, "split16": {"split": 16}, "nosplit": {"split": 1}, "chain": {"chain": 1},
+            "swapall": {"swap": 2}, "noswap": {"swap": 0}, "nosmall": {"small": 0}}
+bad = 0
+for name, st in SETTINGS.items():
+    lib.bnn_set_fused_split(st.get("split", 0))
+    lib.bnn_set_fused_chain(st.get("chain", 0))
+    lib.bnn_set_fused_swap(st.get("swap", 1))
+    lib.bnn_set_fused_small_logits(st.get("small", 1))
+    for b in (1, 5, 130):
+        net = bnn.Network(seed=1)
+        x = orc.fill_random((b, 3, 32, 32), orc.mix64(1, 0x696E707574))
+        ok = np.array_equal(net.forward(x), orc.net(seed=1).forward(x))
+        bad += not ok
+        print(name, b, ok, flush=True)
+net = bnn.Network(seed=1)
+net.set_engine("float")
+x = orc.fill_random((2, 3, 32, 32), 3)
+print("float", net.forward(x).shape)
+sys.exit(1 if bad else 0)
