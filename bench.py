@@ -496,7 +496,7 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(f"b{B}", {}).get(f"layer{top}")
         except (ValueError, OSError):
             traffic = None
-    kernel_name = lib.bnn_last_gemm_kernel().decode()
+    kernel_name = (lib.bnn_net_layer_kernel(net.handle, top) or lib.bnn_last_gemm_kernel()).decode()
 
     # ---- end to end through the public API: every step copies its input from pinned host memory
     # (H2D), runs the forward, and reads its logits back (D2H). Steps are pipelined like a

@@ -252,6 +252,8 @@ int bnn_load_tensor_blob(const char* path, uint64_t shape[4], float* data, size_
 int bnn_net_create_from_spec(const char* path, int binarize_override, bnn_net** out);
 int bnn_spec_info(const char* path, uint64_t input_shape[4], size_t* n_layers);
 
+/* Kernel the last fused forward ran for weighted layer `layer` ("" if none / not fused). */
+const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */
 int bnn_debug_timeline(int op);

@@ -94,6 +94,7 @@ struct FusedStage {
     int Dpad = 0, Kpad = 0;
     bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
     bool small_logits = false;   // tiny final layer: CUDA-core popcount kernel (wbits)
+    const char* kname = "";      // kernel the last forward ran for this stage
     DevBuf w8, prm, wbits;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
     CUtensorMap tm[5];           // weight tile maps, box rows 16, 32, 64, 128, 256 (= BN / cta_group)
     size_t out_words_per_image = 0;
@@ -756,6 +757,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             BNN_TRY(launch_swap(st.in_mode, st.tm[box_index(128)], g, s));
         else
             BNN_TRY(launch_fused(plans[i].cg, plans[i].bn, st.in_mode, st.epi, st.tm[box_index(plans[i].bn / plans[i].cg)], g, s));
+        st.kname = bnn_last_gemm_kernel();
         gemm_ev.close();
         layer_ev.close();
         ++launches;
@@ -788,6 +790,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             c.epi = st.epi;
         }
         BNN_TRY(launch_chain(cp, s));
+        for (size_t i = first_chained; i < plans.size(); ++i) net->stages[i]->kname = bnn_last_gemm_kernel();
         ++launches;
     }
     net->last_launches = launches;
@@ -967,6 +970,13 @@ int bnn_set_fused_split(int split) {
 }
 
 int bnn_debug_timeline(int op) { return fused_timeline(op); }
+
+const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer) {
+    if (net->engine_policy != BNN_ENGINE_FLOAT && use_fused(net))
+        for (const auto& st : net->stages)
+            if (st->layer == layer) return st->kname;
+    return "";
+}
 
 int bnn_set_fused_small_logits(int enabled) {
     g_small_logits = enabled ? 1 : 0;
