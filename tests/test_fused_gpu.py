@@ -45,6 +45,9 @@ FUSABLE = {
     "fc_stack": {"input_shape": [1, 288, 1, 1], "seed": 5, "layers": [lin(4096), lin(96), lin(10)]},
     # tensor input flattened (F = 100: a partial last word), glue between the linears
     "fc_tensor_in": {"input_shape": [1, 4, 5, 5], "seed": 9, "layers": [lin(64)] + G + [lin(10)]},
+    # hidden linear layers on the CUDA-core popcount path (K % 128 == 0), affine glue between
+    "fc_popc": {"input_shape": [1, 256, 1, 1], "seed": 13,
+                "layers": [lin(1024)] + G + [lin(512)] + G + [lin(96), lin(7)]},
 }
 
 
