@@ -149,6 +149,7 @@ __device__ __forceinline__ uint4 load_bits(const FusedGeom& g, const int2* qtab,
     if (!rc.valid) return make_uint4(0, 0, 0, 0);
     if ((g.Cw & 3) == 0) {
         const int2 e = qtab[4 * kb];
+        if (e.y < 0) return make_uint4(0, 0, 0, 0);  // a block past K (FP4's 256-position blocks)
         const int iy = rc.y0 + (e.x >> 16), ix = rc.x0 + int(short(e.x & 0xffff));
         const bool inb = unsigned(iy) < unsigned(g.H) && unsigned(ix) < unsigned(g.W);
         const uint32_t* src = act + (size_t((rc.pix + iy) * g.W + ix)) * g.Cw + e.y;
@@ -1706,6 +1707,383 @@ __global__ void weights_to_bits_kernel(const int8_t* __restrict__ w8, int Kpad, 
     wbits[i] = w;
 }
 
+// ---------------------------------------------------------------------------------------------
+// FP4 swapped-operand conv (kind::mxf4, block-scaled e2m1): the same channels x positions tiles
+// as fused_swap_kernel, but each operand element is a 4-bit e2m1 value instead of an int8:
+// activations {0.0, 1.0} (codes 0x0, 0x2), weights {-1.0, +1.0} (0xA, 0x2), every block scale
+// 2^0 (ue8m0 0x7F). Products and sums are exact in the f32 accumulator (|sum| <= K < 2^24),
+// so the accumulator is the same integer u = sum bit * w as the int8 path. Half the operand
+// bytes per K element (the swapped stage is shared-memory-bandwidth bound) and twice the MMA
+// K per instruction (64).
+//
+// Layout: a 128-byte K-major SW128 row holds 256 elements; element e of a row is nibble e % 2
+// (low first) of byte e / 2. An activation word (32 K positions) expands to 16 bytes in
+// put_word4's order (8 ALU ops); the FP4 weights carry the same within-word permutation.
+// TMEM: accumulators 2 x 224 columns (224 positions per tile), then 32 columns of scale
+// factors for A and 32 for B, filled with 0x7F7F7F7F: every layout the MMA reads sees 2^0.
+constexpr int kSw4N = 224;  // positions per tile
+constexpr int kSfCol = 2 * kSw4N;  // 448: SFA columns [448, 480), SFB [480, 512)
+constexpr size_t kSw4Smem = 1024 + size_t(kStages) * (kRows + kSw4N) * kKB + 256 + kMaxQ * 8;
+
+// 32 activation bits -> 32 e2m1 nibbles (16 bytes) at 16-byte chunk `chunk` of row r. Output
+// word s takes bits s, s+4, ..., s+28 (one shift and one mask: nibble value 2 = e2m1 1.0), so
+// element e = 8s + n of a 32-group holds K position 4n + s; the FP4 weights are permuted to
+// match (prep_weights4_kernel).
+__device__ __forceinline__ void put_word4(uint32_t tile, int r, int chunk, uint32_t w) {
+    put_chunk(tile, r, chunk, (w << 1) & 0x22222222u, w & 0x22222222u, (w >> 1) & 0x22222222u,
+              (w >> 2) & 0x22222222u);
+}
+
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
+// Block-scaled instruction descriptor (CUTLASS InstrDescriptorBlockScaled): E2M1 (MXF4
+// format 1) for A and B, K-major, scale format UE8M0, K = 64, scale-factor ids 0.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(M >> 4) << 24);
+}
+
+template <int IN, int PT>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_swap4_kernel(const __grid_constant__ CUtensorMap tmW4, const FusedGeom g) {
+    static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sW = smem_raw + (base - raw);                 // [kStages][128 * 128] weights (A)
+    uint8_t* sX = sW + size_t(kStages) * kRows * kKB;      // [kStages][224 * 128] activations (B)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(kStages) * kSw4N * kKB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int2* ftab = reinterpret_cast<int2*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int units = gridDim.x, unit = blockIdx.x;
+    const int m_tiles = (g.D + kRows - 1) / kRows;
+    const int n_tiles = (g.rows + kSw4N - 1) / kSw4N;
+    const int tiles = m_tiles * n_tiles;
+    const int KB = g.kb4;  // 256-element K blocks
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmW4);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 4 + 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        fence_mbar_init();
+    }
+    if (IN == FIN_BITS) {
+        const int kw_total = (g.K + 31) >> 5;
+        for (int q = threadIdx.x; q < 8 * KB; q += blockDim.x) {
+            int2 e = make_int2(0, -1);
+            if (q < kw_total) {
+                const int tap = q / g.Cw, cw = q - tap * g.Cw, ky = tap / g.KW, kx = tap - ky * g.KW;
+                e = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), cw);
+            }
+            ftab[q] = e;
+        }
+    } else {
+        for (int tap = threadIdx.x; tap < g.KH * g.KW; tap += blockDim.x) {
+            const int ky = tap / g.KW, kx = tap - ky * g.KW;
+            ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
+        }
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp >= 2 && warp < 6) {  // scale factors: every byte of columns [448, 512) = 2^0
+        uint32_t v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0x7F7F7F7Fu;
+        const uint32_t lane_base = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
+        tmem_st32(lane_base + kSfCol, v);
+        tmem_st32(lane_base + kSfCol + 32, v);
+        tmem_st_wait();
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            WaitClock wc;
+            for (int t = unit; t < tiles; t += units) {
+                const int mt = t % m_tiles;
+                for (int kb = 0; kb < KB; ++kb) {
+                    wc.wait(&empty[stage], phase ^ 1, 0);
+                    mbar_arrive_expect_tx(&full[stage], kRows * kKB);
+                    tma_load_2d(&tmW4, &full[stage], sW + size_t(stage) * kRows * kKB, kb * kKB, mt * kRows);
+                    if (++stage == kStages) stage = 0, phase ^= 1;
+                }
+            }
+            wc.flush(g.dbg, 0);
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_mxf4(kRows, kSw4N);
+        int stage = 0;
+        uint32_t phase = 0;
+        int i = 0;
+        WaitClock wc;
+        for (int t = unit; t < tiles; t += units, ++i) {
+            const int acc = i & 1;
+            wc.wait(&tempty[acc], ((i >> 1) & 1) ^ 1, 0);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + uint32_t(acc * kSw4N);
+            for (int kb = 0; kb < KB; ++kb) {
+                wc.wait(&full[stage], phase, 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
+                    const uint32_t b0 = smem_u32(sX + size_t(stage) * kSw4N * kKB);
+                    const int nk = kb == KB - 1 ? g.kq4 : kKB / 32;  // 64-element K steps past K: zeros
+#pragma unroll
+                    for (int k = 0; k < kKB / 32; ++k) {
+                        if (k >= nk) break;
+                        mma_mxf4(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                 tmem_base + kSfCol, tmem_base + kSfCol + 32, (kb != 0 || k != 0));
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == kStages) stage = 0, phase ^= 1;
+            }
+        }
+        if (lane == 0) wc.flush(g.dbg, 1);
+        for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    } else if (warp < 6 || warp >= 10) {
+        WaitClock wc;
+        // epilogue: lane = channel, 7 chunks of 32 positions (warps 2-5: chunks 0-3, 10-13: 4-6)
+        const int q = warp & 3;
+        const int c0 = warp >= 10 ? 4 : 0, c1 = warp >= 10 ? 7 : 4;
+        int i = 0;
+        for (int t = unit; t < tiles; t += units, ++i) {
+            const int acc = i & 1;
+            const int mt = t % m_tiles, nt = t / m_tiles;
+            const int c = mt * kRows + q * 32 + lane;
+            const bool wvalid = mt * kRows + q * 32 < g.D;
+            const int4 pc = wvalid ? __ldg(g.prm + c) : make_int4(0x7fffffff, 0, 0, 0);
+            const float Tf = float(pc.x);  // exact: |Tu| <= K < 2^24
+            const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
+            const int oword = mt * (kRows / 32) + q;
+            wc.wait(&tfull[acc], (i >> 1) & 1, 0);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kSw4N);
+            uint32_t va[32];
+            for (int cc = c0; cc < c1; ++cc) {
+                tmem_ld32(tbase + uint32_t(cc * 32), va);
+                tmem_ld_wait();
+                if (cc == c1 - 1) {  // accumulator free before the last words
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                }
+                uint32_t mine = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t w = __ballot_sync(0xffffffffu, __uint_as_float(va[j]) >= Tf) ^ flipw;
+                    if (lane == j) mine = w;
+                }
+                const int pos = nt * kSw4N + cc * 32 + lane;
+                if (g.pool) {
+                    mine |= __shfl_xor_sync(0xffffffffu, mine, 1);
+                    mine |= __shfl_xor_sync(0xffffffffu, mine, 2);
+                    if (wvalid && (lane & 3) == 0 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
+                } else if (wvalid && pos < g.rows) {
+                    g.out_bits[size_t(pos) * g.Dw + oword] = mine;
+                }
+            }
+        }
+        if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
+    } else {
+        // producers: thread pt owns tile rows pt and pt + 128 (< 224); blocks are loaded kPF
+        // ahead (the same ring as fused_swap_kernel's producers)
+        const int pt = threadIdx.x - 6 * 32;
+        const bool two = pt + 128 < kSw4N;
+        constexpr int NT = PT ? PT : kMaxPixTaps;
+        struct Bits8 {
+            uint4 lo, hi;
+        };
+        using Raw = typename std::conditional<IN == FIN_BITS, Bits8, PixRaw<NT>>::type;
+        // kPF blocks loaded ahead. (Rotating the slots in place, the loop unrolled kPF times,
+        // measured slower here: 1.38 M vs 1.14 M cycles per CTA for conv 128->128 at B=4096.)
+        constexpr int kPF = 2;
+        int stage = 0;
+        uint32_t phase = 0;
+        const bool one_step = KB == 1 && g.kq4 == 1 && IN == FIN_PIX;  // <= 64 K positions: 32 bytes per row
+        WaitClock wc;
+        int t_ld = unit, kb_ld = 0;
+        RowCtx rc[2];
+        auto set_rows = [&]() {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                int b = 0, oy = 0, ox = 0;
+                rc[h].valid = t_ld < tiles && (h == 0 || two) &&
+                              decode_row(g, (t_ld / m_tiles) * kSw4N + pt + 128 * h, b, oy, ox);
+                rc[h].pix = b * g.H, rc[h].y0 = oy * g.SH, rc[h].x0 = ox * g.SW;
+            }
+        };
+        set_rows();
+        Raw pf[kPF][2];
+        bool pv[kPF][2];
+        auto next_load = [&](Raw (&dst)[2], bool (&v)[2]) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                v[h] = rc[h].valid;
+                if constexpr (IN == FIN_BITS) {
+                    dst[h].lo = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld) : make_uint4(0, 0, 0, 0);
+                    dst[h].hi = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld + 1) : make_uint4(0, 0, 0, 0);
+                } else {
+                    dst[h] = load_pix<false, NT>(g, ftab, rc[h]);
+                }
+            }
+            if (t_ld < tiles && ++kb_ld == KB) {
+                t_ld += units;
+                kb_ld = 0;
+                set_rows();
+            }
+        };
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
+        for (int t = unit; t < tiles; t += units) {
+            for (int kb = 0; kb < KB; ++kb) {
+                uint4 lo[2], hi[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if constexpr (IN == FIN_BITS) {
+                        lo[h] = pf[0][h].lo, hi[h] = pf[0][h].hi;
+                    } else {
+                        lo[h] = gather_pix(g, pf[0][h], pv[0][h]);
+                        hi[h] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < kPF - 1; ++i)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) pf[i][h] = pf[i + 1][h], pv[i][h] = pv[i + 1][h];
+                next_load(pf[kPF - 1], pv[kPF - 1]);
+                wc.wait(&empty[stage], phase ^ 1, 0);
+                const uint32_t tile = smem_u32(sX + size_t(stage) * kSw4N * kKB);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && !two) break;
+                    if (g.dbg_mode & 1) break;  // profiling: no stores (results invalid)
+                    const int r = pt + 128 * h;
+                    put_word4(tile, r, 0, lo[h].x);
+                    put_word4(tile, r, 1, lo[h].y);
+                    if (one_step) continue;  // the MMA reads the first 32 bytes only
+                    put_word4(tile, r, 2, lo[h].z);
+                    put_word4(tile, r, 3, lo[h].w);
+                    put_word4(tile, r, 4, hi[h].x);
+                    put_word4(tile, r, 5, hi[h].y);
+                    put_word4(tile, r, 6, hi[h].z);
+                    put_word4(tile, r, 7, hi[h].w);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[stage]);
+                if (++stage == kStages) stage = 0, phase ^= 1;
+            }
+        }
+        if (pt == 0) wc.flush(g.dbg, 3);
+    }
+
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+}
+
+template <int IN, int PT>
+int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
+    auto kern = fused_swap4_kernel<IN, PT>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSw4Smem)));
+        attr_set = true;
+    }
+    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows)) * ceil_div(size_t(g.rows), size_t(kSw4N)));
+    const int grid = std::min(tiles, num_sms());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSw4Smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
+    FusedGeom gd = g;
+    unsigned long long* dbg = nullptr;
+    if (prof) {
+        BNN_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+        BNN_CUDA(cudaMemset(dbg, 0, 16 * sizeof(unsigned long long)));
+        gd.dbg = dbg;
+        gd.dbg_mode = prof >> 1;
+    }
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
+    BNN_TRY(launch_check("fused_swap4_kernel"));
+    if (prof) {
+        unsigned long long h[16];
+        BNN_CUDA(cudaMemcpy(h, dbg, sizeof h, cudaMemcpyDeviceToHost));
+        cudaFree(dbg);
+        const double n = double(grid);
+        fprintf(stderr,
+                "[swap4 in=%d rows=%d D=%d KB4=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | mma wait-acc %.1f "
+                "wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
+                IN, g.rows, g.D, g.kb4, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
+                h[8] / n / 1e3, h[12] / n / 1e3);
+    }
+    return BNN_OK;
+}
+
+// Build-time FP4 weights: the int8 +-1 rows (engine K order, int8 within-word permutation:
+// position b of a 32-group at byte 4 (b % 8) + b / 8) -> e2m1 nibbles in put_word4's order
+// (element e of a 32-group holds position 4 (e % 8) + e / 8), [Dpad, Kpad4 / 2] bytes;
+// positions >= K are 0.0.
+__global__ void prep_weights4_kernel(const int8_t* __restrict__ w8, int Kpad, int K, int Dpad, int Kpad4,
+                                     uint8_t* __restrict__ w4) {
+    const size_t total = size_t(Dpad) * (Kpad4 / 2);
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const int d = int(i / (Kpad4 / 2)), e0 = int(i % (Kpad4 / 2)) * 2;
+        uint8_t v = 0;
+        for (int h = 0; h < 2; ++h) {
+            const int e = e0 + h, q = e >> 5, el = e & 31;
+            const int bb = 4 * (el % 8) + el / 8, k = 32 * q + bb;  // the K position element e holds
+            if (k >= K) continue;
+            const int8_t s = w8[size_t(d) * Kpad + 32 * q + 4 * (bb % 8) + bb / 8];
+            const uint8_t code = s > 0 ? 0x2 : s < 0 ? 0xA : 0x0;
+            v |= uint8_t(code << (4 * h));
+        }
+        w4[i] = v;
+    }
+}
+
 // Build-time weight preparation: reference packed rows (pack_rows(sign(flatten(W))),
 // K order r) -> int8 +-1 rows [Dpad, Kpad] in the engine's K order. With T > 1 the engine
 // order is tap-major (k' = tap*C + c) and the reference order is channel-major
@@ -1969,6 +2347,24 @@ int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s
     logits_popc_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(static_cast<const uint32_t*>(g.in), g.Cw, g.K, wbits,
                                                                  g.prm, g.D, g.rows, g.out_f32, g.ldo);
     return launch_check("logits_popc_kernel");
+}
+
+int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_t* w4, cudaStream_t s) {
+    const size_t total = size_t(Dpad) * (Kpad4 / 2);
+    const unsigned grid = unsigned(std::min<size_t>(ceil_div(total, 256), size_t(num_sms()) * 16));
+    prep_weights4_kernel<<<grid, 256, 0, s>>>(w8, Kpad, K, Dpad, Kpad4, w4);
+    return launch_check("prep_weights4_kernel");
+}
+
+int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaStream_t s) {
+    if (g.rows <= 0) return BNN_OK;
+    set_last_gemm("fused_swap_mxf4");
+    if (in_mode == FIN_PIX) {
+        if (g.KH * g.KW == 9) return launch_swap4_t<FIN_PIX, 9>(tm4, g, s);
+        return launch_swap4_t<FIN_PIX, 0>(tm4, g, s);
+    }
+    if (in_mode == FIN_BITS) return launch_swap4_t<FIN_BITS, 0>(tm4, g, s);
+    return fail(BNN_E_CONFIG, "FP4 swapped fused layer: packed-bit or pixel input only");
 }
 
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {

@@ -57,6 +57,7 @@ struct FusedGeom {
     int pdl_late;             // trigger dependent launch at the end of the CTA (else at entry)
     int kq_last;              // 32-byte K steps that carry data in the last K block (1..4)
     FastDiv dv0, dv1;         // decode_row divisors: pool (OW/2, OH/2) or (OH*OW, OW)
+    int kb4, kq4;             // FP4 path: 256-element K blocks, 64-element K steps in the last
 };
 
 // Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.
@@ -80,6 +81,10 @@ int launch_chain(const ChainParams& p, cudaStream_t s);
 // Swapped-operand conv (fused_swap_kernel): 128 channels x 256 positions per tile, bits
 // epilogue, CTA-local; tm must be the weight map with box rows 128.
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
+// FP4 (kind::mxf4) swapped-operand conv; tm4 maps the e2m1 weights [Dpad, Kpad4/2] bytes, box
+// rows 128 x 128 bytes.
+int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_t* w4, cudaStream_t s);
+int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaStream_t s);
 // Tiny final logits layer on the CUDA cores (logits_popc_kernel); wbits from prep_logit_bits.
 int prep_logit_bits(const int8_t* w8, int Kpad, int K, int D, int Kw, uint32_t* wbits, cudaStream_t s);
 int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s);

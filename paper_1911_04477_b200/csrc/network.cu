@@ -41,6 +41,7 @@ int launch_transpose(const float*, size_t, size_t, float*, cudaStream_t);
 int launch_fill_random(uint64_t, uint64_t, size_t, float*, cudaStream_t);
 int launch_affine_scale(float*, size_t, cudaStream_t);
 int launch_unary(int, const float*, size_t, float*, cudaStream_t);
+int make_tmap_2d_s8(CUtensorMap* map, const void* base, size_t rows, size_t K, size_t ld, uint32_t box_rows);
 int launch_float_gemm(const float*, const float*, size_t, size_t, size_t, const float*, size_t, float*, cudaStream_t);
 int launch_im2col_f32(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*, float*, cudaStream_t);
 
@@ -95,7 +96,10 @@ struct FusedStage {
     bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
     bool small_logits = false;   // tiny final layer: CUDA-core popcount kernel (wbits)
     const char* kname = "";      // kernel the last forward ran for this stage
-    DevBuf w8, prm, wbits;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
+    DevBuf w8, prm, wbits;
+    DevBuf w4;                   // FP4 (e2m1) weights [Dpad, Kpad4 / 2] for the mxf4 swapped kernel
+    CUtensorMap tm4;             // its weight map (box 128 rows x 128 bytes)
+    bool fp4_ok = false;              // int8 +-1 weights [Dpad, Kpad] (engine K order), float4 params
     CUtensorMap tm[5];           // weight tile maps, box rows 16, 32, 64, 128, 256 (= BN / cta_group)
     size_t out_words_per_image = 0;
 };
@@ -369,6 +373,15 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         const int bns[5] = {16, 32, 64, 128, 256};
         for (int b = 0; b < 5; ++b)
             BNN_TRY(fused_make_tmap(&st->tm[b], st->w8.as<int8_t>(), st->Dpad, st->Kpad, bns[b]));
+        if (kind == BNN_LAYER_CONV && st->epi == FEPI_BITS && st->in_mode != FIN_F32) {  // FP4 operands
+            const int Kpad4 = int(round_up(size_t(g.K), 256));
+            g.kb4 = Kpad4 / 256;
+            g.kq4 = (g.K - 256 * (g.kb4 - 1) + 63) / 64;
+            BNN_TRY(st->w4.alloc(size_t(st->Dpad) * (Kpad4 / 2)));
+            BNN_TRY(prep_weights4(st->w8.as<int8_t>(), st->Kpad, g.K, st->Dpad, Kpad4, st->w4.as<uint8_t>(), s));
+            BNN_TRY(make_tmap_2d_s8(&st->tm4, st->w4.p, size_t(st->Dpad), size_t(Kpad4 / 2), size_t(Kpad4 / 2), 128));
+            st->fp4_ok = true;
+        }
         if (st->epi == FEPI_LOGITS && kind == BNN_LAYER_LINEAR && g.D <= 64) {
             st->small_logits = true;
             BNN_TRY(st->wbits.alloc(size_t(g.D) * g.Cw * sizeof(uint32_t)));
@@ -654,6 +667,18 @@ bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
            (g_swap == 2 || st.g.D <= 128);
 }
 
+// FP4 operands (fused_swap4_kernel, kind::mxf4): BNN_FUSED_FP4 / bnn_set_fused_fp4: 0 off,
+// 1 (default) the swapped layers with a packed-bit input (conv 128->128: 1.26 -> 1.14 M cycles
+// per CTA at B=4096, profiles/r01_fp4_roles.log), 2 every conv layer with a packed-bit output
+// (measured slower for the pixel-input first layer and the wider layers).
+int g_fp4 = -1;
+
+bool use_fp4(const bnn_net* net, const FusedStage& st, int cg) {
+    if (g_fp4 < 0) g_fp4 = getenv("BNN_FUSED_FP4") ? atoi(getenv("BNN_FUSED_FP4")) : 1;
+    if (!st.fp4_ok || g_fp4 == 0 || g_forced_cg > 0 || g_forced_bn > 0 || cg != 1) return false;
+    return g_fp4 == 2 || (use_swap(net, st, cg) && st.in_mode == FIN_BITS);
+}
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -753,6 +778,8 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         EventPair gemm_ev(net, st.layer, 1, s);
         if (st.small_logits && g_small_logits)
             BNN_TRY(launch_logits_popc(g, st.wbits.as<uint32_t>(), s));
+        else if (use_fp4(net, st, plans[i].cg))
+            BNN_TRY(launch_swap4(st.in_mode, st.tm4, g, s));
         else if (use_swap(net, st, plans[i].cg))
             BNN_TRY(launch_swap(st.in_mode, st.tm[box_index(128)], g, s));
         else
@@ -980,6 +1007,13 @@ const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer) {
 
 int bnn_set_fused_small_logits(int enabled) {
     g_small_logits = enabled ? 1 : 0;
+    ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_set_fused_fp4(int mode) {
+    if (mode < 0 || mode > 2) return fail(BNN_E_CONFIG, "fused fp4: 0 (off), 1 (swapped layers) or 2 (all convs)");
+    g_fp4 = mode;
     ++g_tiling_epoch;
     return BNN_OK;
 }
