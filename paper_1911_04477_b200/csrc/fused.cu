@@ -1721,9 +1721,19 @@ __global__ void weights_to_bits_kernel(const int8_t* __restrict__ w8, int Kpad, 
 // put_word4's order (8 ALU ops); the FP4 weights carry the same within-word permutation.
 // TMEM: accumulators 2 x 224 columns (224 positions per tile), then 32 columns of scale
 // factors for A and 32 for B, filled with 0x7F7F7F7F: every layout the MMA reads sees 2^0.
-constexpr int kSw4N = 224;  // positions per tile
-constexpr int kSfCol = 2 * kSw4N;  // 448: SFA columns [448, 480), SFB [480, 512)
-constexpr size_t kSw4Smem = 1024 + size_t(kStages) * (kRows + kSw4N) * kKB + 256 + kMaxQ * 8;
+// NP positions per tile: 224 (4 producer warps, 2 rows per thread, 14 warps), 192 (6 producer
+// warps, 1 row per thread, 16 warps) or 240 (8 producer warps, 1 row per thread, 4 epilogue
+// warps, 14 warps; the scale factors take the last 32 TMEM columns). The producers bound this
+// kernel, and an MMA costs about the same for any N here, so wide tiles fed by more producer
+// warps win.
+template <int NP>
+constexpr size_t sw4_smem() {
+    return 1024 + size_t(kStages) * (kRows + NP) * kKB + 256 + kMaxQ * 8;
+}
+template <int NP>
+constexpr int sw4_threads() {
+    return NP == 192 ? 512 : kThreads;
+}
 
 // 32 activation bits -> 32 e2m1 nibbles (16 bytes) at 16-byte chunk `chunk` of row r. Output
 // word s takes bits s, s+4, ..., s+28 (one shift and one mask: nibble value 2 = e2m1 1.0), so
@@ -1750,10 +1760,15 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
     return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(M >> 4) << 24);
 }
 
-template <int IN, int PT>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int IN, int PT, int NP>
+__global__ void __launch_bounds__(sw4_threads<NP>(), 1)
     fused_swap4_kernel(const __grid_constant__ CUtensorMap tmW4, const FusedGeom g) {
     static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
+    static_assert(NP == 192 || NP == 224 || NP == 240, "tile positions");
+    constexpr int kSw4N = NP;
+    constexpr int kSfCol = NP == 240 ? 480 : 2 * kSw4N;  // SFA, then SFB: 16 columns each at NP 240
+    constexpr int kProd = NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
+    constexpr int kEpi = NP == 240 ? 4 : 8;                   // epilogue warps
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -1778,12 +1793,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW4);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 4 + 1);
+            mbar_init(&full[s], kProd + 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);
+            mbar_init(&tempty[a], kEpi);
         }
         fence_mbar_init();
     }
@@ -1815,7 +1830,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 32; ++j) v[j] = 0x7F7F7F7Fu;
         const uint32_t lane_base = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
         tmem_st32(lane_base + kSfCol, v);
-        tmem_st32(lane_base + kSfCol + 32, v);
+        if (NP != 240) tmem_st32(lane_base + kSfCol + 32, v);
         tmem_st_wait();
     }
     __syncwarp();
@@ -1862,7 +1877,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < kKB / 32; ++k) {
                         if (k >= nk) break;
                         mma_mxf4(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                 tmem_base + kSfCol, tmem_base + kSfCol + 32, (kb != 0 || k != 0));
+                                 tmem_base + kSfCol, tmem_base + kSfCol + (NP == 240 ? 16 : 32), (kb != 0 || k != 0));
                     }
                     mma_commit(&empty[stage]);
                     if (kb == KB - 1) mma_commit(&tfull[acc]);
@@ -1875,11 +1890,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
-    } else if (warp < 6 || warp >= 10) {
+    } else if (warp < 6 || (kEpi == 8 && warp >= 10 && warp < 14)) {
         WaitClock wc;
-        // epilogue: lane = channel, 7 chunks of 32 positions (warps 2-5: chunks 0-3, 10-13: 4-6)
+        // epilogue: lane = channel, ceil(NP/32) chunks of 32 positions (split over warps 2-5 /
+        // 10-13 when there are 8 epilogue warps)
         const int q = warp & 3;
-        const int c0 = warp >= 10 ? 4 : 0, c1 = warp >= 10 ? 7 : 4;
+        constexpr int NC = (kSw4N + 31) / 32, NH = kEpi == 8 ? (NC + 1) / 2 : NC;
+        const int c0 = warp >= 10 ? NH : 0, c1 = warp >= 10 ? NC : NH;
         int i = 0;
         for (int t = unit; t < tiles; t += units, ++i) {
             const int acc = i & 1;
@@ -1908,7 +1925,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t w = __ballot_sync(0xffffffffu, __uint_as_float(va[j]) >= Tf) ^ flipw;
                     if (lane == j) mine = w;
                 }
-                const int pos = nt * kSw4N + cc * 32 + lane;
+                const int pos = (cc * 32 + lane < kSw4N) ? nt * kSw4N + cc * 32 + lane : g.rows;  // past the tile: none
                 if (g.pool) {
                     mine |= __shfl_xor_sync(0xffffffffu, mine, 1);
                     mine |= __shfl_xor_sync(0xffffffffu, mine, 2);
@@ -1920,10 +1937,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (warp == 2 && lane == 0) wc.flush(g.dbg, 2);
     } else {
-        // producers: thread pt owns tile rows pt and pt + 128 (< 224); blocks are loaded kPF
-        // ahead (the same ring as fused_swap_kernel's producers)
-        const int pt = threadIdx.x - 6 * 32;
-        const bool two = pt + 128 < kSw4N;
+        // producers: thread pt owns tile row pt (NP = 192: warps 6-9, 14-15) or rows pt and
+        // pt + 128 (NP = 224: warps 6-9); blocks are loaded kPF ahead
+        const int pt = NP == 240 ? (warp - 6) * 32 + lane : (warp < 10 ? warp - 6 : warp - 10) * 32 + lane;
+        const bool one = pt < kSw4N;  // NP = 240: the last warp has 16 rows
+        const bool two = NP == 224 && pt + 128 < kSw4N;
         constexpr int NT = PT ? PT : kMaxPixTaps;
         struct Bits8 {
             uint4 lo, hi;
@@ -1942,7 +1960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 int b = 0, oy = 0, ox = 0;
-                rc[h].valid = t_ld < tiles && (h == 0 || two) &&
+                rc[h].valid = t_ld < tiles && (h == 0 ? one : two) &&
                               decode_row(g, (t_ld / m_tiles) * kSw4N + pt + 128 * h, b, oy, ox);
                 rc[h].pix = b * g.H, rc[h].y0 = oy * g.SH, rc[h].x0 = ox * g.SW;
             }
@@ -1990,7 +2008,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t tile = smem_u32(sX + size_t(stage) * kSw4N * kKB);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && !two) break;
+                    if ((h == 1 && !two) || (h == 0 && !one)) break;  // no such tile row
                     if (g.dbg_mode & 1) break;  // profiling: no stores (results invalid)
                     const int r = pt + 128 * h;
                     put_word4(tile, r, 0, lo[h].x);
@@ -2017,20 +2035,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
 }
 
-template <int IN, int PT>
+template <int IN, int PT, int NP>
 int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_swap4_kernel<IN, PT>;
+    auto kern = fused_swap4_kernel<IN, PT, NP>;
     static bool attr_set = false;
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSw4Smem)));
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw4_smem<NP>())));
         attr_set = true;
     }
-    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows)) * ceil_div(size_t(g.rows), size_t(kSw4N)));
+    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows)) * ceil_div(size_t(g.rows), size_t(NP)));
     const int grid = std::min(tiles, num_sms());
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSw4Smem;
+    cfg.blockDim = dim3(unsigned(sw4_threads<NP>()));
+    cfg.dynamicSmemBytes = sw4_smem<NP>();
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -2359,11 +2377,18 @@ int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_
 int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
     set_last_gemm("fused_swap_mxf4");
+    // tile positions (BNN_FP4_NP): 192 measured fastest (conv 128->128 at B=4096, cycles per CTA:
+    // 192 -> 0.94 M, 224 -> 1.14 M, 240 -> 1.18 M: epilogue-bound with 4 epilogue warps)
+    static const int np = getenv("BNN_FP4_NP") ? atoi(getenv("BNN_FP4_NP")) : 192;
     if (in_mode == FIN_PIX) {
-        if (g.KH * g.KW == 9) return launch_swap4_t<FIN_PIX, 9>(tm4, g, s);
-        return launch_swap4_t<FIN_PIX, 0>(tm4, g, s);
+        if (g.KH * g.KW == 9) return launch_swap4_t<FIN_PIX, 9, 224>(tm4, g, s);
+        return launch_swap4_t<FIN_PIX, 0, 224>(tm4, g, s);
     }
-    if (in_mode == FIN_BITS) return launch_swap4_t<FIN_BITS, 0>(tm4, g, s);
+    if (in_mode == FIN_BITS) {
+        if (np == 224) return launch_swap4_t<FIN_BITS, 0, 224>(tm4, g, s);
+        if (np == 192) return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
+        return launch_swap4_t<FIN_BITS, 0, 240>(tm4, g, s);
+    }
     return fail(BNN_E_CONFIG, "FP4 swapped fused layer: packed-bit or pixel input only");
 }
 
