@@ -255,8 +255,8 @@ int bnn_spec_info(const char* path, uint64_t input_shape[4], size_t* n_layers);
 /* Kernel the last fused forward ran for weighted layer `layer` ("" if none / not fused). */
 const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer);
 /* Fused engine: FP4 operands (kind::mxf4 block-scaled e2m1, exact for +-1 x {0,1}) in the
- * swapped-operand conv kernel: 0 off, 1 (default) swapped layers with a packed-bit input,
- * 2 all convs. Bit-exact in every mode. */
+ * swapped-operand conv kernel: 0 off, 1 (default) every conv with a packed-bit input, 2 also
+ * the pixel-input first conv. Bit-exact in every mode. */
 int bnn_set_fused_fp4(int mode);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */

@@ -668,15 +668,16 @@ bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
 }
 
 // FP4 operands (fused_swap4_kernel, kind::mxf4): BNN_FUSED_FP4 / bnn_set_fused_fp4: 0 off,
-// 1 (default) the swapped layers with a packed-bit input (conv 128->128: 1.26 -> 1.14 M cycles
-// per CTA at B=4096, profiles/r01_fp4_roles.log), 2 every conv layer with a packed-bit output
-// (measured slower for the pixel-input first layer and the wider layers).
+// 1 (default) every conv layer with a packed-bit input and output (conv 128->128: 1.26 -> 0.94 M
+// cycles per CTA at B=4096; the wider layers about even with the position-major int8 kernel at
+// large batch and faster at 256, profiles/r01_fp4_*), 2 also the pixel-input first layer
+// (measured slower there: its one K step leaves the epilogue the bound).
 int g_fp4 = -1;
 
 bool use_fp4(const bnn_net* net, const FusedStage& st, int cg) {
     if (g_fp4 < 0) g_fp4 = getenv("BNN_FUSED_FP4") ? atoi(getenv("BNN_FUSED_FP4")) : 1;
     if (!st.fp4_ok || g_fp4 == 0 || g_forced_cg > 0 || g_forced_bn > 0 || cg != 1) return false;
-    return g_fp4 == 2 || (use_swap(net, st, cg) && st.in_mode == FIN_BITS);
+    return g_fp4 == 2 || st.in_mode == FIN_BITS;
 }
 
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
