@@ -629,7 +629,7 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "binary (+-1 bits; int8 tensor-core MMA, int32 accumulate), f32 logits",
+            "dtype": "binary (+-1 bits; exact FP4 e2m1 / int8 tensor-core MMA, integer-valued accumulate), f32 logits",
             "data": "synthetic: reference fill_random input stream (seed 1), seed-derived weights",
             "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
                        "parallelism": f"dp{world}: batch shards, replicated packed weights, NCCL logits gather",
@@ -674,7 +674,7 @@ def run_reference(args):
     ref = RefLib()
     net = ref.net_default(args.seed)
     cores = os.cpu_count() or 1
-    per_step = cores  # bounded sample per step: one image per host thread
+    per_step = 4 * cores  # bounded sample per step: four images per host thread (~50 ms)
     x = ref.fill_random((per_step, 3, 32, 32), ref.mix64(args.seed, INPUT_STREAM))
     for _ in range(args.warmup):
         net.forward(x, batch_threads=cores)
