@@ -1726,9 +1726,16 @@ __global__ void weights_to_bits_kernel(const int8_t* __restrict__ w8, int Kpad, 
 // warps, 14 warps; the scale factors take the last 32 TMEM columns). The producers bound this
 // kernel, and an MMA costs about the same for any N here, so wide tiles fed by more producer
 // warps win.
-template <int NP>
+// CG = 2 (layers with >= 256 channels, packed-bit input, NP = 192): a CTA pair (cluster of 2)
+// computes 256 channels x 192 positions with cta_group::2 M=256 instructions issued by the
+// even CTA. Each CTA TMA-loads its own 128 weight rows and expands only its half of the
+// positions (96 rows, two threads per row: one per 128-position half of the K block), so the
+// activation expansion that bounds the CG = 1 kernel is done once per 256 channels instead of
+// once per 128, with half the rows per thread. Each CTA holds its 128 channels x 192 positions
+// of the accumulator in its own TMEM and runs the same epilogue.
+template <int NP, int CG = 1>
 constexpr size_t sw4_smem() {
-    return 1024 + size_t(kStages) * (kRows + NP) * kKB + 256 + kMaxQ * 8;
+    return 1024 + size_t(CG == 2 ? kStages2 : kStages) * (kRows + NP / CG) * kKB + 256 + kMaxQ * 8;
 }
 template <int NP>
 constexpr int sw4_threads() {
@@ -1744,14 +1751,26 @@ __device__ __forceinline__ void put_word4(uint32_t tile, int r, int chunk, uint3
               (w >> 2) & 0x22222222u);
 }
 
+template <int CG = 1>
 __device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
-        : "memory");
+    if constexpr (CG == 2) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+                d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+                d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+            : "memory");
+    }
 }
 
 // Block-scaled instruction descriptor (CUTLASS InstrDescriptorBlockScaled): E2M1 (MXF4
@@ -1760,45 +1779,51 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
     return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(M >> 4) << 24);
 }
 
-template <int IN, int PT, int NP>
+template <int IN, int PT, int NP, int CG = 1>
 __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
     fused_swap4_kernel(const __grid_constant__ CUtensorMap tmW4, const FusedGeom g) {
     static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
     static_assert(NP == 192 || NP == 224 || NP == 240, "tile positions");
+    static_assert(CG == 1 || (CG == 2 && IN == FIN_BITS && NP == 192), "CTA pairs: packed bits, 192 positions");
     constexpr int kSw4N = NP;
+    constexpr int kBH = NP / CG;  // activation rows this CTA expands per stage
+    constexpr int kS = CG == 2 ? kStages2 : kStages;
     constexpr int kSfCol = NP == 240 ? 480 : 2 * kSw4N;  // SFA, then SFB: 16 columns each at NP 240
     constexpr int kProd = NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
     constexpr int kEpi = NP == 240 ? 4 : 8;                   // epilogue warps
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t* sW = smem_raw + (base - raw);                 // [kStages][128 * 128] weights (A)
-    uint8_t* sX = sW + size_t(kStages) * kRows * kKB;      // [kStages][224 * 128] activations (B)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(kStages) * kSw4N * kKB);
+    uint8_t* sW = smem_raw + (base - raw);           // [kS][128 * 128] weights (A)
+    uint8_t* sX = sW + size_t(kS) * kRows * kKB;     // [kS][kBH * 128] activations (B)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + size_t(kS) * kBH * kKB);
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* empty = bars + kS;
+    uint64_t* tfull = bars + 2 * kS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int2* ftab = reinterpret_cast<int2*>(bars + 32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
-    const int units = gridDim.x, unit = blockIdx.x;
-    const int m_tiles = (g.D + kRows - 1) / kRows;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const int units = gridDim.x / CG, unit = blockIdx.x / CG;
+    const int m_tiles = (g.D + kRows * CG - 1) / (kRows * CG);
     const int n_tiles = (g.rows + kSw4N - 1) / kSw4N;
     const int tiles = m_tiles * n_tiles;
     const int KB = g.kb4;  // 256-element K blocks
+    // barrier the producers / TMA / epilogue signal: the even CTA's (shared::cluster address)
+    auto leader = [&](uint64_t* bar) { return CG == 2 ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW4);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], kProd + 1);
+        for (int s = 0; s < kS; ++s) {
+            mbar_init(&full[s], CG * (kProd + 1));
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpi);
+            mbar_init(&tempty[a], CG * kEpi);
         }
         fence_mbar_init();
     }
@@ -1818,7 +1843,12 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
             ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
         }
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) {
+        if (CG == 2)
+            tmem_alloc_cg2<512>(tmem_slot);
+        else
+            tmem_alloc<512>(tmem_slot);
+    }
     __syncwarp();
     tc_fence_before();
     __syncthreads();
@@ -1836,6 +1866,9 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    // CG = 2: the peer's barriers are initialised and its scale factors written before any
+    // remote arrive or pair MMA
+    if (CG == 2) cluster_sync();
     tc_fence_after();
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -1848,20 +1881,27 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                 const int mt = t % m_tiles;
                 for (int kb = 0; kb < KB; ++kb) {
                     wc.wait(&empty[stage], phase ^ 1, 0);
-                    mbar_arrive_expect_tx(&full[stage], kRows * kKB);
-                    tma_load_2d(&tmW4, &full[stage], sW + size_t(stage) * kRows * kKB, kb * kKB, mt * kRows);
-                    if (++stage == kStages) stage = 0, phase ^= 1;
+                    uint8_t* dst = sW + size_t(stage) * kRows * kKB;
+                    if (CG == 2) {
+                        const uint32_t fb = leader(&full[stage]);
+                        mbar_arrive_expect_tx_cluster(fb, kRows * kKB);
+                        tma_load_2d_cg2(&tmW4, fb, dst, kb * kKB, (mt * CG + int(rank)) * kRows);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], kRows * kKB);
+                        tma_load_2d(&tmW4, &full[stage], dst, kb * kKB, mt * kRows);
+                    }
+                    if (++stage == kS) stage = 0, phase ^= 1;
                 }
             }
             wc.flush(g.dbg, 0);
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc = idesc_mxf4(kRows, kSw4N);
+        constexpr uint32_t idesc = idesc_mxf4(kRows * CG, kSw4N);
         int stage = 0;
         uint32_t phase = 0;
         int i = 0;
         WaitClock wc;
-        for (int t = unit; t < tiles; t += units, ++i) {
+        for (int t = unit; t < tiles && (CG == 1 || rank == 0); t += units, ++i) {
             const int acc = i & 1;
             wc.wait(&tempty[acc], ((i >> 1) & 1) ^ 1, 0);
             tc_fence_after();
@@ -1871,25 +1911,33 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
-                    const uint32_t b0 = smem_u32(sX + size_t(stage) * kSw4N * kKB);
+                    const uint32_t b0 = smem_u32(sX + size_t(stage) * kBH * kKB);
                     const int nk = kb == KB - 1 ? g.kq4 : kKB / 32;  // 64-element K steps past K: zeros
 #pragma unroll
                     for (int k = 0; k < kKB / 32; ++k) {
                         if (k >= nk) break;
-                        mma_mxf4(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                 tmem_base + kSfCol, tmem_base + kSfCol + (NP == 240 ? 16 : 32), (kb != 0 || k != 0));
+                        mma_mxf4<CG>(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                     tmem_base + kSfCol, tmem_base + kSfCol + (NP == 240 ? 16 : 32),
+                                     (kb != 0 || k != 0));
                     }
-                    mma_commit(&empty[stage]);
-                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                    if (CG == 2) {
+                        mma_commit_cg2_mc(&empty[stage], 3);  // both CTAs' slots free
+                        if (kb == KB - 1) mma_commit_cg2_mc(&tfull[acc], 3);
+                    } else {
+                        mma_commit(&empty[stage]);
+                        if (kb == KB - 1) mma_commit(&tfull[acc]);
+                    }
                 }
                 __syncwarp();
-                if (++stage == kStages) stage = 0, phase ^= 1;
+                if (++stage == kS) stage = 0, phase ^= 1;
             }
         }
         if (lane == 0) wc.flush(g.dbg, 1);
-        for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if (CG == 1) {
+            for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
+            tc_fence_after();
+            tmem_dealloc<512>(tmem_base);
+        }  // CG = 2: both CTAs deallocate after the final cluster barrier
     } else if (warp < 6 || (kEpi == 8 && warp >= 10 && warp < 14)) {
         WaitClock wc;
         // epilogue: lane = channel, ceil(NP/32) chunks of 32 positions (split over warps 2-5 /
@@ -1901,12 +1949,13 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
         for (int t = unit; t < tiles; t += units, ++i) {
             const int acc = i & 1;
             const int mt = t % m_tiles, nt = t / m_tiles;
-            const int c = mt * kRows + q * 32 + lane;
-            const bool wvalid = mt * kRows + q * 32 < g.D;
+            const int m0 = (mt * CG + int(rank)) * kRows;  // this CTA's first channel
+            const int c = m0 + q * 32 + lane;
+            const bool wvalid = m0 + q * 32 < g.D;
             const int4 pc = wvalid ? __ldg(g.prm + c) : make_int4(0x7fffffff, 0, 0, 0);
             const float Tf = float(pc.x);  // exact: |Tu| <= K < 2^24
             const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
-            const int oword = mt * (kRows / 32) + q;
+            const int oword = m0 / 32 + q;
             wc.wait(&tfull[acc], (i >> 1) & 1, 0);
             tc_fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kSw4N);
@@ -1917,7 +1966,12 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                 if (cc == c1 - 1) {  // accumulator free before the last words
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    if (lane == 0) {
+                        if (CG == 2)
+                            mbar_arrive_cluster(leader(&tempty[acc]));
+                        else
+                            mbar_arrive(&tempty[acc]);
+                    }
                 }
                 uint32_t mine = 0;
 #pragma unroll
@@ -1940,7 +1994,10 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
         // producers: thread pt owns tile row pt (NP = 192: warps 6-9, 14-15) or rows pt and
         // pt + 128 (NP = 224: warps 6-9); blocks are loaded kPF ahead
         const int pt = NP == 240 ? (warp - 6) * 32 + lane : (warp < 10 ? warp - 6 : warp - 10) * 32 + lane;
-        const bool one = pt < kSw4N;  // NP = 240: the last warp has 16 rows
+        // CG = 2: thread pt expands row pt % 96 of this CTA's half, K words 4 * (pt / 96) .. +3
+        // of each 8-word block
+        const int prow = CG == 2 ? pt % kBH : pt, phalf = CG == 2 ? pt / kBH : 0;
+        const bool one = CG == 2 || pt < kSw4N;  // NP = 240: the last warp has 16 rows
         const bool two = NP == 224 && pt + 128 < kSw4N;
         constexpr int NT = PT ? PT : kMaxPixTaps;
         struct Bits8 {
@@ -1961,7 +2018,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
             for (int h = 0; h < 2; ++h) {
                 int b = 0, oy = 0, ox = 0;
                 rc[h].valid = t_ld < tiles && (h == 0 ? one : two) &&
-                              decode_row(g, (t_ld / m_tiles) * kSw4N + pt + 128 * h, b, oy, ox);
+                              decode_row(g, (t_ld / m_tiles) * kSw4N + int(rank) * kBH + prow + 128 * h, b, oy, ox);
                 rc[h].pix = b * g.H, rc[h].y0 = oy * g.SH, rc[h].x0 = ox * g.SW;
             }
         };
@@ -1972,7 +2029,10 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 v[h] = rc[h].valid;
-                if constexpr (IN == FIN_BITS) {
+                if constexpr (IN == FIN_BITS && CG == 2) {
+                    dst[h].lo = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld + phalf) : make_uint4(0, 0, 0, 0);
+                    dst[h].hi = make_uint4(0, 0, 0, 0);
+                } else if constexpr (IN == FIN_BITS) {
                     dst[h].lo = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld) : make_uint4(0, 0, 0, 0);
                     dst[h].hi = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld + 1) : make_uint4(0, 0, 0, 0);
                 } else {
@@ -2005,11 +2065,18 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                     for (int h = 0; h < 2; ++h) pf[i][h] = pf[i + 1][h], pv[i][h] = pv[i + 1][h];
                 next_load(pf[kPF - 1], pv[kPF - 1]);
                 wc.wait(&empty[stage], phase ^ 1, 0);
-                const uint32_t tile = smem_u32(sX + size_t(stage) * kSw4N * kKB);
+                const uint32_t tile = smem_u32(sX + size_t(stage) * kBH * kKB);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     if ((h == 1 && !two) || (h == 0 && !one)) break;  // no such tile row
                     if (g.dbg_mode & 1) break;  // profiling: no stores (results invalid)
+                    if constexpr (CG == 2) {
+                        put_word4(tile, prow, 4 * phalf + 0, lo[0].x);
+                        put_word4(tile, prow, 4 * phalf + 1, lo[0].y);
+                        put_word4(tile, prow, 4 * phalf + 2, lo[0].z);
+                        put_word4(tile, prow, 4 * phalf + 3, lo[0].w);
+                        break;
+                    }
                     const int r = pt + 128 * h;
                     put_word4(tile, r, 0, lo[h].x);
                     put_word4(tile, r, 1, lo[h].y);
@@ -2023,8 +2090,13 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full[stage]);
-                if (++stage == kStages) stage = 0, phase ^= 1;
+                if (lane == 0) {
+                    if (CG == 2)
+                        mbar_arrive_cluster(leader(&full[stage]));
+                    else
+                        mbar_arrive(&full[stage]);
+                }
+                if (++stage == kS) stage = 0, phase ^= 1;
             }
         }
         if (pt == 0) wc.flush(g.dbg, 3);
@@ -2033,28 +2105,36 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) {
+        cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
+        if (warp == 1) tmem_dealloc_cg2<512>(tmem_base);
+    }
 }
 
-template <int IN, int PT, int NP>
+template <int IN, int PT, int NP, int CG = 1>
 int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_swap4_kernel<IN, PT, NP>;
+    auto kern = fused_swap4_kernel<IN, PT, NP, CG>;
     static bool attr_set = false;
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw4_smem<NP>())));
+        BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw4_smem<NP, CG>())));
         attr_set = true;
     }
-    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows)) * ceil_div(size_t(g.rows), size_t(NP)));
-    const int grid = std::min(tiles, num_sms());
+    const int tiles = int(ceil_div(size_t(g.D), size_t(kRows * CG)) * ceil_div(size_t(g.rows), size_t(NP)));
+    const int grid = std::min(tiles, num_sms() / CG) * CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
     cfg.blockDim = dim3(unsigned(sw4_threads<NP>()));
-    cfg.dynamicSmemBytes = sw4_smem<NP>();
+    cfg.dynamicSmemBytes = sw4_smem<NP, CG>();
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CG;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CG == 2 ? 2 : 1;
     static const int prof = getenv("BNN_FUSED_PROFILE") ? atoi(getenv("BNN_FUSED_PROFILE")) : 0;
     FusedGeom gd = g;
     unsigned long long* dbg = nullptr;
@@ -2072,9 +2152,9 @@ int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
         cudaFree(dbg);
         const double n = double(grid);
         fprintf(stderr,
-                "[swap4 in=%d rows=%d D=%d KB4=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | mma wait-acc %.1f "
+                "[swap4 in=%d cg=%d rows=%d D=%d KB4=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | mma wait-acc %.1f "
                 "wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
-                IN, g.rows, g.D, g.kb4, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
+                IN, CG, g.rows, g.D, g.kb4, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
                 h[8] / n / 1e3, h[12] / n / 1e3);
     }
     return BNN_OK;
@@ -2374,6 +2454,15 @@ int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_
     return launch_check("prep_weights4_kernel");
 }
 
+// CTA pairs for the FP4 swapped kernel on layers with >= 256 channels (bnn_set_fused_fp4_pair,
+// BNN_FP4_PAIR): -1 env / default on
+int g_fp4_pair = -1;
+
+int fused_set_fp4_pair(int enabled) {
+    g_fp4_pair = enabled ? 1 : 0;
+    return BNN_OK;
+}
+
 int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
     set_last_gemm("fused_swap_mxf4");
@@ -2385,6 +2474,8 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
         return launch_swap4_t<FIN_PIX, 0, 224>(tm4, g, s);
     }
     if (in_mode == FIN_BITS) {
+        if (g_fp4_pair < 0) g_fp4_pair = getenv("BNN_FP4_PAIR") ? atoi(getenv("BNN_FP4_PAIR")) : 1;
+        if (g_fp4_pair && g.D >= 2 * kRows && np == 192) return launch_swap4_t<FIN_BITS, 0, 192, 2>(tm4, g, s);
         if (np == 224) return launch_swap4_t<FIN_BITS, 0, 224>(tm4, g, s);
         if (np == 192) return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
         return launch_swap4_t<FIN_BITS, 0, 240>(tm4, g, s);

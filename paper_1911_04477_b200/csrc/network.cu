@@ -1032,6 +1032,11 @@ int bnn_set_fused_chain(int enabled) {
     return BNN_OK;
 }
 
+int bnn_set_fused_fp4_pair(int enabled) {
+    ++g_tiling_epoch;  // captured graphs hold the old kernels
+    return fused_set_fp4_pair(enabled);
+}
+
 int bnn_set_fused_tmem_a(int enabled) {
     ++g_tiling_epoch;  // captured graphs hold the old kernels
     return fused_set_tmem_a(enabled);

@@ -40,6 +40,10 @@ FUSABLE = {
     # C = 256 / 512 fast path with pooling down to 1x1, then a single logits layer
     "wide": {"input_shape": [1, 3, 8, 8], "seed": 3,
              "layers": [conv(256)] + POOL + G + [conv(512)] + POOL + G + [conv(256)] + POOL + G + [lin(33)]},
+    # FP4 CTA pairs with partial channel pairs (384 = 1.5 pairs, 320: the odd CTA's channels
+    # all past D), pooled and unpooled, position counts not a multiple of the 192-position tile
+    "pairs": {"input_shape": [1, 3, 12, 12], "seed": 21,
+              "layers": [conv(64)] + G + [conv(384)] + POOL + G + [conv(320)] + G + [lin(10)]},
     # linear-first stacks (BASELINE cfg1 / cfg4 shape class): K1 pack_rows of the float input,
     # linear -> linear with no glue (sign of float(a) + bias), a 4096-wide hidden layer
     "fc_stack": {"input_shape": [1, 288, 1, 1], "seed": 5, "layers": [lin(4096), lin(96), lin(10)]},
@@ -55,7 +59,7 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "noswap", "swapall", "nofp4", "fp4all", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "noswap", "swapall", "nofp4", "fp4all", "nopair", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -73,6 +77,7 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_small_logits(0 if p == "nosmall" else 1))
     bnn._lib.check(lib.bnn_set_fused_fp4({"fp4": 1, "fp4all": 2, "nofp4": 0}.get(p, 1)))
+    bnn._lib.check(lib.bnn_set_fused_fp4_pair(0 if p == "nopair" else 1))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_tmem_a(1)
@@ -81,6 +86,7 @@ def tiling(bnn, request):
     lib.bnn_set_fused_swap(1)
     lib.bnn_set_fused_small_logits(1)
     lib.bnn_set_fused_fp4(1)
+    lib.bnn_set_fused_fp4_pair(1)
 
 
 @pytest.fixture
