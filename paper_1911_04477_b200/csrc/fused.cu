@@ -1390,6 +1390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const int units = gridDim.x, unit = blockIdx.x;
     const int m_tiles = (g.D + kRows - 1) / kRows;
     const int n_tiles = (g.rows + kSwN - 1) / kSwN;
@@ -1431,6 +1432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 2] = gtimer();
 
     if (warp == 0) {
         // ------------------------------------------------------------ weight TMA (A)
@@ -1613,9 +1615,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pt == 0) wc.flush(g.dbg, 3);
     }
 
+    if (g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
     __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
     tc_fence_before();
     __syncthreads();  // (TMEM: deallocated by the MMA warp)
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
 }
 
 template <int IN, int PT>
@@ -1737,9 +1741,11 @@ template <int NP, int CG = 1>
 constexpr size_t sw4_smem() {
     return 1024 + size_t(CG == 2 ? kStages2 : kStages) * (kRows + NP / CG) * kKB + 256 + kMaxQ * 8;
 }
-template <int NP>
+// SP = 1 (CG = 1, NP = 192): 12 producer warps, two threads per tile row (one per 128-position
+// half of each K block), 22 warps in all.
+template <int NP, int SP = 0>
 constexpr int sw4_threads() {
-    return NP == 192 ? 512 : kThreads;
+    return SP ? 704 : NP == 192 ? 512 : kThreads;
 }
 
 // 32 activation bits -> 32 e2m1 nibbles (16 bytes) at 16-byte chunk `chunk` of row r. Output
@@ -1779,17 +1785,19 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
     return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(M >> 4) << 24);
 }
 
-template <int IN, int PT, int NP, int CG = 1>
-__global__ void __launch_bounds__(sw4_threads<NP>(), 1)
+template <int IN, int PT, int NP, int CG = 1, int SP = 0>
+__global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
     fused_swap4_kernel(const __grid_constant__ CUtensorMap tmW4, const FusedGeom g) {
     static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
     static_assert(NP == 192 || NP == 224 || NP == 240, "tile positions");
     static_assert(CG == 1 || (CG == 2 && IN == FIN_BITS && NP == 192), "CTA pairs: packed bits, 192 positions");
+    static_assert(!SP || (CG == 1 && IN == FIN_BITS && NP == 192), "split producers: packed bits, 192 positions");
+    constexpr bool kSplit = CG == 2 || SP;  // two producer threads per tile row
     constexpr int kSw4N = NP;
     constexpr int kBH = NP / CG;  // activation rows this CTA expands per stage
     constexpr int kS = CG == 2 ? kStages2 : kStages;
     constexpr int kSfCol = NP == 240 ? 480 : 2 * kSw4N;  // SFA, then SFB: 16 columns each at NP 240
-    constexpr int kProd = NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
+    constexpr int kProd = SP ? 12 : NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
     constexpr int kEpi = NP == 240 ? 4 : 8;                   // epilogue warps
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -1806,6 +1814,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     const int units = gridDim.x / CG, unit = blockIdx.x / CG;
     const int m_tiles = (g.D + kRows * CG - 1) / (kRows * CG);
@@ -1871,6 +1880,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
     if (CG == 2) cluster_sync();
     tc_fence_after();
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 2] = gtimer();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1954,7 +1964,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
             const bool wvalid = m0 + q * 32 < g.D;
             const int4 pc = wvalid ? __ldg(g.prm + c) : make_int4(0x7fffffff, 0, 0, 0);
             const float Tf = float(pc.x);  // exact: |Tu| <= K < 2^24
-            const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
+            const bool flip = pc.y != 0;
             const int oword = m0 / 32 + q;
             wc.wait(&tfull[acc], (i >> 1) & 1, 0);
             tc_fence_after();
@@ -1974,18 +1984,29 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                     }
                 }
                 uint32_t mine = 0;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t w = __ballot_sync(0xffffffffu, __uint_as_float(va[j]) >= Tf) ^ flipw;
-                    if (lane == j) mine = w;
-                }
-                const int pos = (cc * 32 + lane < kSw4N) ? nt * kSw4N + cc * 32 + lane : g.rows;  // past the tile: none
                 if (g.pool) {
-                    mine |= __shfl_xor_sync(0xffffffffu, mine, 1);
-                    mine |= __shfl_xor_sync(0xffffffffu, mine, 2);
-                    if (wvalid && (lane & 3) == 0 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
-                } else if (wvalid && pos < g.rows) {
-                    g.out_bits[size_t(pos) * g.Dw + oword] = mine;
+                    // 32 columns = 8 pool windows (pool-major: 4 adjacent columns). The pooled
+                    // bit OR_k((u_k >= T) ^ flip) is (max_k u_k >= T) without flip and
+                    // (min_k u_k < T) with it: one compare and one ballot per window.
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) {
+                        const float a = __uint_as_float(va[4 * p]), b = __uint_as_float(va[4 * p + 1]);
+                        const float c = __uint_as_float(va[4 * p + 2]), d = __uint_as_float(va[4 * p + 3]);
+                        const float m = flip ? fminf(fminf(a, b), fminf(c, d)) : fmaxf(fmaxf(a, b), fmaxf(c, d));
+                        const uint32_t w = __ballot_sync(0xffffffffu, (m >= Tf) != flip);
+                        if (lane == p) mine = w;
+                    }
+                    const int q0 = cc * 32 + 4 * lane;  // lane p < 8: window p's first column
+                    if (wvalid && lane < 8 && q0 < kSw4N && nt * kSw4N + q0 < g.rows)
+                        g.out_bits[size_t((nt * kSw4N + q0) >> 2) * g.Dw + oword] = mine;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t w = __ballot_sync(0xffffffffu, (__uint_as_float(va[j]) >= Tf) != flip);
+                        if (lane == j) mine = w;
+                    }
+                    const int pos = (cc * 32 + lane < kSw4N) ? nt * kSw4N + cc * 32 + lane : g.rows;  // past the tile: none
+                    if (wvalid && pos < g.rows) g.out_bits[size_t(pos) * g.Dw + oword] = mine;
                 }
             }
         }
@@ -1996,8 +2017,8 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
         const int pt = NP == 240 ? (warp - 6) * 32 + lane : (warp < 10 ? warp - 6 : warp - 10) * 32 + lane;
         // CG = 2: thread pt expands row pt % 96 of this CTA's half, K words 4 * (pt / 96) .. +3
         // of each 8-word block
-        const int prow = CG == 2 ? pt % kBH : pt, phalf = CG == 2 ? pt / kBH : 0;
-        const bool one = CG == 2 || pt < kSw4N;  // NP = 240: the last warp has 16 rows
+        const int prow = kSplit ? pt % kBH : pt, phalf = kSplit ? pt / kBH : 0;
+        const bool one = kSplit || pt < kSw4N;  // NP = 240: the last warp has 16 rows
         const bool two = NP == 224 && pt + 128 < kSw4N;
         constexpr int NT = PT ? PT : kMaxPixTaps;
         struct Bits8 {
@@ -2029,7 +2050,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 v[h] = rc[h].valid;
-                if constexpr (IN == FIN_BITS && CG == 2) {
+                if constexpr (IN == FIN_BITS && kSplit) {
                     dst[h].lo = t_ld < tiles ? load_bits(g, ftab, rc[h], 2 * kb_ld + phalf) : make_uint4(0, 0, 0, 0);
                     dst[h].hi = make_uint4(0, 0, 0, 0);
                 } else if constexpr (IN == FIN_BITS) {
@@ -2070,7 +2091,7 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
                 for (int h = 0; h < 2; ++h) {
                     if ((h == 1 && !two) || (h == 0 && !one)) break;  // no such tile row
                     if (g.dbg_mode & 1) break;  // profiling: no stores (results invalid)
-                    if constexpr (CG == 2) {
+                    if constexpr (kSplit) {
                         put_word4(tile, prow, 4 * phalf + 0, lo[0].x);
                         put_word4(tile, prow, 4 * phalf + 1, lo[0].y);
                         put_word4(tile, prow, 4 * phalf + 2, lo[0].z);
@@ -2102,18 +2123,20 @@ __global__ void __launch_bounds__(sw4_threads<NP>(), 1)
         if (pt == 0) wc.flush(g.dbg, 3);
     }
 
+    if (g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
     if (CG == 2) {
         cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
         if (warp == 1) tmem_dealloc_cg2<512>(tmem_base);
     }
 }
 
-template <int IN, int PT, int NP, int CG = 1>
+template <int IN, int PT, int NP, int CG = 1, int SP = 0>
 int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    auto kern = fused_swap4_kernel<IN, PT, NP, CG>;
+    auto kern = fused_swap4_kernel<IN, PT, NP, CG, SP>;
     static bool attr_set = false;
     if (!attr_set) {
         BNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw4_smem<NP, CG>())));
@@ -2123,7 +2146,7 @@ int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms() / CG) * CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(unsigned(sw4_threads<NP>()));
+    cfg.blockDim = dim3(unsigned(sw4_threads<NP, SP>()));
     cfg.dynamicSmemBytes = sw4_smem<NP, CG>();
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -2144,6 +2167,8 @@ int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
         gd.dbg = dbg;
         gd.dbg_mode = prof >> 1;
     }
+    gd.tl = fused_timeline_slot(1);
+    if (gd.tl) g_tl_names.push_back("swap4 cg=" + std::to_string(CG) + " D=" + std::to_string(g.D) + " KB4=" + std::to_string(g.kb4));
     BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm, gd));
     BNN_TRY(launch_check("fused_swap4_kernel"));
     if (prof) {
@@ -2153,9 +2178,9 @@ int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
         const double n = double(grid);
         fprintf(stderr,
                 "[swap4 in=%d cg=%d rows=%d D=%d KB4=%d grid=%d] per-CTA kcycles: total %.1f | tma wait %.1f | mma wait-acc %.1f "
-                "wait-full %.1f | epi wait %.1f | prod wait %.1f\n",
+                "wait-full %.1f | epi wait %.1f | prod wait %.1f | role totals mma %.1f epi %.1f prod %.1f\n",
                 IN, CG, g.rows, g.D, g.kb4, grid, h[3] / n / 1e3, h[0] / n / 1e3, h[4] / n / 1e3, h[5] / n / 1e3,
-                h[8] / n / 1e3, h[12] / n / 1e3);
+                h[8] / n / 1e3, h[12] / n / 1e3, h[7] / n / 1e3, h[11] / n / 1e3, h[15] / n / 1e3);
     }
     return BNN_OK;
 }
@@ -2477,6 +2502,8 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
         if (g_fp4_pair < 0) g_fp4_pair = getenv("BNN_FP4_PAIR") ? atoi(getenv("BNN_FP4_PAIR")) : 1;
         if (g_fp4_pair && g.D >= 2 * kRows && np == 192) return launch_swap4_t<FIN_BITS, 0, 192, 2>(tm4, g, s);
         if (np == 224) return launch_swap4_t<FIN_BITS, 0, 224>(tm4, g, s);
+        static const int sp = getenv("BNN_FP4_SPLIT") ? atoi(getenv("BNN_FP4_SPLIT")) : 1;
+        if (np == 192 && sp) return launch_swap4_t<FIN_BITS, 0, 192, 1, 1>(tm4, g, s);
         if (np == 192) return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
         return launch_swap4_t<FIN_BITS, 0, 240>(tm4, g, s);
     }
