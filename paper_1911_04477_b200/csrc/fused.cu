@@ -1501,7 +1501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool wvalid = mt * kRows + q * 32 < g.D;  // D % 32 == 0: whole words
             const int4 pc = wvalid ? __ldg(g.prm + c) : make_int4(0x7fffffff, 0, 0, 0);
             const int Tu = pc.x;
-            const uint32_t flipw = __ballot_sync(0xffffffffu, pc.y != 0);
+            const bool flip = pc.y != 0;  // folded into each compare: bit = (u >= Tu) != flip
             const int oword = mt * (kRows / 32) + q;
             wc.wait(&tfull[acc], (i >> 1) & 1, 0);
             tc_fence_after();
@@ -1509,18 +1509,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t va[32], vb[32];
             auto emit = [&](const uint32_t(&v)[32], int cc) {
                 uint32_t mine = 0;
+                if (g.pool) {  // one compare per pool window, as in fused_swap4_kernel
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t w = __ballot_sync(0xffffffffu, int(v[j]) >= Tu) ^ flipw;
-                    if (lane == j) mine = w;
-                }
-                const int pos = nt * kSwN + col0 + cc * 32 + lane;
-                if (g.pool) {
-                    mine |= __shfl_xor_sync(0xffffffffu, mine, 1);
-                    mine |= __shfl_xor_sync(0xffffffffu, mine, 2);
-                    if (wvalid && (lane & 3) == 0 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
-                } else if (wvalid && pos < g.rows) {
-                    g.out_bits[size_t(pos) * g.Dw + oword] = mine;
+                    for (int p = 0; p < 8; ++p) {
+                        const int a = int(v[4 * p]), b = int(v[4 * p + 1]), c = int(v[4 * p + 2]), d = int(v[4 * p + 3]);
+                        const int m = flip ? min(min(a, b), min(c, d)) : max(max(a, b), max(c, d));
+                        const uint32_t w = __ballot_sync(0xffffffffu, (m >= Tu) != flip);
+                        if (lane == p) mine = w;
+                    }
+                    const int pos = nt * kSwN + col0 + cc * 32 + 4 * lane;
+                    if (wvalid && lane < 8 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t w = __ballot_sync(0xffffffffu, (int(v[j]) >= Tu) != flip);
+                        if (lane == j) mine = w;
+                    }
+                    const int pos = nt * kSwN + col0 + cc * 32 + lane;
+                    if (wvalid && pos < g.rows) g.out_bits[size_t(pos) * g.Dw + oword] = mine;
                 }
             };
             tmem_ld32(tbase, va);
@@ -1743,9 +1749,10 @@ constexpr size_t sw4_smem() {
 }
 // SP = 1 (CG = 1, NP = 192): 12 producer warps, two threads per tile row (one per 128-position
 // half of each K block), 22 warps in all.
-template <int NP, int SP = 0>
+// CG = 2, NP = 224: 8 producer warps (2-thread rows over 112 rows per CTA), 18 warps.
+template <int NP, int SP = 0, int CG = 1>
 constexpr int sw4_threads() {
-    return SP ? 704 : NP == 192 ? 512 : kThreads;
+    return SP ? 704 : (CG == 2 && NP == 224) ? 576 : NP == 192 ? 512 : kThreads;
 }
 
 // 32 activation bits -> 32 e2m1 nibbles (16 bytes) at 16-byte chunk `chunk` of row r. Output
@@ -1786,18 +1793,18 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
 }
 
 template <int IN, int PT, int NP, int CG = 1, int SP = 0>
-__global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
+__global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
     fused_swap4_kernel(const __grid_constant__ CUtensorMap tmW4, const FusedGeom g) {
     static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
     static_assert(NP == 192 || NP == 224 || NP == 240, "tile positions");
-    static_assert(CG == 1 || (CG == 2 && IN == FIN_BITS && NP == 192), "CTA pairs: packed bits, 192 positions");
+    static_assert(CG == 1 || (CG == 2 && IN == FIN_BITS && (NP == 192 || NP == 224)), "CTA pairs: packed bits");
     static_assert(!SP || (CG == 1 && IN == FIN_BITS && NP == 192), "split producers: packed bits, 192 positions");
     constexpr bool kSplit = CG == 2 || SP;  // two producer threads per tile row
     constexpr int kSw4N = NP;
     constexpr int kBH = NP / CG;  // activation rows this CTA expands per stage
     constexpr int kS = CG == 2 ? kStages2 : kStages;
     constexpr int kSfCol = NP == 240 ? 480 : 2 * kSw4N;  // SFA, then SFB: 16 columns each at NP 240
-    constexpr int kProd = SP ? 12 : NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
+    constexpr int kProd = SP ? 12 : (CG == 2 && NP == 224) ? 8 : NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
     constexpr int kEpi = NP == 240 ? 4 : 8;                   // epilogue warps
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -1904,6 +1911,14 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
                 }
             }
             wc.flush(g.dbg, 0);
+            if (CG == 2) {
+                // every stage's last release (the pair MMA's multicast commit) has landed in
+                // this CTA's barriers before it may exit
+                for (int k = 0; k < kS; ++k) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (++stage == kS) stage = 0, phase ^= 1;
+                }
+            }
         }
     } else if (warp == 1) {
         constexpr uint32_t idesc = idesc_mxf4(kRows * CG, kSw4N);
@@ -1943,10 +1958,12 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
             }
         }
         if (lane == 0) wc.flush(g.dbg, 1);
-        if (CG == 1) {
+        if (CG == 1 || rank == 0) {
+            // the epilogue has read the last accumulators (CG = 2: both CTAs' epilogue warps,
+            // whose remote arrives have then all landed here)
             for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
             tc_fence_after();
-            tmem_dealloc<512>(tmem_base);
+            if (CG == 1) tmem_dealloc<512>(tmem_base);
         }  // CG = 2: both CTAs deallocate after the final cluster barrier
     } else if (warp < 6 || (kEpi == 8 && warp >= 10 && warp < 14)) {
         WaitClock wc;
@@ -2018,8 +2035,8 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
         // CG = 2: thread pt expands row pt % 96 of this CTA's half, K words 4 * (pt / 96) .. +3
         // of each 8-word block
         const int prow = kSplit ? pt % kBH : pt, phalf = kSplit ? pt / kBH : 0;
-        const bool one = kSplit || pt < kSw4N;  // NP = 240: the last warp has 16 rows
-        const bool two = NP == 224 && pt + 128 < kSw4N;
+        const bool one = kSplit ? pt < 2 * kBH : pt < kSw4N;  // NP = 240: the last warp has 16 rows
+        const bool two = NP == 224 && !kSplit && pt + 128 < kSw4N;
         constexpr int NT = PT ? PT : kMaxPixTaps;
         struct Bits8 {
             uint4 lo, hi;
@@ -2123,14 +2140,18 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP>(), 1)
         if (pt == 0) wc.flush(g.dbg, 3);
     }
 
-    if (g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
+    if (CG == 1 && g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();
     __syncwarp();
     tc_fence_before();
     __syncthreads();
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = gtimer();
     if (CG == 2) {
-        cluster_sync();  // no remote arrive / pair MMA may target a CTA that has exited
+        // Every cross-CTA operation has landed (the drains above: the leader saw all remote
+        // arrives, each CTA saw all multicast commits), so the teardown barrier needs no
+        // release of this CTA's global stores.
+        cluster_sync_relaxed();
         if (warp == 1) tmem_dealloc_cg2<512>(tmem_base);
+        if (g.tl && warp == 1 && lane == 0) g.tl[blockIdx.x * 4 + 1] = gtimer();  // k1: TMEM released
     }
 }
 
@@ -2146,7 +2167,7 @@ int launch_swap4_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms() / CG) * CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(unsigned(sw4_threads<NP, SP>()));
+    cfg.blockDim = dim3(unsigned(sw4_threads<NP, SP, CG>()));
     cfg.dynamicSmemBytes = sw4_smem<NP, CG>();
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -2483,8 +2504,9 @@ int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_
 // BNN_FP4_PAIR): -1 env / default on
 int g_fp4_pair = -1;
 
-int fused_set_fp4_pair(int enabled) {
-    g_fp4_pair = enabled ? 1 : 0;
+int fused_set_fp4_pair(int mode) {
+    if (mode < 0 || mode > 3) return fail(BNN_E_CONFIG, "fp4 pair mode: 0 off, 1 auto, 2 192 positions, 3 224");
+    g_fp4_pair = mode;
     return BNN_OK;
 }
 
@@ -2500,7 +2522,15 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
     }
     if (in_mode == FIN_BITS) {
         if (g_fp4_pair < 0) g_fp4_pair = getenv("BNN_FP4_PAIR") ? atoi(getenv("BNN_FP4_PAIR")) : 1;
-        if (g_fp4_pair && g.D >= 2 * kRows && np == 192) return launch_swap4_t<FIN_BITS, 0, 192, 2>(tm4, g, s);
+        if (g_fp4_pair && g.D >= 2 * kRows && np == 192) {
+            // 192 or 224 positions per pair tile: whichever needs fewer rounds of the pairs
+            // (e.g. 16 x 16 x 256 rows: 4.6 -> 5 rounds at 192, 3.95 -> 4 at 224)
+            const size_t pairs = size_t(num_sms() / 2), mp = ceil_div(size_t(g.D), size_t(2 * kRows));
+            const size_t r192 = ceil_div(mp * ceil_div(size_t(g.rows), size_t(192)), pairs);
+            const size_t r224 = ceil_div(mp * ceil_div(size_t(g.rows), size_t(224)), pairs);
+            if (g_fp4_pair == 3 || (g_fp4_pair == 1 && r224 < r192)) return launch_swap4_t<FIN_BITS, 0, 224, 2>(tm4, g, s);
+            return launch_swap4_t<FIN_BITS, 0, 192, 2>(tm4, g, s);
+        }
         if (np == 224) return launch_swap4_t<FIN_BITS, 0, 224>(tm4, g, s);
         static const int sp = getenv("BNN_FP4_SPLIT") ? atoi(getenv("BNN_FP4_SPLIT")) : 1;
         if (np == 192 && sp) return launch_swap4_t<FIN_BITS, 0, 192, 1, 1>(tm4, g, s);

@@ -96,7 +96,7 @@ int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const fl
 int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN);
 int fused_set_tmem_a(int enabled);
 int fused_tmem_a();
-int fused_set_fp4_pair(int enabled);
+int fused_set_fp4_pair(int mode);
 int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s);
 // cg = 1: CTA-local M=128 tiles; cg = 2: CTA pairs with cta_group::2 M=256 tiles. tm must be
 // the weight map whose box has BN / cg rows.

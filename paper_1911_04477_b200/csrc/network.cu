@@ -1032,9 +1032,9 @@ int bnn_set_fused_chain(int enabled) {
     return BNN_OK;
 }
 
-int bnn_set_fused_fp4_pair(int enabled) {
+int bnn_set_fused_fp4_pair(int mode) {
     ++g_tiling_epoch;  // captured graphs hold the old kernels
-    return fused_set_fp4_pair(enabled);
+    return fused_set_fp4_pair(mode);
 }
 
 int bnn_set_fused_tmem_a(int enabled) {

@@ -218,6 +218,13 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Cluster barrier without release semantics: no flush of the CTA's outstanding writes (the
+// release form measured ~5 us at the end of a pair kernel with the epilogue's stores in flight).
+// Only for teardown after every cross-CTA operation is known to have landed.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // shared::cluster address of the variable at local shared::cta address `a` in CTA `rank`
 __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
     uint32_t r;
