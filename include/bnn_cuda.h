@@ -259,8 +259,9 @@ const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer);
  * the pixel-input first conv. Bit-exact in every mode. */
 int bnn_set_fused_fp4(int mode);
 /* Fused engine: FP4 swapped conv on CTA pairs (cta_group::2, 256 channels per pair: each SM
- * expands half the activation rows) for layers with >= 256 channels: 0 off, 1 (default) on
- * with 192 or 224 positions per tile (fewer rounds), 2 / 3 forced 192 / 224. */
+ * expands half the activation rows) for layers with >= 256 channels: 0 off, 1 (default) on.
+ * Positions per tile (pairs and the 128-channel kernel): 192 or 224, whichever needs fewer
+ * rounds over the SMs; modes 2 / 3 force 192 / 224 (mode 0: 192). */
 int bnn_set_fused_fp4_pair(int mode);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */

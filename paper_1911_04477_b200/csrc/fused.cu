@@ -1752,7 +1752,7 @@ constexpr size_t sw4_smem() {
 // CG = 2, NP = 224: 8 producer warps (2-thread rows over 112 rows per CTA), 18 warps.
 template <int NP, int SP = 0, int CG = 1>
 constexpr int sw4_threads() {
-    return SP ? 704 : (CG == 2 && NP == 224) ? 576 : NP == 192 ? 512 : kThreads;
+    return SP ? (NP == 224 ? 768 : 704) : (CG == 2 && NP == 224) ? 576 : NP == 192 ? 512 : kThreads;
 }
 
 // 32 activation bits -> 32 e2m1 nibbles (16 bytes) at 16-byte chunk `chunk` of row r. Output
@@ -1798,13 +1798,13 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
     static_assert(IN == FIN_BITS || IN == FIN_PIX, "packed-bit or pixel-packed input");
     static_assert(NP == 192 || NP == 224 || NP == 240, "tile positions");
     static_assert(CG == 1 || (CG == 2 && IN == FIN_BITS && (NP == 192 || NP == 224)), "CTA pairs: packed bits");
-    static_assert(!SP || (CG == 1 && IN == FIN_BITS && NP == 192), "split producers: packed bits, 192 positions");
+    static_assert(!SP || (CG == 1 && IN == FIN_BITS && (NP == 192 || NP == 224)), "split producers: packed bits");
     constexpr bool kSplit = CG == 2 || SP;  // two producer threads per tile row
     constexpr int kSw4N = NP;
     constexpr int kBH = NP / CG;  // activation rows this CTA expands per stage
     constexpr int kS = CG == 2 ? kStages2 : kStages;
     constexpr int kSfCol = NP == 240 ? 480 : 2 * kSw4N;  // SFA, then SFB: 16 columns each at NP 240
-    constexpr int kProd = SP ? 12 : (CG == 2 && NP == 224) ? 8 : NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
+    constexpr int kProd = SP ? (NP == 224 ? 14 : 12) : (CG == 2 && NP == 224) ? 8 : NP == 240 ? 8 : NP == 192 ? 6 : 4;  // producer warps
     constexpr int kEpi = NP == 240 ? 4 : 8;                   // epilogue warps
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -2533,7 +2533,15 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
         }
         if (np == 224) return launch_swap4_t<FIN_BITS, 0, 224>(tm4, g, s);
         static const int sp = getenv("BNN_FP4_SPLIT") ? atoi(getenv("BNN_FP4_SPLIT")) : 1;
-        if (np == 192 && sp) return launch_swap4_t<FIN_BITS, 0, 192, 1, 1>(tm4, g, s);
+        if (np == 192 && sp) {
+            // 192 or 224 positions per tile (14 producer warps at 224): fewer rounds wins
+            const size_t sms = size_t(num_sms()), mt = ceil_div(size_t(g.D), size_t(kRows));
+            const size_t r192 = ceil_div(mt * ceil_div(size_t(g.rows), size_t(192)), sms);
+            const size_t r224 = ceil_div(mt * ceil_div(size_t(g.rows), size_t(224)), sms);
+            if (g_fp4_pair == 3 || (g_fp4_pair == 1 && r224 < r192))
+                return launch_swap4_t<FIN_BITS, 0, 224, 1, 1>(tm4, g, s);
+            return launch_swap4_t<FIN_BITS, 0, 192, 1, 1>(tm4, g, s);
+        }
         if (np == 192) return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
         return launch_swap4_t<FIN_BITS, 0, 240>(tm4, g, s);
     }
