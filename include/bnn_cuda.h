@@ -294,6 +294,19 @@ int bnn_host_linear_forward_packed(const float* x, size_t K, size_t N, const uin
                                    size_t M, const float* bias, float* out);
 int bnn_host_net_forward(bnn_net* net, const float* x, size_t batch, float* logits);
 
+/* Serving pipeline over host buffers (the reference's network_forward per batch, run as a
+ * stream of batches): each submitted batch is copied in from host memory, run through the
+ * network and its logits [features, batch] copied back, on separate copy / compute streams so
+ * that batch i+1's H2D and batch i-1's D2H overlap batch i's forward. Host buffers should be
+ * pinned (cudaHostAlloc / torch pin_memory) for the copies to be asynchronous. At most `depth`
+ * (2..8) batches may be outstanding; bnn_pipe_wait(seq) blocks until batch seq's logits are in
+ * its host buffer. */
+typedef struct bnn_pipe bnn_pipe;
+int bnn_pipe_create(bnn_net* net, size_t batch, int depth, bnn_pipe** out);
+int bnn_pipe_submit(bnn_pipe* p, const float* x, float* logits, uint64_t* seq);
+int bnn_pipe_wait(bnn_pipe* p, uint64_t seq);
+int bnn_pipe_destroy(bnn_pipe* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,7 +7,7 @@ reference interface (``api``) plus the ctypes binding (``_lib``).
 """
 from ._lib import (BnnError, ConfigError, CudaError, EncodingError, IoError, ShapeError,  # noqa: F401
                    EXPORTS, LIB_PATH, load)
-from .api import (COL_PACKED, ROW_PACKED, ConvGeometry, Network, PackedBitMatrix,  # noqa: F401
+from .api import (COL_PACKED, ROW_PACKED, ConvGeometry, Network, PackedBitMatrix, Pipeline,  # noqa: F401
                   affine_norm, bias_add, conv_forward_binary, default_layers, fill_random,
                   flatten_to_columns, fnv1a_hash, htanh, im2col_sign_pack, linear_forward,
                   linear_forward_packed, load_packed_blob, load_tensor_blob, maxpool2, mix64,

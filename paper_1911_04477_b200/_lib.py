@@ -131,6 +131,10 @@ _SIGS = {
     "bnn_host_conv_forward_binary": (_I, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "bnn_host_linear_forward_packed": (_I, [_P, _SZ, _SZ, _P, _SZ, _P, _P]),
     "bnn_host_net_forward": (_I, [_P, _P, _SZ, _P]),
+    "bnn_pipe_create": (_I, [_P, _SZ, _I, _P]),
+    "bnn_pipe_submit": (_I, [_P, _P, _P, _P]),
+    "bnn_pipe_wait": (_I, [_P, _U64]),
+    "bnn_pipe_destroy": (_I, [_P]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -540,6 +540,10 @@ class Network:
 
     ENGINES = {"auto": 0, "generic": 1, "fused": 2, "float": 3}
 
+    def pipeline(self, batch: int, depth: int = 3) -> "Pipeline":
+        """A serving pipeline of host-buffer batches (bnn_pipe_*)."""
+        return Pipeline(self, batch, depth)
+
     def set_engine(self, name: str) -> None:
         """Select the device engine: "fused" (one tcgen05 launch per weighted layer, packed-bit
         activations), "generic" (one kernel per reference op) or "auto" (fused when the topology
@@ -589,3 +593,35 @@ class Network:
             elif k == "maxpool":
                 h, w = h // 2, w // 2
         return c
+
+
+class Pipeline:
+    """Host buffers in and out, batches pipelined (bnn_pipe_*): submit() copies a batch in,
+    runs the network and copies its logits back, asynchronously; wait(seq) blocks until batch
+    seq's logits are in the buffer passed to submit(). Host buffers should be pinned (e.g.
+    torch pin_memory tensors) for the copies to overlap the forward of the previous batch."""
+
+    def __init__(self, net: "Network", batch: int, depth: int = 3):
+        h = C.c_void_p()
+        check(load().bnn_pipe_create(net._h, batch, depth, C.byref(h)))
+        self._h, self._net, self.batch, self.depth = h, net, batch, depth
+
+    def submit(self, x_ptr: int, logits_ptr: int) -> int:
+        """x_ptr: host float32 [batch, C, H, W]; logits_ptr: host float32 [features, batch]."""
+        seq = C.c_uint64()
+        check(load().bnn_pipe_submit(self._h, C.c_void_p(x_ptr), C.c_void_p(logits_ptr), C.byref(seq)))
+        return seq.value
+
+    def wait(self, seq: int) -> None:
+        check(load().bnn_pipe_wait(self._h, seq))
+
+    def close(self) -> None:
+        if self._h:
+            load().bnn_pipe_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

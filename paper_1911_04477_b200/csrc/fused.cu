@@ -1520,11 +1520,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int pos = nt * kSwN + col0 + cc * 32 + 4 * lane;
                     if (wvalid && lane < 8 && pos < g.rows) g.out_bits[size_t(pos >> 2) * g.Dw + oword] = mine;
                 } else {
+                    uint32_t mk[4] = {0u, 0u, 0u, 0u};  // four independent select chains
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const uint32_t w = __ballot_sync(0xffffffffu, (int(v[j]) >= Tu) != flip);
-                        if (lane == j) mine = w;
+                        if (lane == j) mk[j & 3] = w;
                     }
+                    mine = (mk[0] | mk[1]) | (mk[2] | mk[3]);
                     const int pos = nt * kSwN + col0 + cc * 32 + lane;
                     if (wvalid && pos < g.rows) g.out_bits[size_t(pos) * g.Dw + oword] = mine;
                 }
@@ -2017,11 +2019,13 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
                     if (wvalid && lane < 8 && q0 < kSw4N && nt * kSw4N + q0 < g.rows)
                         g.out_bits[size_t((nt * kSw4N + q0) >> 2) * g.Dw + oword] = mine;
                 } else {
+                    uint32_t mk[4] = {0u, 0u, 0u, 0u};  // four independent select chains
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const uint32_t w = __ballot_sync(0xffffffffu, (__uint_as_float(va[j]) >= Tf) != flip);
-                        if (lane == j) mine = w;
+                        if (lane == j) mk[j & 3] = w;
                     }
+                    mine = (mk[0] | mk[1]) | (mk[2] | mk[3]);
                     const int pos = (cc * 32 + lane < kSw4N) ? nt * kSw4N + cc * 32 + lane : g.rows;  // past the tile: none
                     if (wvalid && pos < g.rows) g.out_bits[size_t(pos) * g.Dw + oword] = mine;
                 }

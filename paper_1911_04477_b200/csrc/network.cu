@@ -1149,3 +1149,92 @@ int bnn_host_net_forward(bnn_net* net, const float* x, size_t batch, float* logi
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Serving pipeline over host buffers: each submitted batch is copied in from (pinned) host
+// memory, run through the network and its logits copied back, on three streams so that batch
+// i+1's H2D and batch i-1's D2H overlap batch i's forward. `depth` device buffer sets; the
+// forward of each set replays its own captured graph (bnn_net_forward's cache).
+struct bnn_pipe {
+    bnn_net* net = nullptr;
+    size_t batch = 0, nx = 0, ny = 0;
+    int depth = 0;
+    uint64_t submitted = 0;
+    cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
+    std::vector<float*> dx, dy;
+    std::vector<cudaEvent_t> ev_in, ev_run, ev_out;
+};
+
+extern "C" {
+
+int bnn_pipe_create(bnn_net* net, size_t batch, int depth, bnn_pipe** out) {
+    BNN_TRY(require_sm100());
+    if (!net || !out || batch == 0 || depth < 2 || depth > 8)
+        return fail(BNN_E_CONFIG, "pipe: need a network, batch > 0 and 2 <= depth <= 8");
+    auto p = std::make_unique<bnn_pipe>();
+    p->net = net, p->batch = batch, p->depth = depth;
+    p->nx = batch * net->in_c * net->in_h * net->in_w, p->ny = batch * net->logits;
+    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_run, cudaStreamNonBlocking));
+    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    for (int k = 0; k < depth; ++k) {
+        float *x = nullptr, *y = nullptr;
+        BNN_CUDA(cudaMalloc(&x, p->nx * 4));
+        p->dx.push_back(x);
+        BNN_CUDA(cudaMalloc(&y, p->ny * 4));
+        p->dy.push_back(y);
+        cudaEvent_t e[3];
+        for (auto& ev : e) BNN_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        p->ev_in.push_back(e[0]), p->ev_run.push_back(e[1]), p->ev_out.push_back(e[2]);
+    }
+    *out = p.release();
+    return BNN_OK;
+}
+
+// Enqueue one batch: x [batch, C, H, W] and logits [features, batch] are host buffers (pinned
+// for asynchronous copies). Returns its sequence number in *seq. The caller must not reuse
+// `logits` before bnn_pipe_wait(seq), nor have more than `depth` batches outstanding.
+int bnn_pipe_submit(bnn_pipe* p, const float* x, float* logits, uint64_t* seq) {
+    if (!p) return fail(BNN_E_CONFIG, "pipe: null");
+    const int k = int(p->submitted % uint64_t(p->depth));
+    BNN_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_run[k], 0));  // set k's previous forward read dx[k]
+    BNN_CUDA(cudaMemcpyAsync(p->dx[k], x, p->nx * 4, cudaMemcpyHostToDevice, p->s_in));
+    BNN_CUDA(cudaEventRecord(p->ev_in[k], p->s_in));
+    BNN_CUDA(cudaStreamWaitEvent(p->s_run, p->ev_in[k], 0));
+    BNN_CUDA(cudaStreamWaitEvent(p->s_run, p->ev_out[k], 0));  // set k's previous D2H read dy[k]
+    BNN_TRY(forward(p->net, p->dx[k], p->batch, p->dy[k], p->s_run));
+    BNN_CUDA(cudaEventRecord(p->ev_run[k], p->s_run));
+    BNN_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_run[k], 0));
+    BNN_CUDA(cudaMemcpyAsync(logits, p->dy[k], p->ny * 4, cudaMemcpyDeviceToHost, p->s_out));
+    BNN_CUDA(cudaEventRecord(p->ev_out[k], p->s_out));
+    if (seq) *seq = p->submitted;
+    ++p->submitted;
+    return BNN_OK;
+}
+
+// Block until batch `seq`'s logits are in its host buffer (seq within the last `depth`).
+int bnn_pipe_wait(bnn_pipe* p, uint64_t seq) {
+    if (!p) return fail(BNN_E_CONFIG, "pipe: null");
+    if (seq >= p->submitted || seq + uint64_t(p->depth) < p->submitted)
+        return fail(BNN_E_CONFIG, "pipe: batch " + std::to_string(seq) + " is not among the last " +
+                                      std::to_string(p->depth) + " submitted");
+    BNN_CUDA(cudaEventSynchronize(p->ev_out[seq % uint64_t(p->depth)]));
+    return BNN_OK;
+}
+
+int bnn_pipe_destroy(bnn_pipe* p) {
+    if (!p) return BNN_OK;
+    if (p->s_out) cudaStreamSynchronize(p->s_out);
+    if (p->s_run) cudaStreamSynchronize(p->s_run);
+    if (p->s_in) cudaStreamSynchronize(p->s_in);
+    for (auto v : p->dx) cudaFree(v);
+    for (auto v : p->dy) cudaFree(v);
+    for (auto* evs : {&p->ev_in, &p->ev_run, &p->ev_out})
+        for (auto e : *evs) cudaEventDestroy(e);
+    for (auto s : {p->s_in, p->s_run, p->s_out})
+        if (s) cudaStreamDestroy(s);
+    delete p;
+    return BNN_OK;
+}
+
+}  // extern "C"

@@ -188,3 +188,29 @@ def test_graph_replay_matches_eager(bnn, orc):
         net.forward_device(x, out, st.cuda_stream)
         st.synchronize()
     assert np.array_equal(out.cpu().numpy(), orc.net(seed=6).forward(x2.cpu().numpy()))
+
+
+def test_pipeline_host_buffers_vs_oracle(bnn, orc):
+    """bnn_pipe_*: batches submitted from pinned host buffers come back with the oracle's
+    logits, in order, with more batches in flight than buffer sets would allow unsynchronised."""
+    torch = pytest.importorskip("torch")
+    net = bnn.Network(seed=2)
+    B, depth = 7, 3
+    xs = [orc.fill_random((B, 3, 32, 32), orc.mix64(s, INPUT_STREAM)) for s in range(5)]
+    want = [orc.net(seed=2).forward(x) for x in xs]
+    hx = [torch.from_numpy(x).pin_memory() for x in xs]
+    hy = [torch.empty((net.logits, B), dtype=torch.float32).pin_memory() for _ in range(depth)]
+    pipe = net.pipeline(B, depth)
+    seqs = []
+    for i in range(12):
+        if i >= depth:
+            pipe.wait(seqs[i - depth])
+            k = i - depth
+            assert np.array_equal(hy[k % depth].numpy(), want[k % 5]), k
+        seqs.append(pipe.submit(hx[i % 5].data_ptr(), hy[i % depth].data_ptr()))
+    with pytest.raises(bnn.ConfigError):
+        pipe.wait(seqs[0])  # no longer among the last `depth`
+    for k in range(12 - depth, 12):
+        pipe.wait(seqs[k])
+        assert np.array_equal(hy[k % depth].numpy(), want[k % 5]), k
+    pipe.close()
