@@ -436,6 +436,14 @@ void choose_tile(int D, size_t rows, int KB, bool pool, int& cg, int& bn, int& k
         const int kmin = g_forced_split > 1 ? 1 : 4;  // auto: at least 4 K-blocks per slice
         // every split tile needs its own co-resident CTA (fused.cu split-K completion)
         while (ks < cap && out_tiles * size_t(ks * 2) <= units && ks * 2 * kmin <= KB) ks *= 2;
+        // Half-width tiles with half the slices keep the same CTA count and halve the partial
+        // sums written and re-read (fc 8192->1024 at batch 256: 28 -> 24 us per layer event).
+        if (ks > 1 && bn == 256 && !bn_forced && g_forced_split <= 1) {
+            const size_t out2 = m_tiles * ceil_div(size_t(D), size_t(128));
+            int ks2 = 1;
+            while (ks2 < cap && out2 * size_t(ks2 * 2) <= units && ks2 * 2 * kmin <= KB) ks2 *= 2;
+            if (ks2 > 1 && out2 * size_t(ks2) >= out_tiles * size_t(ks)) bn = 128, ks = ks2;
+        }
     }
     if (ks == 1 && !bn_forced)
         while (bn > 32 && m_tiles * ceil_div(size_t(D), size_t(bn)) < units) bn /= 2;
