@@ -2419,9 +2419,44 @@ int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int B
     return make_tmap_2d_s8(map, w, size_t(Dpad), size_t(Kpad), size_t(Kpad), uint32_t(BN));
 }
 
+// Four pixels per thread (HW % 4 == 0, 16-byte aligned input): one 16-byte load per channel
+// and one 16-byte store; 32-bit index math. C is a template constant for the 3-channel input.
+template <int CT>
+__global__ void pack_pixels4_kernel(const float4* __restrict__ x, int C, unsigned HW4, unsigned total4,
+                                    uint4* __restrict__ out) {
+    const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total4) return;
+    const unsigned b = i / HW4, p = i - b * HW4;
+    const int nc = CT ? CT : C;
+    const float4* src = x + size_t(b) * nc * HW4 + p;
+    uint4 w = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < (CT ? CT : 32); ++c) {
+        if (!CT && c >= nc) break;
+        const float4 v = __ldg(src + size_t(c) * HW4);
+        w.x |= uint32_t(v.x >= 0.0f) << c;
+        w.y |= uint32_t(v.y >= 0.0f) << c;
+        w.z |= uint32_t(v.z >= 0.0f) << c;
+        w.w |= uint32_t(v.w >= 0.0f) << c;
+    }
+    out[i] = w;
+}
+
 int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s) {
     const size_t total = B * HW;
     if (!total) return BNN_OK;
+    if (HW % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+        total / 4 < (size_t(1) << 31)) {
+        const unsigned t4 = unsigned(total / 4), hw4 = unsigned(HW / 4);
+        const unsigned grid = unsigned(ceil_div(size_t(t4), size_t(256)));
+        if (C == 3)
+            pack_pixels4_kernel<3><<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C, hw4, t4,
+                                                        reinterpret_cast<uint4*>(out));
+        else
+            pack_pixels4_kernel<0><<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(x), C, hw4, t4,
+                                                        reinterpret_cast<uint4*>(out));
+        return launch_check("pack_pixels4_kernel");
+    }
     const unsigned grid = unsigned(std::min<size_t>(ceil_div(total, 256), size_t(num_sms()) * 8));
     pack_pixels_kernel<<<grid, 256, 0, s>>>(x, C, HW, total, out);
     return launch_check("pack_pixels_kernel");

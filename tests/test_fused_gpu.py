@@ -40,6 +40,8 @@ FUSABLE = {
     # C = 256 / 512 fast path with pooling down to 1x1, then a single logits layer
     "wide": {"input_shape": [1, 3, 8, 8], "seed": 3,
              "layers": [conv(256)] + POOL + G + [conv(512)] + POOL + G + [conv(256)] + POOL + G + [lin(33)]},
+    # 4-channel pixel input (the vectorised pixel packer's generic-C path), 8 x 8
+    "pix4": {"input_shape": [1, 4, 8, 8], "seed": 17, "layers": [conv(32)] + G + [lin(10)]},
     # FP4 CTA pairs with partial channel pairs (384 = 1.5 pairs, 320: the odd CTA's channels
     # all past D), pooled and unpooled, position counts not a multiple of the 192-position tile
     "pairs": {"input_shape": [1, 3, 12, 12], "seed": 21,
