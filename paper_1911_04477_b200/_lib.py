@@ -108,6 +108,7 @@ _SIGS = {
     "bnn_debug_timeline": (_I, [_I]),
     "bnn_set_fused_swap": (_I, [_I]),
     "bnn_set_fused_small_logits": (_I, [_I]),
+    "bnn_set_fused_pix_popc": (_I, [_I]),
     "bnn_set_fused_fp4": (_I, [_I]),
     "bnn_set_fused_fp4_pair": (_I, [_I]),
     "bnn_float_gemm_f32": (_I, [_P, _SZ, _SZ, _P, _SZ, _P, _SZ, _P, _P]),

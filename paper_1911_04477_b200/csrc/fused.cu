@@ -45,6 +45,7 @@
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "bnn_common.cuh"
 #include "fused.cuh"
@@ -1679,6 +1680,96 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Pixel-input first conv with K = T*C <= 32 (the 3x3 RGB layer: K = 27) on the CUDA cores.
+// One patch is one word, so the layer is one XOR + POPC per (position, channel): 33.5 M popcounts
+// at batch 256, against a tensor-core launch that issues a single K=32 MMA per tile and is bound
+// by its epilogue and pixel gathers. With the patch x and channel d's weights w_d as K-bit words
+// (1 = +1; bits >= K are 0 in both), the reference's xnor value is a = K - 2 p, p = popc(x ^ w_d)
+// (kernels.hpp:46-54), and its float decision sign(htanh(fmaf(scale, float(a) + bias, shift)))
+// is (a >= T_d) ^ flip_d (prep_params_kernel). In the accumulator form a >= T_d <=> u >= Tu_d
+// with a = 2u - S_d, so a >= T_d <=> p <= (K + S_d)/2 - Tu_d = P_d (K + S_d = 2 * #(+1 weights)
+// is even): one compare per channel with no per-position term. A 2x2 max pool is the OR of the
+// four (a >= T_d) before the flip (network.cpp:133-149: max of the floats = float of the max
+// integer), i.e. min of the four popcounts <= P_d.
+// One thread per output (pooled) position; the patch is gathered tap-major / channel-minor (the
+// engine K order, weights_to_bits_kernel's bit order), out-of-image taps read +1 on every
+// channel (sign(0.0) of im2col's zero padding). The per-channel weights and thresholds are a
+// kernel parameter (PixParams): with the channel loops unrolled, every w_d / P_d is a
+// constant-bank operand of the XOR / compare, so a channel costs XOR, POPC, compare, select.
+template <int DW, bool F32, bool POOL>
+__global__ void __launch_bounds__(256, F32 ? 6 : 8) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
+    const uint32_t* pix = static_cast<const uint32_t*>(g.in);
+    const float* xf = static_cast<const float*>(g.in);
+    const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
+    const int PH2 = g.OH / 2, PW2 = g.OW / 2;
+    const int np = POOL ? g.B * PH2 * PW2 : g.B * g.OH * g.OW;  // output (pooled) positions
+    const size_t HW = size_t(g.H) * g.W;
+    constexpr int NS = POOL ? 4 : 1;
+    for (int p = int(blockIdx.x * blockDim.x + threadIdx.x); p < np; p += int(gridDim.x * blockDim.x)) {
+        uint32_t xs[NS];
+#pragma unroll
+        for (int sub = 0; sub < NS; ++sub) {
+            int b, oy, ox;
+            if (POOL) {  // pooled index ((b*OH/2 + py)*OW/2 + px), window element sub
+                const int t = g.dv0.div(p), px = p - t * PW2;
+                b = g.dv1.div(t);
+                oy = 2 * (t - b * PH2) + (sub >> 1), ox = 2 * px + (sub & 1);
+            } else {
+                b = g.dv0.div(p);
+                const int r = p - b * g.OH * g.OW;
+                oy = g.dv1.div(r), ox = r - oy * g.OW;
+            }
+            const int y0 = oy * g.SH - g.PH, x0 = ox * g.SW - g.PW;
+            uint32_t x = 0;
+            int sh = 0;
+            for (int kh = 0; kh < g.KH; ++kh) {
+                const int iy = y0 + kh;
+                const bool yin = unsigned(iy) < unsigned(g.H);
+                const size_t row = (size_t(b) * (F32 ? g.C : 1) * g.H + iy) * g.W;
+                for (int kw = 0; kw < g.KW; ++kw, sh += g.C) {
+                    const int ix = x0 + kw;
+                    uint32_t v = cmask;
+                    if (yin && unsigned(ix) < unsigned(g.W)) {
+                        if constexpr (F32) {  // bit c = (x[b, c, iy, ix] >= 0) (binarize.cpp:9)
+                            v = 0;
+                            for (int c = 0; c < g.C; ++c) v |= uint32_t(__ldg(xf + row + c * HW + ix) >= 0.0f) << c;
+                        } else {
+                            v = __ldg(pix + row + ix);
+                        }
+                    }
+                    x |= v << sh;
+                }
+            }
+            xs[sub] = x;
+        }
+        uint32_t o[DW];
+#pragma unroll
+        for (int w = 0; w < DW; ++w) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int d = 32 * w + j;
+                int c = __popc(xs[0] ^ pp.w[d]);
+                if (POOL) c = min(min(c, __popc(xs[1] ^ pp.w[d])), min(__popc(xs[2] ^ pp.w[d]), __popc(xs[3] ^ pp.w[d])));
+                acc |= c <= pp.p[d] ? (1u << j) : 0u;
+            }
+            o[w] = acc ^ pp.flip[w];
+        }
+        uint32_t* out = g.out_bits + size_t(p) * DW;
+        if constexpr (DW % 4 == 0) {
+#pragma unroll
+            for (int w = 0; w < DW; w += 4) *reinterpret_cast<uint4*>(out + w) = make_uint4(o[w], o[w + 1], o[w + 2], o[w + 3]);
+        } else if constexpr (DW % 2 == 0) {
+#pragma unroll
+            for (int w = 0; w < DW; w += 2) *reinterpret_cast<uint2*>(out + w) = make_uint2(o[w], o[w + 1]);
+        } else {
+#pragma unroll
+            for (int w = 0; w < DW; ++w) out[w] = o[w];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Tiny final layers (a handful of logits, e.g. 1024 -> 10): one CUDA-core thread per logit,
 // xnor-popcount over the packed input row, instead of a tensor-core launch whose fixed
 // pipeline latency (TMA, expansion, 8 dependent K blocks on 2 CTAs) dominates: the layer
@@ -2530,6 +2621,61 @@ int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s
     logits_popc_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(static_cast<const uint32_t*>(g.in), g.Cw, g.K, wbits,
                                                                  g.prm, g.D, g.rows, g.out_f32, g.ldo);
     return launch_check("logits_popc_kernel");
+}
+
+bool pix_popc_ok(const FusedGeom& g) { return g.K <= 32 && g.Dw >= 1 && g.Dw <= 8 && g.D == 32 * g.Dw; }
+
+// Grid: the resident CTA count (occupancy x SMs), positions strided over it, so every SM gets
+// the same share (262144 positions at B=256 are ~1.15 waves of 256-thread CTAs: a tail wave of
+// whole CTAs would leave most SMs idle).
+template <int DW, bool F32, bool POOL>
+static void launch_pix_k(const FusedGeom& g, const PixParams& pp, size_t np, cudaStream_t s) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pix_popc_kernel<DW, F32, POOL>, 256, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+    }
+    const unsigned grid = unsigned(std::min<size_t>(ceil_div(np, size_t(256)), size_t(num_sms()) * per_sm));
+    pix_popc_kernel<DW, F32, POOL><<<grid, 256, 0, s>>>(g, pp);
+}
+
+template <bool F32, bool POOL>
+static void launch_pix_dw(const FusedGeom& g, const PixParams& pp, size_t np, cudaStream_t s) {
+    switch (g.Dw) {
+#define BNN_PIX_CASE(n) \
+    case n: launch_pix_k<n, F32, POOL>(g, pp, np, s); break;
+        BNN_PIX_CASE(1) BNN_PIX_CASE(2) BNN_PIX_CASE(3) BNN_PIX_CASE(4)
+        BNN_PIX_CASE(5) BNN_PIX_CASE(6) BNN_PIX_CASE(7) BNN_PIX_CASE(8)
+#undef BNN_PIX_CASE
+    }
+}
+
+int make_pix_params(const uint32_t* wbits_host, const int4* prm_host, int D, int K, PixParams* pp) {
+    if (D > 256 || D % 32) return fail(BNN_E_CONFIG, "pix_popc: needs 32..256 output channels, a multiple of 32");
+    memset(pp, 0, sizeof *pp);
+    for (int d = 0; d < D; ++d) {
+        const int4 e = prm_host[d];  // (Tu, flip, S, bias bits)
+        pp->w[d] = wbits_host[d];
+        pp->p[d] = (K + e.z) / 2 - e.x;  // K + S is even
+        if (e.y) pp->flip[d / 32] |= 1u << (d % 32);
+    }
+    return BNN_OK;
+}
+
+int launch_pix_popc(const FusedGeom& g, const PixParams& pp, bool f32_in, cudaStream_t s) {
+    if (!pix_popc_ok(g)) return fail(BNN_E_CONFIG, "pix_popc: needs K <= 32 and 32..256 output channels");
+    const size_t np = g.pool ? size_t(g.B) * (g.OH / 2) * (g.OW / 2) : size_t(g.B) * g.OH * g.OW;
+    if (np == 0) return BNN_OK;
+    set_last_gemm("pix_popc");
+    if (f32_in) {
+        if (g.pool) launch_pix_dw<true, true>(g, pp, np, s);
+        else launch_pix_dw<true, false>(g, pp, np, s);
+    } else {
+        if (g.pool) launch_pix_dw<false, true>(g, pp, np, s);
+        else launch_pix_dw<false, false>(g, pp, np, s);
+    }
+    return launch_check("pix_popc_kernel");
 }
 
 int prep_weights4(const int8_t* w8, int Kpad, int K, int Dpad, int Kpad4, uint8_t* w4, cudaStream_t s) {

@@ -88,6 +88,19 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
 // Tiny final logits layer on the CUDA cores (logits_popc_kernel); wbits from prep_logit_bits.
 int prep_logit_bits(const int8_t* w8, int Kpad, int K, int D, int Kw, uint32_t* wbits, cudaStream_t s);
 int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s);
+// Pixel-input first conv with K <= 32 and 32..256 output channels on the CUDA cores
+// (pix_popc_kernel). PixParams (a kernel parameter: constant-bank operands): channel d's weight
+// bits in the engine K order (prep_logit_bits, one word per channel), its popcount threshold
+// P_d and the flip bits, from make_pix_params over host copies of wbits and the stage params.
+// f32_in: g.in is the float NCHW input (signs taken in the gather), else pack_pixels' words.
+struct PixParams {
+    uint32_t w[256];
+    int p[256];
+    uint32_t flip[8];
+};
+bool pix_popc_ok(const FusedGeom& g);
+int make_pix_params(const uint32_t* wbits_host, const int4* prm_host, int D, int K, PixParams* pp);
+int launch_pix_popc(const FusedGeom& g, const PixParams& pp, bool f32_in, cudaStream_t s);
 
 int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, int T, int perm_bits, int Dpad,
                        int Kpad, int8_t* out, cudaStream_t s);

@@ -95,6 +95,8 @@ struct FusedStage {
     int Dpad = 0, Kpad = 0;
     bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
     bool small_logits = false;   // tiny final layer: CUDA-core popcount kernel (wbits)
+    bool pix_popc = false;       // pixel-input first conv with K <= 32: CUDA-core kernel
+    PixParams pix{};             // its per-channel weight words, thresholds and flips
     const char* kname = "";      // kernel the last forward ran for this stage
     DevBuf w8, prm, wbits;
     DevBuf w4;                   // FP4 (e2m1) weights [Dpad, Kpad4 / 2] for the mxf4 swapped kernel
@@ -387,6 +389,17 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
             BNN_TRY(st->wbits.alloc(size_t(g.D) * g.Cw * sizeof(uint32_t)));
             BNN_TRY(prep_logit_bits(st->w8.as<int8_t>(), st->Kpad, g.K, g.D, g.Cw, st->wbits.as<uint32_t>(), s));
         }
+        if (st->in_mode == FIN_PIX && st->epi == FEPI_BITS && pix_popc_ok(g)) {
+            st->pix_popc = true;
+            BNN_TRY(st->wbits.alloc(size_t(g.D) * sizeof(uint32_t)));
+            BNN_TRY(prep_logit_bits(st->w8.as<int8_t>(), st->Kpad, g.K, g.D, 1, st->wbits.as<uint32_t>(), s));
+            std::vector<uint32_t> wb(g.D);
+            std::vector<int4> pr(g.D);
+            BNN_CUDA(cudaMemcpyAsync(wb.data(), st->wbits.p, wb.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+            BNN_CUDA(cudaMemcpyAsync(pr.data(), st->prm.p, pr.size() * sizeof(int4), cudaMemcpyDeviceToHost, s));
+            BNN_CUDA(cudaStreamSynchronize(s));
+            BNN_TRY(make_pix_params(wb.data(), pr.data(), g.D, g.K, &st->pix));
+        }
         if (st->epi == FEPI_BITS) {
             const size_t pos = kind == BNN_LAYER_CONV ? size_t(g.OH) * g.OW / (pool ? 4 : 1) : 1;
             st->out_words_per_image = pos * g.Dw;
@@ -667,6 +680,7 @@ int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
 // Forced tilings (bnn_set_fused_tiling) keep the position-major kernel.
 int g_swap = -1;
 int g_small_logits = 1;  // bnn_set_fused_small_logits: tiny final layers on the CUDA cores
+int g_pix_popc = -1;     // bnn_set_fused_pix_popc / BNN_PIX_POPC (default 2): K <= 32 pixel-input convs on the CUDA cores
 
 bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
     if (g_swap < 0) g_swap = getenv("BNN_FUSED_SWAP") ? atoi(getenv("BNN_FUSED_SWAP")) : 1;
@@ -776,7 +790,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         FusedStage& st = *net->stages[i];
         const FusedGeom& g = plans[i].g;
         EventPair layer_ev(net, st.layer, 0, s);
-        if (st.in_mode == FIN_PIX) {  // first-layer sign bits, one word per pixel
+        if (g_pix_popc < 0) g_pix_popc = getenv("BNN_PIX_POPC") ? atoi(getenv("BNN_PIX_POPC")) : 2;
+        // pix_popc 1: the CUDA-core first conv reads the float input itself (no pack_pixels);
+        // 2 (default): after pack_pixels (B=256: 1.71 M img/s vs 1.67 M, the 27 scattered float
+        // loads per position cost more than the packer's launch)
+        const bool pix_f32 = st.pix_popc && g_pix_popc == 1;
+        if (st.in_mode == FIN_PIX && !pix_f32) {  // first-layer sign bits, one word per pixel
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
             ++launches;
         }
@@ -785,8 +804,13 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             ++launches;
         }
         EventPair gemm_ev(net, st.layer, 1, s);
-        if (st.small_logits && g_small_logits)
+        if (st.small_logits && g_small_logits) {
             BNN_TRY(launch_logits_popc(g, st.wbits.as<uint32_t>(), s));
+        } else if (st.pix_popc && g_pix_popc) {
+            FusedGeom gp = g;
+            if (pix_f32) gp.in = x;
+            BNN_TRY(launch_pix_popc(gp, st.pix, pix_f32, s));
+        }
         else if (use_fp4(net, st, plans[i].cg))
             BNN_TRY(launch_swap4(st.in_mode, st.tm4, g, s));
         else if (use_swap(net, st, plans[i].cg))
@@ -1016,6 +1040,13 @@ const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer) {
 
 int bnn_set_fused_small_logits(int enabled) {
     g_small_logits = enabled ? 1 : 0;
+    ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_set_fused_pix_popc(int mode) {
+    if (mode < 0 || mode > 2) return fail(BNN_E_CONFIG, "fused pix_popc: 0 (off), 1 (float input) or 2 (packed pixels)");
+    g_pix_popc = mode;
     ++g_tiling_epoch;
     return BNN_OK;
 }

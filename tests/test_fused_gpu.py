@@ -46,6 +46,12 @@ FUSABLE = {
     # all past D), pooled and unpooled, position counts not a multiple of the 192-position tile
     "pairs": {"input_shape": [1, 3, 12, 12], "seed": 21,
               "layers": [conv(64)] + G + [conv(384)] + POOL + G + [conv(320)] + G + [lin(10)]},
+    # CUDA-core pixel conv (K <= 32): pooled first layer with 3 output words, stride 2 with 2
+    # words and a 2x2 kernel over 8 channels (K = 32: the full patch word), odd sizes
+    "pix_pool": {"input_shape": [1, 3, 10, 14], "seed": 23,
+                 "layers": [conv(96)] + POOL + G + [conv(64, 3, 2, 1)] + G + [lin(10)]},
+    "pix_s2": {"input_shape": [1, 3, 9, 7], "seed": 25, "layers": [conv(64, 3, 2, 1)] + G + [lin(10)]},
+    "pix_k32": {"input_shape": [1, 8, 7, 9], "seed": 27, "layers": [conv(256, 2, 1, 0)] + G + [lin(10)]},
     # linear-first stacks (BASELINE cfg1 / cfg4 shape class): K1 pack_rows of the float input,
     # linear -> linear with no glue (sign of float(a) + bias), a 4096-wide hidden layer
     "fc_stack": {"input_shape": [1, 288, 1, 1], "seed": 5, "layers": [lin(4096), lin(96), lin(10)]},
@@ -61,14 +67,17 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "nopixpopc", "pixf32", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
     swapped-operand conv kernels, A operand in TMEM and split-K for the small-batch linear
     layers), with the position-major conv kernel (noswap), with all stages chained in
     one persistent launch, with the A operand staged in shared memory, with each cta_group
-    forced, and with split-K off / forced to 16 (per-layer and chained)."""
+    forced, and with split-K off / forced to 16 (per-layer and chained). The CUDA-core first conv
+    (pix_popc) runs under "auto" (after the pixel packer) and "pixf32" (reading the float
+    input itself, no packer launch); the other settings put the
+    pixel-input layer on the tensor-core kernels they select."""
     lib = bnn.load()
     p = request.param
     bnn._lib.check(lib.bnn_set_fused_tiling({"cg1": 1, "cg2": 2}.get(p, 0), 0))
@@ -78,6 +87,7 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
     bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_small_logits(0 if p == "nosmall" else 1))
+    bnn._lib.check(lib.bnn_set_fused_pix_popc({"auto": 2, "pixf32": 1}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_fp4({"fp4": 1, "fp4all": 2, "nofp4": 0}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_fp4_pair({"nopair": 0, "pair224": 3}.get(p, 1)))
     yield p
@@ -87,6 +97,7 @@ def tiling(bnn, request):
     lib.bnn_set_fused_chain(0)
     lib.bnn_set_fused_swap(1)
     lib.bnn_set_fused_small_logits(1)
+    lib.bnn_set_fused_pix_popc(2)
     lib.bnn_set_fused_fp4(1)
     lib.bnn_set_fused_fp4_pair(1)
 
@@ -107,7 +118,8 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     x = orc.fill_random((batch, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     got = net.forward(x)
     # first-layer pixel encoder + one launch per weighted layer (10), or + one chained launch (2)
-    assert net.last_launches() == (2 if tiling in CHAINED else 10)
+    # pack_pixels + 9 weighted layers, or 9 when the CUDA-core first conv reads the floats itself
+    assert net.last_launches() == (2 if tiling in CHAINED else 9 if tiling == "pixf32" else 10)
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 
