@@ -1698,6 +1698,10 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
 // constant-bank operand of the XOR / compare, so a channel costs XOR, POPC, compare, select.
 template <int DW, bool F32, bool POOL>
 __global__ void __launch_bounds__(256, F32 ? 6 : 8) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
+    // PDL: the next layer may start its prologue (it waits for this grid before reading);
+    // this grid waits for the pixel packer's words
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t* pix = static_cast<const uint32_t*>(g.in);
     const float* xf = static_cast<const float*>(g.in);
     const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
@@ -2515,6 +2519,9 @@ int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int B
 template <int CT>
 __global__ void pack_pixels4_kernel(const float4* __restrict__ x, int C, unsigned HW4, unsigned total4,
                                     uint4* __restrict__ out) {
+    // PDL: a dependent first conv (pix_popc_kernel) may become resident now; it waits for this
+    // grid's completion before reading the words
+    asm volatile("griddepcontrol.launch_dependents;");
     const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total4) return;
     const unsigned b = i / HW4, p = i - b * HW4;
@@ -2636,8 +2643,16 @@ static void launch_pix_k(const FusedGeom& g, const PixParams& pp, size_t np, cud
             per_sm < 1)
             per_sm = 1;
     }
-    const unsigned grid = unsigned(std::min<size_t>(ceil_div(np, size_t(256)), size_t(num_sms()) * per_sm));
-    pix_popc_kernel<DW, F32, POOL><<<grid, 256, 0, s>>>(g, pp);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min<size_t>(ceil_div(np, size_t(256)), size_t(num_sms()) * per_sm)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, pix_popc_kernel<DW, F32, POOL>, g, pp);  // errors: launch_check
 }
 
 template <bool F32, bool POOL>
