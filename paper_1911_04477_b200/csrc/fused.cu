@@ -1781,6 +1781,8 @@ __global__ void __launch_bounds__(256, F32 ? 6 : 8) pix_popc_kernel(const FusedG
 // logit = float(a) + bias (kernels.cpp:90-107), written [D, ldo] (features x batch).
 __global__ void logits_popc_kernel(const uint32_t* __restrict__ act, int Kw, int K, const uint32_t* __restrict__ wbits,
                                    const int4* __restrict__ prm, int D, int B, float* __restrict__ out, int ldo) {
+    // PDL: resident while the previous layer drains (it triggers at entry); wait for its bits
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= D * B) return;
     const int d = i / B, b = i - d * B;  // consecutive threads: consecutive images (coalesced logits)
@@ -2625,8 +2627,17 @@ int launch_logits_popc(const FusedGeom& g, const uint32_t* wbits, cudaStream_t s
     const int n = g.D * g.rows;
     if (n == 0) return BNN_OK;
     set_last_gemm("logits_popc");
-    logits_popc_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(static_cast<const uint32_t*>(g.in), g.Cw, g.K, wbits,
-                                                                 g.prm, g.D, g.rows, g.out_f32, g.ldo);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((n + 127) / 128));
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, logits_popc_kernel, static_cast<const uint32_t*>(g.in), g.Cw, g.K, wbits, g.prm, g.D,
+                       g.rows, g.out_f32, g.ldo);  // errors: launch_check
     return launch_check("logits_popc_kernel");
 }
 
