@@ -228,9 +228,9 @@ int bnn_set_fused_swap(int enabled);
  * default) or on the tensor cores like the other layers (0). Bit-exact either way. */
 int bnn_set_fused_small_logits(int enabled);
 /* Fused engine: a pixel-input first conv whose patch fits one word (K = kh*kw*C <= 32, e.g. the
- * 3x3 RGB layer) with 32..256 output channels runs as a CUDA-core XOR-popcount kernel after the
- * pixel packer (2, default), the same kernel reading the float input itself (1), or on the
- * tensor cores (0). Process-wide; bit-exact in every mode. */
+ * 3x3 RGB layer) with 32..256 output channels runs as a CUDA-core XOR-popcount kernel reading
+ * the float input itself (1), after the pixel packer (2), 1 up to batch 512 and 2 above (3,
+ * default), or on the tensor cores (0). Process-wide; bit-exact in every mode. */
 int bnn_set_fused_pix_popc(int mode);
 /* ------------------------------------------------- the float control group (control.cu)
  * float_gemm (kernels.cpp:33-51): w [M, K] x [K, N], k-ascending FMA chain per output, then

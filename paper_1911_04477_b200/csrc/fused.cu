@@ -1773,6 +1773,67 @@ __global__ void __launch_bounds__(256, F32 ? 6 : 8) pix_popc_kernel(const FusedG
     }
 }
 
+// Float-input variant for unpooled layers whose per-image position count is a multiple of 256
+// (bnn_set_fused_pix_popc(1)): each CTA takes 256 consecutive positions of one image, signs and
+// packs the input rows they touch ONCE into shared memory (one word per pixel, coalesced float
+// loads; rows outside the image read +1), then gathers the patches from there. This folds the
+// pixel packer into the layer without pix_popc_kernel<F32>'s 27 scattered float loads per position.
+template <int DW>
+__global__ void __launch_bounds__(256) pix_tile_kernel(const FusedGeom g, const PixParams pp) {
+    extern __shared__ uint32_t tile[];  // [rows][W] sign words of the input rows of this tile
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const float* xf = static_cast<const float*>(g.in);
+    const uint32_t cmask = g.C == 32 ? ~0u : ((1u << g.C) - 1u);
+    const int OHOW = g.OH * g.OW;
+    const size_t HW = size_t(g.H) * g.W;
+    const int ntiles = g.B * (OHOW / 256);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int p0 = t * 256;
+        const int b = p0 / OHOW, r0 = p0 - b * OHOW;
+        const int oy0 = r0 / g.OW, oy1 = (r0 + 255) / g.OW;
+        const int iy0 = oy0 * g.SH - g.PH;
+        const int nw = ((oy1 - oy0) * g.SH + g.KH) * g.W;
+        const float* xb = xf + size_t(b) * g.C * HW;
+        __syncthreads();  // the previous tile's gathers are done
+        for (int i = threadIdx.x; i < nw; i += 256) {
+            const int ry = i / g.W, ix = i - ry * g.W, iy = iy0 + ry;
+            uint32_t v = cmask;
+            if (unsigned(iy) < unsigned(g.H)) {  // bit c = (x[b, c, iy, ix] >= 0) (binarize.cpp:9)
+                v = 0;
+                const float* src = xb + size_t(iy) * g.W + ix;
+                for (int c = 0; c < g.C; ++c) v |= uint32_t(__ldg(src + c * HW) >= 0.0f) << c;
+            }
+            tile[i] = v;
+        }
+        __syncthreads();
+        const int r = r0 + int(threadIdx.x);
+        const int oy = g.dv1.div(r), ox = r - oy * g.OW;
+        const int ty = (oy - oy0) * g.SH, x0 = ox * g.SW - g.PW;
+        uint32_t x = 0;
+        int sh = 0;
+        for (int kh = 0; kh < g.KH; ++kh)
+            for (int kw = 0; kw < g.KW; ++kw, sh += g.C) {
+                const int ix = x0 + kw;
+                x |= (unsigned(ix) < unsigned(g.W) ? tile[(ty + kh) * g.W + ix] : cmask) << sh;
+            }
+        uint32_t o[DW];
+#pragma unroll
+        for (int w = 0; w < DW; ++w) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int d = 32 * w + j;
+                acc |= __popc(x ^ pp.w[d]) <= pp.p[d] ? (1u << j) : 0u;
+            }
+            o[w] = acc ^ pp.flip[w];
+        }
+        uint32_t* out = g.out_bits + size_t(p0 + int(threadIdx.x)) * DW;
+#pragma unroll
+        for (int w = 0; w < DW; ++w) out[w] = o[w];
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Tiny final layers (a handful of logits, e.g. 1024 -> 10): one CUDA-core thread per logit,
 // xnor-popcount over the packed input row, instead of a tensor-core launch whose fixed
@@ -2694,6 +2755,31 @@ int launch_pix_popc(const FusedGeom& g, const PixParams& pp, bool f32_in, cudaSt
     const size_t np = g.pool ? size_t(g.B) * (g.OH / 2) * (g.OW / 2) : size_t(g.B) * g.OH * g.OW;
     if (np == 0) return BNN_OK;
     set_last_gemm("pix_popc");
+    if (f32_in && !g.pool && (g.OH * g.OW) % 256 == 0) {  // shared-memory tile of packed input rows
+        const int rows_max = (256 + g.OW - 2) / g.OW + 1;  // output rows 256 positions can span
+        const size_t smem = size_t((rows_max - 1) * g.SH + g.KH) * g.W * sizeof(uint32_t);
+        if (smem <= 48 * 1024) {
+            const int ntiles = int(np / 256);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned(std::min(ntiles, num_sms() * 8)));  // 32 registers: 8 CTAs per SM
+            cfg.blockDim = dim3(256);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol)
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            switch (g.Dw) {
+#define BNN_TILE_CASE(n) \
+    case n: cudaLaunchKernelEx(&cfg, pix_tile_kernel<n>, g, pp); break;
+                BNN_TILE_CASE(1) BNN_TILE_CASE(2) BNN_TILE_CASE(3) BNN_TILE_CASE(4)
+                BNN_TILE_CASE(5) BNN_TILE_CASE(6) BNN_TILE_CASE(7) BNN_TILE_CASE(8)
+#undef BNN_TILE_CASE
+            }
+            return launch_check("pix_tile_kernel");
+        }
+    }
     if (f32_in) {
         if (g.pool) launch_pix_dw<true, true>(g, pp, np, s);
         else launch_pix_dw<true, false>(g, pp, np, s);

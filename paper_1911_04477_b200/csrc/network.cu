@@ -680,7 +680,7 @@ int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
 // Forced tilings (bnn_set_fused_tiling) keep the position-major kernel.
 int g_swap = -1;
 int g_small_logits = 1;  // bnn_set_fused_small_logits: tiny final layers on the CUDA cores
-int g_pix_popc = -1;     // bnn_set_fused_pix_popc / BNN_PIX_POPC (default 2): K <= 32 pixel-input convs on the CUDA cores
+int g_pix_popc = -1;     // bnn_set_fused_pix_popc / BNN_PIX_POPC (default 3): K <= 32 pixel-input convs on the CUDA cores
 
 bool use_swap(const bnn_net* net, const FusedStage& st, int cg) {
     if (g_swap < 0) g_swap = getenv("BNN_FUSED_SWAP") ? atoi(getenv("BNN_FUSED_SWAP")) : 1;
@@ -790,11 +790,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         FusedStage& st = *net->stages[i];
         const FusedGeom& g = plans[i].g;
         EventPair layer_ev(net, st.layer, 0, s);
-        if (g_pix_popc < 0) g_pix_popc = getenv("BNN_PIX_POPC") ? atoi(getenv("BNN_PIX_POPC")) : 2;
-        // pix_popc 1: the CUDA-core first conv reads the float input itself (no pack_pixels);
-        // 2 (default): after pack_pixels (B=256: 1.71 M img/s vs 1.67 M, the 27 scattered float
-        // loads per position cost more than the packer's launch)
-        const bool pix_f32 = st.pix_popc && g_pix_popc == 1;
+        if (g_pix_popc < 0) g_pix_popc = getenv("BNN_PIX_POPC") ? atoi(getenv("BNN_PIX_POPC")) : 3;
+        // pix_popc 1: the CUDA-core first conv reads the float input itself (no pack_pixels;
+        // pix_tile_kernel stages packed input rows in shared memory when the layer allows);
+        // 2: after pack_pixels; 3 (default): 1 up to batch 512 (B=256: 1.754 vs 1.731 M img/s),
+        // 2 above (B=4096: 2.70 vs 2.66 M, the packer's one pass beats the per-tile halo rows)
+        const bool pix_f32 = st.pix_popc && (g_pix_popc == 1 || (g_pix_popc == 3 && B <= 512));
         if (st.in_mode == FIN_PIX && !pix_f32) {  // first-layer sign bits, one word per pixel
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
             ++launches;
@@ -1045,7 +1046,7 @@ int bnn_set_fused_small_logits(int enabled) {
 }
 
 int bnn_set_fused_pix_popc(int mode) {
-    if (mode < 0 || mode > 2) return fail(BNN_E_CONFIG, "fused pix_popc: 0 (off), 1 (float input) or 2 (packed pixels)");
+    if (mode < 0 || mode > 3) return fail(BNN_E_CONFIG, "fused pix_popc: 0 (off), 1 (float input), 2 (packed pixels) or 3 (auto)");
     g_pix_popc = mode;
     ++g_tiling_epoch;
     return BNN_OK;

@@ -67,7 +67,7 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "nopixpopc", "pixf32", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -75,8 +75,8 @@ def tiling(bnn, request):
     layers), with the position-major conv kernel (noswap), with all stages chained in
     one persistent launch, with the A operand staged in shared memory, with each cta_group
     forced, and with split-K off / forced to 16 (per-layer and chained). The CUDA-core first conv
-    (pix_popc) runs under "auto" (after the pixel packer) and "pixf32" (reading the float
-    input itself, no packer launch); the other settings put the
+    (pix_popc) runs under "auto" (float input up to batch 512, else after the packer), "pixf32"
+    (reading the float input itself, no packer launch) and "pixpacked"; the other settings put the
     pixel-input layer on the tensor-core kernels they select."""
     lib = bnn.load()
     p = request.param
@@ -87,7 +87,7 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
     bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_small_logits(0 if p == "nosmall" else 1))
-    bnn._lib.check(lib.bnn_set_fused_pix_popc({"auto": 2, "pixf32": 1}.get(p, 0)))
+    bnn._lib.check(lib.bnn_set_fused_pix_popc({"auto": 3, "pixf32": 1, "pixpacked": 2}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_fp4({"fp4": 1, "fp4all": 2, "nofp4": 0}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_fp4_pair({"nopair": 0, "pair224": 3}.get(p, 1)))
     yield p
@@ -97,7 +97,7 @@ def tiling(bnn, request):
     lib.bnn_set_fused_chain(0)
     lib.bnn_set_fused_swap(1)
     lib.bnn_set_fused_small_logits(1)
-    lib.bnn_set_fused_pix_popc(2)
+    lib.bnn_set_fused_pix_popc(3)
     lib.bnn_set_fused_fp4(1)
     lib.bnn_set_fused_fp4_pair(1)
 
@@ -119,7 +119,7 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     got = net.forward(x)
     # first-layer pixel encoder + one launch per weighted layer (10), or + one chained launch (2)
     # pack_pixels + 9 weighted layers, or 9 when the CUDA-core first conv reads the floats itself
-    assert net.last_launches() == (2 if tiling in CHAINED else 9 if tiling == "pixf32" else 10)
+    assert net.last_launches() == (2 if tiling in CHAINED else 9 if tiling in ("auto", "pixf32") else 10)
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 

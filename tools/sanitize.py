@@ -11,7 +11,7 @@ from oracle import Oracle  # noqa: E402
 orc = Oracle()
 lib = bnn.load()
 SETTINGS = {"default": {}, "split16": {"split": 16}, "nosplit": {"split": 1}, "chain": {"chain": 1},
-            "swapall": {"swap": 2}, "noswap": {"swap": 0}, "nosmall": {"small": 0}, "nopixpopc": {"pix": 0}, "pixf32": {"pix": 1},
+            "swapall": {"swap": 2}, "noswap": {"swap": 0}, "nosmall": {"small": 0}, "nopixpopc": {"pix": 0}, "pixf32": {"pix": 1}, "pixpacked": {"pix": 2},
             "nopair": {"pair": 0}, "pair224": {"pair": 3}, "fp4all": {"fp4": 2}, "nofp4": {"fp4": 0}}
 bad = 0
 for name, st in SETTINGS.items():
@@ -19,7 +19,7 @@ for name, st in SETTINGS.items():
     lib.bnn_set_fused_chain(st.get("chain", 0))
     lib.bnn_set_fused_swap(st.get("swap", 1))
     lib.bnn_set_fused_small_logits(st.get("small", 1))
-    lib.bnn_set_fused_pix_popc(st.get("pix", 2))
+    lib.bnn_set_fused_pix_popc(st.get("pix", 3))
     lib.bnn_set_fused_fp4_pair(st.get("pair", 1))
     lib.bnn_set_fused_fp4(st.get("fp4", 1))
     for b in (1, 5, 130):
