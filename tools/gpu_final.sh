@@ -6,6 +6,6 @@ timeout 1200 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider 
 timeout 120 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fused|pack_pixels|logits|pix_popc" -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-sweep --no-configs > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fused|pix_popc" -c 9 -o gpurun_out/prof_b256 -f python tools/prof_net.py 256 > gpurun_out/prof.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fused|pack_pixels|logits|pix_" -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-sweep --no-configs > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fused|pix_" -c 9 -o gpurun_out/prof_b256 -f python tools/prof_net.py 256 > gpurun_out/prof.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/prof.log
