@@ -9,20 +9,26 @@
 // (host buffers in and out, synchronous). There is no CPU fallback: without a B200 every
 // compute call throws bnn::CudaError.
 //
-// Scope: encode (sign, htanh, pack_rows, pack_cols, unpack), lowering
-// (binary im2col, flatten_weights, reshape_output), the xnor GEMM and its epilogue (xnor_gemm,
-// to_float, bias_add), the two layer forwards, the network glue, and the seeded generator.
-// Out of scope: the float control-group path (float_gemm,
-// conv_forward_float, KernelChoice::Float), naive_conv, col2im, blob and JSON I/O, the CLI.
+// Scope: the reference's tensor.hpp, binarize.hpp, lowering.hpp, kernels.hpp, network.hpp and
+// bench.hpp declarations: encode, lowering (im2col, col2im,
+// reshape_output, flatten_weights), the xnor GEMM and its epilogue, the float control group
+// (float_gemm, conv_forward_float), the BinaryReference and naive forwards, the network
+// (build_network, network_forward with ExecKernel / ForwardOptions, the JSON spec), the
+// bench/verify harness (run_benchmark, run_verify, verify_network, the report JSON) and the
+// blob formats. Additions beyond the reference are marked "B200:". Not provided: the bnnbench
+// CLI (out of scope).
 #pragma once
 
 #include <array>
+#include <bit>
 #include <cstddef>
 #include <cstdint>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <iosfwd>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -136,12 +142,32 @@ PackedBitMatrix sign_pack_rows(const FloatMatrix& w);
 PackedBitMatrix sign_pack_cols(const FloatMatrix& x);
 
 // ---------------------------------------------------------------- lowering (lowering.hpp)
-// pack_cols(sign(im2col(x, batch_index, geom))) without the float patch matrix.
+// [K*K*C, outH*outW] float patch matrix of one batch slice (lowering.hpp:11), on the device.
+FloatMatrix im2col(const FloatTensor& x, std::size_t batch_index, const ConvGeometry& geom);
+// Adjoint of im2col (lowering.hpp:17-18), on the device, bit-identical sums.
+FloatTensor col2im(const FloatMatrix& m, const ConvGeometry& geom, std::size_t out_h, std::size_t out_w);
+// B200: pack_cols(sign(im2col(x, batch_index, geom))) without the float patch matrix.
 PackedBitMatrix im2col_sign_pack(const FloatTensor& x, std::size_t batch_index, const ConvGeometry& geom);
 FloatTensor reshape_output(const FloatMatrix& m, std::size_t out_h, std::size_t out_w);
 FloatMatrix flatten_weights(const FloatTensor& w);
 
 // ---------------------------------------------------------------- GEMM (kernels.hpp)
+// Word primitives (kernels.hpp:25-39): host inline like the reference's; the device kernels use
+// the POPC / LOP3 instructions and the tensor cores instead.
+constexpr int popcount32_portable(std::uint32_t x) noexcept {
+    x = x - ((x >> 1) & 0x55555555u);
+    x = (x & 0x33333333u) + ((x >> 2) & 0x33333333u);
+    x = (x + (x >> 4)) & 0x0F0F0F0Fu;
+    return static_cast<int>((x * 0x01010101u) >> 24);
+}
+inline int popcount32(std::uint32_t x) noexcept { return std::popcount(x); }
+inline int word_dot(std::uint32_t w, std::uint32_t x) noexcept { return 2 * popcount32(~(w ^ x)) - 32; }
+
+// Control-group float GEMM (kernels.hpp:44), on the CUDA cores with the reference's k-ascending
+// FMA chain per output: bit-identical. `threads` is accepted for source compatibility.
+FloatMatrix float_gemm(const FloatMatrix& w, const FloatMatrix& x, unsigned threads = 1);
+// Direct convolution of one batch slice (kernels.hpp:63-64), bit-identical.
+FloatTensor naive_conv(const FloatTensor& x, std::size_t batch_index, const FloatTensor& w, const ConvGeometry& geom);
 // `threads` is accepted for source compatibility; the device grid replaces it.
 IntMatrix xnor_gemm(const PackedBitMatrix& w, const PackedBitMatrix& x, std::size_t inner_len,
                     unsigned threads = 1);
@@ -152,13 +178,25 @@ FloatMatrix bias_add(FloatMatrix a, std::span<const float> bias);
 enum class LayerKind { Conv, Linear, MaxPool, AffineNorm, SignAct, HtanhAct };
 enum class KernelChoice { Float, Binary, Naive };
 
+const char* to_string(LayerKind k);
+const char* to_string(KernelChoice k);
+LayerKind parse_layer_kind(const std::string& s);
+KernelChoice parse_kernel_choice(const std::string& s);
+
+FloatTensor conv_forward_float(const FloatTensor& x, const FloatMatrix& w_flat, std::span<const float> bias,
+                               const ConvGeometry& geom, unsigned threads = 1);
 FloatTensor conv_forward_binary(const FloatTensor& x, const PackedBitMatrix& packed_w,
                                 std::span<const float> bias, const ConvGeometry& geom, unsigned threads = 1);
-// Only KernelChoice::Binary is on the device path; Float/Naive throw ConfigError.
+FloatTensor conv_forward_binary_reference(const FloatTensor& x, const FloatMatrix& w_pm1, std::span<const float> bias,
+                                          const ConvGeometry& geom, unsigned threads = 1);
+FloatTensor conv_forward_naive(const FloatTensor& x, const FloatTensor& w, std::span<const float> bias,
+                               const ConvGeometry& geom);
 FloatMatrix linear_forward(const FloatMatrix& x, const FloatMatrix& w, std::span<const float> bias,
                            KernelChoice kernel, unsigned threads = 1);
 FloatMatrix linear_forward_packed(const FloatMatrix& x, const PackedBitMatrix& packed_w,
                                   std::span<const float> bias, unsigned threads = 1);
+FloatMatrix linear_forward_binary_reference(const FloatMatrix& x, const FloatMatrix& w_pm1,
+                                            std::span<const float> bias, unsigned threads = 1);
 FloatTensor maxpool2(const FloatTensor& x);
 FloatTensor affine_norm(FloatTensor x, std::span<const float> scale, std::span<const float> shift);
 FloatMatrix affine_norm(FloatMatrix x, std::span<const float> scale, std::span<const float> shift);
@@ -175,6 +213,7 @@ struct LayerSpec {
     KernelChoice kernel = KernelChoice::Float;
     std::optional<std::uint64_t> seed;
     std::string weights_blob;  // tensor blob path; empty -> seeded weights (network.hpp:36)
+    bool operator==(const LayerSpec&) const = default;
 };
 
 struct NetworkSpec {
@@ -183,22 +222,74 @@ struct NetworkSpec {
     std::uint64_t seed = 1;
     bool binarize_weights = false;
     std::vector<LayerSpec> layers;
+    bool operator==(const NetworkSpec&) const = default;
 };
+
+// A layer with resolved shapes and its parameters (network.hpp:57-77). The host copies mirror
+// the device engine's; network_forward re-uploads any the caller changed.
+struct BuiltLayer {
+    LayerSpec spec;
+    ConvGeometry geom;
+    std::size_t in_features = 0, out_features = 0;
+    FloatTensor weight_tensor;       // conv, [D, C, kH, kW]
+    FloatMatrix weights;             // conv [D, K2C] / linear [out, in]
+    PackedBitMatrix packed_weights;  // row-packed sign(weights)
+    std::vector<float> bias;
+    std::vector<float> scale, shift;
+    std::size_t out_channels = 0, out_h = 0, out_w = 0;
+    bool out_flat = false;
+    bool has_weights() const { return spec.kind == LayerKind::Conv || spec.kind == LayerKind::Linear; }
+    std::size_t float_weight_bytes() const { return weights.data.size() * sizeof(float); }
+    std::size_t packed_weight_bytes() const { return packed_weights.byte_size(); }
+};
+
+namespace detail {
+struct DeviceEngine;  // the device network (bnn_net) + the parameter snapshot it was built from
+}
+
+struct Network {
+    NetworkSpec spec;
+    std::vector<BuiltLayer> layers;
+    std::size_t in_channels = 0, in_h = 0, in_w = 0;
+    std::size_t logits = 0;
+    std::size_t parameter_count = 0;
+    // B200: the device engine build_network created (parameters generated and packed on the
+    // device once). Copies of a Network share it.
+    std::shared_ptr<detail::DeviceEngine> device;
+};
+
+// Validate the shape chain and materialize the parameters (network.cpp:203-306), on the device.
+Network build_network(const NetworkSpec& spec);
+
+enum class ExecKernel { PerLayer, Float, Binary, Naive, BinaryReference };
+
+struct ForwardOptions {
+    ExecKernel kernel = ExecKernel::PerLayer;
+    unsigned threads = 1;                          // accepted; the device grid replaces it
+    std::vector<double>* layer_seconds = nullptr;  // per-layer device time (CUDA events), accumulated
+};
+
+// network_forward (network.hpp:104-105): [batch, C, H, W] -> logits [features, batch].
+// ExecKernel::Binary (and PerLayer over an all-Binary network) runs the fused tcgen05 engine;
+// the others run their layer-by-layer device graphs. Bit-identical to the reference for every
+// ExecKernel. layer_seconds: the fused engine folds each weighted layer's glue into its launch,
+// so the glue layers' entries stay 0.
+FloatMatrix network_forward(const Network& net, const FloatTensor& x, const ForwardOptions& opts = {});
 
 // The reference's VGG-small benchmark topology (network.cpp:422-465).
 NetworkSpec build_default_network(KernelChoice kernel, std::uint64_t seed);
+NetworkSpec load_network_spec(const std::string& path);
+void save_network_spec(const NetworkSpec& spec, const std::string& path);
 
-// build_network + network_forward(ExecKernel::Binary) on the current device: parameters are
-// generated from the spec's seeds and packed once at construction (network.cpp:203-306).
+// B200: the device network as an owning handle (build_network + network_forward(Binary)), for
+// callers that keep one network resident; Network above is the reference-shaped entry point.
 class DeviceNetwork {
 public:
     explicit DeviceNetwork(const NetworkSpec& spec);
-    // load_network_spec (network.cpp:487-536) + build_network: a NetworkSpec JSON file.
     static DeviceNetwork from_spec_file(const std::string& path);
     ~DeviceNetwork();
     DeviceNetwork(const DeviceNetwork&) = delete;
     DeviceNetwork& operator=(const DeviceNetwork&) = delete;
-    // [batch, C, H, W] -> logits [features, batch] (network.hpp:104-105).
     FloatMatrix forward(const FloatTensor& x);
     std::size_t logits() const;
     bnn_net* handle() const { return net_; }
@@ -221,8 +312,80 @@ FloatTensor load_tensor_blob(const std::string& path);
 
 FloatMatrix network_forward(DeviceNetwork& net, const FloatTensor& x);
 
-// FNV-1a over the float bytes (bench.cpp:23-33): cheap whole-output bit-exactness checks.
+// ---------------------------------------------------------------- harness (bench.hpp)
+constexpr double kVerifyTolerance = 1e-4;
+
+struct BenchConfig {
+    std::string spec_path;  // empty: built-in default network
+    std::vector<KernelChoice> kernels{KernelChoice::Binary, KernelChoice::Float};
+    std::size_t batch = 64;
+    std::size_t iterations = 20;
+    std::size_t warmup = 3;
+    unsigned threads = 1;
+    std::uint64_t seed = 1;
+    std::string out_path;
+    std::string input_blob;
+    bool layer_times = true;
+};
+
+struct KernelStats {
+    KernelChoice kernel = KernelChoice::Binary;
+    std::vector<double> samples_s;  // wall-clock seconds per timed network_forward
+    double median_s = 0, min_s = 0, mean_s = 0;
+    std::vector<double> layer_seconds;
+    std::uint64_t logits_hash = 0;
+};
+
+struct SpeedupEntry {
+    std::string baseline;
+    std::string target;
+    double ratio = 0;
+};
+
+struct LayerMemory {
+    std::size_t layer_index = 0;
+    std::string label;
+    std::size_t float_bytes = 0;
+    std::size_t packed_bytes = 0;
+};
+
+struct BenchReport {
+    std::string network_name;
+    std::string spec_path;
+    std::size_t batch = 0, iterations = 0, warmup = 0;
+    unsigned threads = 1;
+    std::uint64_t seed = 0;
+    std::string environment;
+    double timer_resolution_ns = 0;
+    std::vector<KernelStats> kernels;
+    std::vector<LayerMemory> weight_memory;
+    std::size_t total_float_bytes = 0, total_packed_bytes = 0;
+    std::vector<SpeedupEntry> speedups;
+};
+
+struct VerifySummary {
+    std::string network_name;
+    std::size_t batch = 0;
+    std::size_t compared = 0;
+    double max_abs_deviation = 0;
+    double tolerance = kVerifyTolerance;
+    bool pass = false;
+    bool pad_correction_exercised = false;
+};
+
+double median(std::vector<double> samples);
+// FNV-1a over the float bytes (bench.cpp:23-33).
+std::uint64_t fnv1a_hash(const FloatMatrix& m);
+// B200: the same hash of any float span.
 std::uint64_t fnv1a_hash(std::span<const float> values);
+BenchReport run_benchmark(const BenchConfig& cfg);
+VerifySummary run_verify(const BenchConfig& cfg);
+// Binary vs BinaryReference on the device (bench.cpp:172-191); the max deviation is reduced on
+// the device. Callers may perturb net.layers[i] first (test hook, test_bench.cpp:159-173).
+VerifySummary verify_network(const Network& net, const FloatTensor& input, unsigned threads = 1);
+void emit_report(const BenchReport& r, const std::string& path);
+BenchReport parse_report(const std::string& path);
+void print_report(const BenchReport& r, std::ostream& os);
 
 }  // namespace bnn
 

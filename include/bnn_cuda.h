@@ -147,6 +147,9 @@ int bnn_fill_random_f32(uint64_t seed, uint64_t offset, size_t n, float* out, bn
 uint64_t bnn_mix64(uint64_t seed, uint64_t counter); /* tensor.cpp:65-71 (host) */
 /* fnv1a_hash (bench.cpp:23-33) of a device float buffer; synchronous. */
 int bnn_fnv1a_f32(const float* x, size_t n, uint64_t* hash, bnn_stream_t s);
+/* max_i |a[i] - b[i]| of two device arrays (verify_network's deviation, bench.cpp:178-181),
+ * computed on the device; synchronous. */
+int bnn_max_abs_diff_f32(const float* a, const float* b, size_t n, double* out, bnn_stream_t s);
 
 /* ------------------------------------------------------------- network engine
  * build_network + network_forward, ExecKernel::Binary (network.cpp:203-420). Weights are
@@ -155,13 +158,18 @@ int bnn_fnv1a_f32(const float* x, size_t n, uint64_t* hash, bnn_stream_t s);
 enum { BNN_LAYER_CONV = 0, BNN_LAYER_LINEAR = 1, BNN_LAYER_MAXPOOL = 2, BNN_LAYER_AFFINE = 3,
        BNN_LAYER_SIGN = 4, BNN_LAYER_HTANH = 5 }; /* LayerKind order, network.hpp:15 */
 
-typedef struct { /* LayerSpec (network.hpp:23-39), binary kernel */
+/* KernelChoice (network.hpp:16), a weighted layer's own kernel under BNN_ENGINE_PER_LAYER */
+enum { BNN_KERNEL_FLOAT = 0, BNN_KERNEL_BINARY = 1, BNN_KERNEL_NAIVE = 2 };
+
+typedef struct { /* LayerSpec (network.hpp:23-39) */
     uint32_t kind;
     uint32_t has_seed;
     uint64_t seed;
     uint64_t out_channels, kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w;
     uint64_t out_features;
     const char* weights_blob; /* tensor blob path of the float weights; NULL -> seeded weights */
+    uint32_t kernel;          /* BNN_KERNEL_* (LayerSpec::kernel) */
+    uint32_t reserved;
 } bnn_layer_spec;
 
 typedef struct bnn_net bnn_net;
@@ -179,6 +187,17 @@ size_t bnn_net_num_layers(const bnn_net* net);
  * bias / affine parameters to host buffers (NULL to skip). */
 int bnn_net_layer_params(const bnn_net* net, size_t i, uint32_t* packed, size_t* rows,
                          size_t* cols, float* bias, float* scale, float* shift);
+/* BuiltLayer's parameters (network.hpp:57-77) to / from host buffers, NULL to skip: packed
+ * [rows, ceil(cols/32)] words, float weights [rows, cols] (after binarize_weights), bias
+ * [rows], affine scale / shift [channels]. Setting replaces the device copies the engines
+ * use (Binary / fused: packed, bias, scale, shift; Float / BinaryReference / Naive: weights,
+ * bias, scale, shift) and re-prepares the fused engine, as if the network had been built
+ * with them -- the reference's test hook of perturbing net.layers[i] (test_bench.cpp:159-173).
+ * Synchronous. */
+int bnn_net_layer_data(const bnn_net* net, size_t i, uint32_t* packed, float* weights, float* bias,
+                       float* scale, float* shift);
+int bnn_net_set_layer_data(bnn_net* net, size_t i, const uint32_t* packed, const float* weights,
+                           const float* bias, const float* scale, const float* shift);
 /* network_forward (network.cpp:330-420): x device [B, C, H, W] -> logits device
  * [features, B] (the reference layout, network.hpp:104-105). Stream-ordered. */
 int bnn_net_forward(bnn_net* net, const float* x, size_t batch, float* logits, bnn_stream_t s);
@@ -201,8 +220,17 @@ int bnn_net_layer_shape(const bnn_net* net, size_t i, size_t out[8]);
 /* BNN_ENGINE_FLOAT: the paper's float control group (ExecKernel::Float: conv_forward_float /
  * linear_forward Float on the float weights, control.cu), bit-exact with the reference's
  * FMA-contracted float_gemm. */
-enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2, BNN_ENGINE_FLOAT = 3 };
+/* BNN_ENGINE_BINARY_REFERENCE: ExecKernel::BinaryReference, the graph verify_network checks the
+ * xnor path against (sign(im2col) / sign(x) then float_gemm on sign(weights), network.cpp:81-94,
+ * 128-131). BNN_ENGINE_NAIVE: ExecKernel::Naive (direct convolution, network.cpp:96-111; linear
+ * layers as Float). BNN_ENGINE_PER_LAYER: ExecKernel::PerLayer, each weighted layer runs its
+ * spec's KernelChoice (bnn_layer_spec.kernel); all-Binary networks use the fused engine. All of
+ * them are bit-exact with the reference's network_forward under the same ExecKernel. */
+enum { BNN_ENGINE_AUTO = 0, BNN_ENGINE_GENERIC = 1, BNN_ENGINE_FUSED = 2, BNN_ENGINE_FLOAT = 3,
+       BNN_ENGINE_BINARY_REFERENCE = 4, BNN_ENGINE_NAIVE = 5, BNN_ENGINE_PER_LAYER = 6 };
 int bnn_net_set_engine(bnn_net* net, int policy);
+/* Layer i's KernelChoice (BNN_KERNEL_*) for BNN_ENGINE_PER_LAYER (LayerSpec::kernel). */
+int bnn_net_set_layer_kernel(bnn_net* net, size_t i, int kernel);
 /* Fused-engine tile shape override, process-wide (tests / experiments): cta_group 1 (M=128
  * per CTA) or 2 (CTA pairs, M=256, tcgen05 cta_group::2), bn = MMA N in {32,64,128,256};
  * 0 = automatic (the default). */
@@ -237,6 +265,18 @@ int bnn_set_fused_pix_popc(int mode);
  * + bias (may be NULL) with the reshape epilogue of bnn_xnor_gemm_bias_f32 (P = 0: P = N). */
 int bnn_float_gemm_f32(const float* w, size_t M, size_t K, const float* x, size_t N, const float* bias,
                        size_t P, float* out, bnn_stream_t s);
+/* im2col (lowering.cpp:7-43, float, zero padding) of batch slices [b0, b0 + nb): cols
+ * [C*kH*kW, nb*oh*ow]; nb = 1 is the reference's im2col(x, b0, geom). */
+int bnn_im2col_f32(const float* x, size_t B, size_t C, size_t H, size_t W, size_t b0, size_t nb,
+                   const bnn_conv_geom* g, float* cols, bnn_stream_t s);
+/* col2im (lowering.cpp:45-84), the adjoint: m [C*kH*kW, oh*ow] -> x [1, C, in_h, in_w], with
+ * the input extents recovered from the geometry (returned in *in_h / *in_w; x == NULL queries
+ * them only). Bit-identical (same additions in the same order). */
+int bnn_col2im_f32(const float* m, size_t rows, size_t cols, const bnn_conv_geom* g, size_t oh, size_t ow,
+                   float* x, size_t* in_h, size_t* in_w, bnn_stream_t s);
+/* conv_forward_naive (network.cpp:96-111, naive_conv kernels.cpp:109-147): w [D, C, kH, kW]. */
+int bnn_conv_forward_naive_f32(const float* x, size_t B, size_t C, size_t H, size_t W, const float* w,
+                               const float* bias, const bnn_conv_geom* g, float* out, bnn_stream_t s);
 /* conv_forward_float (network.cpp:50-63). */
 int bnn_conv_forward_float_f32(const float* x, size_t B, size_t C, size_t H, size_t W, const float* w_flat,
                                const float* bias, const bnn_conv_geom* g, float* out, bnn_stream_t s);
@@ -257,6 +297,18 @@ int bnn_load_tensor_blob(const char* path, uint64_t shape[4], float* data, size_
 int bnn_net_create_from_spec(const char* path, int binarize_override, bnn_net** out);
 int bnn_spec_info(const char* path, uint64_t input_shape[4], size_t* n_layers);
 
+/* ------------------------------------------------------ bench / verify harness (bench.cpp)
+ * run_verify (bench.cpp:193-199): the default network (spec_path NULL) or a NetworkSpec file
+ * with binarize_weights forced on, input from input_blob or fill_random(batch, ...,
+ * mix64(seed, "input")); Binary vs BinaryReference on the device.
+ * run_benchmark (bench.cpp:102-170) + emit_report (bench.cpp:219-257): kernels_mask bit 0
+ * Binary, bit 1 Float, bit 2 Naive (in that order); the report JSON is written to out_path in
+ * the reference's schema. */
+int bnn_run_verify(const char* spec_path, size_t batch, uint64_t seed, const char* input_blob, double* max_dev,
+                   size_t* compared, int* pass, int* pad_exercised);
+int bnn_run_benchmark(const char* spec_path, size_t batch, size_t iterations, size_t warmup, uint64_t seed,
+                      int kernels_mask, int layer_times, const char* out_path);
+
 /* Kernel the last fused forward ran for weighted layer `layer` ("" if none / not fused). */
 const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer);
 /* Fused engine: FP4 operands (kind::mxf4 block-scaled e2m1, exact for +-1 x {0,1}) in the
@@ -271,7 +323,8 @@ int bnn_set_fused_fp4_pair(int mode);
 /* Debug timeline of the fused engine's launches (globaltimer stamps per CTA; stderr):
  * op 1 = start recording, op 2 = print the recorded launches and stop. */
 int bnn_debug_timeline(int op);
-/* Engine the next bnn_net_forward uses (GENERIC or FUSED). */
+/* Engine the next bnn_net_forward uses (FUSED, GENERIC, FLOAT, BINARY_REFERENCE, NAIVE or
+ * PER_LAYER when that mixes kernels). */
 int bnn_net_engine(const bnn_net* net);
 /* Number of kernels the last bnn_net_forward enqueued (the benchmark's gpu_launches). */
 size_t bnn_net_last_launches(const bnn_net* net);
@@ -285,6 +338,10 @@ size_t bnn_net_device_bytes(const bnn_net* net);
  *   bmma: mma.sync m16n8k256 b1 xor.popc (candidate B; software-emulated on sm_100a) */
 int bnn_probe_popc_peak(double* bops_per_s, double* ms, bnn_stream_t s);
 int bnn_probe_bmma_peak(double* bops_per_s, double* ms, bnn_stream_t s);
+/*   umma: tcgen05.mma dispatch rate (candidate C), kind 0 = kind::i8 (+-1 bytes), 1 = kind::mxf4
+ *         (block-scaled e2m1, the fused conv kernels' operands), M = 128, N in [64, 256]; ops = 2
+ *         per MAC; *cycles_per_mma = cycles per instruction on one SM. */
+int bnn_probe_umma_peak(int kind, int N, double* ops_per_s, double* cycles_per_mma, bnn_stream_t s);
 
 /* ------------------------------------------------- host-buffer (reference-exact) API
  * Same semantics as the reference functions; synchronous; internal stream. */
@@ -305,7 +362,9 @@ int bnn_host_net_forward(bnn_net* net, const float* x, size_t batch, float* logi
  * that batch i+1's H2D and batch i-1's D2H overlap batch i's forward. Host buffers should be
  * pinned (cudaHostAlloc / torch pin_memory) for the copies to be asynchronous. At most `depth`
  * (2..8) batches may be outstanding; bnn_pipe_wait(seq) blocks until batch seq's logits are in
- * its host buffer. */
+ * its host buffer. Both copies are asynchronous: a submitted batch's `x` must stay unchanged and
+ * its `logits` untouched until bnn_pipe_wait(seq) returns. Each buffer set replays its own
+ * captured CUDA graph of the forward after its first two batches. */
 typedef struct bnn_pipe bnn_pipe;
 int bnn_pipe_create(bnn_net* net, size_t batch, int depth, bnn_pipe** out);
 int bnn_pipe_submit(bnn_pipe* p, const float* x, float* logits, uint64_t* seq);

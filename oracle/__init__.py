@@ -349,6 +349,29 @@ class RefLib:
         L.bnnref_net_layer_info.argtypes = [_P, _SZ, _P]
         L.bnnref_net_layer_params.argtypes = [_P, _SZ, _P, _P, _P, _P]
         L.bnnref_net_forward.argtypes = [_P, _P, _SZ, C.c_int, C.c_uint, C.c_uint, _P]
+        L.bnnref_run_verify.argtypes = [C.c_char_p, _SZ, _U64, C.POINTER(C.c_double), C.POINTER(_SZ),
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.bnnref_run_benchmark.argtypes = [C.c_char_p, _SZ, _SZ, _SZ, _U64, C.c_int, C.c_char_p]
+        L.bnnref_parse_report.argtypes = [C.c_char_p, C.POINTER(_SZ), C.POINTER(_U64)]
+
+    def run_verify(self, spec_path=None, batch=64, seed=1):
+        """run_verify (bench.cpp:193-199) -> the VerifySummary fields."""
+        dev, n, ok, pad = C.c_double(), C.c_size_t(), C.c_int(), C.c_int()
+        self._check(self.lib.bnnref_run_verify(None if spec_path is None else str(spec_path).encode(), batch, seed,
+                                               C.byref(dev), C.byref(n), C.byref(ok), C.byref(pad)))
+        return {"max_abs_deviation": dev.value, "compared": n.value, "pass": bool(ok.value),
+                "pad_correction_exercised": bool(pad.value)}
+
+    def run_benchmark(self, out_path, spec_path=None, batch=4, iterations=2, warmup=1, seed=1, kernels_mask=3):
+        """run_benchmark + emit_report (bench.cpp:102-170, 219-257) into out_path."""
+        self._check(self.lib.bnnref_run_benchmark(None if spec_path is None else str(spec_path).encode(), batch,
+                                                  iterations, warmup, seed, kernels_mask, str(out_path).encode()))
+
+    def parse_report(self, path):
+        """parse_report (bench.cpp:259-303): (kernel count, first kernel's logits hash)."""
+        n, h = C.c_size_t(), C.c_uint64()
+        self._check(self.lib.bnnref_parse_report(str(path).encode(), C.byref(n), C.byref(h)))
+        return n.value, h.value
 
     def _check(self, rc):
         if rc:
@@ -539,7 +562,7 @@ class RefNet:
     def forward(self, x, exec_kind="binary", threads=1, batch_threads=1):
         x = np.ascontiguousarray(x, np.float32)
         out = np.empty((self.logits, x.shape[0]), np.float32)
-        ek = {"float": 1, "binary": 2, "binary_reference": 4}[exec_kind]  # ExecKernel (network.hpp:91)
+        ek = {"per_layer": 0, "float": 1, "binary": 2, "naive": 3, "binary_reference": 4}[exec_kind]  # ExecKernel (network.hpp:91)
         self.ref._check(self.ref.lib.bnnref_net_forward(self.h, x.ctypes.data, x.shape[0], ek,
                                                         threads, batch_threads, out.ctypes.data))
         return out

@@ -332,7 +332,8 @@ void bnnref_net_layer_params(void* h, std::size_t i, std::uint32_t* packed, floa
         std::memcpy(shift, l.shift.data(), l.shift.size() * sizeof(float));
 }
 
-// network.cpp:330-420. exec: 2 = ExecKernel::Binary, 4 = BinaryReference.
+// network.cpp:330-420. exec: the ExecKernel value (0 PerLayer, 1 Float, 2 Binary, 3 Naive,
+// 4 BinaryReference).
 // x: [B, C, H, W]; logits: [features, B] (network.hpp:104-105).
 // batch_threads > 1 splits the batch into contiguous shards, one std::thread per
 // shard, each calling the reference network_forward on its slice (re-entrant,
@@ -371,6 +372,52 @@ int bnnref_net_forward(void* h, const float* x, std::size_t batch, int exec, uns
         }
         for (auto& e : errs)
             if (!e.empty()) throw ShapeError(e);
+    });
+}
+
+// run_verify (bench.cpp:193-199): spec_path NULL -> the default network.
+int bnnref_run_verify(const char* spec_path, std::size_t batch, std::uint64_t seed, double* max_dev,
+                      std::size_t* compared, int* pass, int* pad_exercised) {
+    return guarded([&] {
+        BenchConfig cfg;
+        cfg.spec_path = spec_path ? spec_path : "";
+        cfg.batch = batch;
+        cfg.seed = seed;
+        const VerifySummary s = run_verify(cfg);
+        *max_dev = s.max_abs_deviation;
+        *compared = s.compared;
+        *pass = s.pass ? 1 : 0;
+        *pad_exercised = s.pad_correction_exercised ? 1 : 0;
+    });
+}
+
+// run_benchmark (bench.cpp:102-170) + emit_report (bench.cpp:219-257). kernels_mask: bit 0
+// Binary, bit 1 Float, bit 2 Naive, in that order.
+int bnnref_run_benchmark(const char* spec_path, std::size_t batch, std::size_t iterations,
+                         std::size_t warmup, std::uint64_t seed, int kernels_mask,
+                         const char* out_path) {
+    return guarded([&] {
+        BenchConfig cfg;
+        cfg.spec_path = spec_path ? spec_path : "";
+        cfg.batch = batch;
+        cfg.iterations = iterations;
+        cfg.warmup = warmup;
+        cfg.seed = seed;
+        cfg.kernels.clear();
+        if (kernels_mask & 1) cfg.kernels.push_back(KernelChoice::Binary);
+        if (kernels_mask & 2) cfg.kernels.push_back(KernelChoice::Float);
+        if (kernels_mask & 4) cfg.kernels.push_back(KernelChoice::Naive);
+        emit_report(run_benchmark(cfg), out_path);
+    });
+}
+
+// parse_report (bench.cpp:259-303): 1 when the reference parser accepts the file; the
+// network name and the first kernel's logits hash come back for cross-checking.
+int bnnref_parse_report(const char* path, std::size_t* n_kernels, std::uint64_t* first_hash) {
+    return guarded([&] {
+        const BenchReport r = parse_report(path);
+        *n_kernels = r.kernels.size();
+        *first_hash = r.kernels.empty() ? 0 : r.kernels.front().logits_hash;
     });
 }
 

@@ -55,12 +55,14 @@ class ConvGeom(C.Structure):
 
 
 class LayerSpec(C.Structure):
-    """bnn_layer_spec == LayerSpec (network.hpp:23-39) for binary, seeded layers."""
+    """bnn_layer_spec == LayerSpec (network.hpp:23-39); kernel = KernelChoice (0 float, 1 binary,
+    2 naive), used by the per-layer engine."""
 
     _fields_ = [("kind", C.c_uint32), ("has_seed", C.c_uint32), ("seed", _U64),
                 ("out_channels", _U64), ("kernel_h", _U64), ("kernel_w", _U64),
                 ("stride_h", _U64), ("stride_w", _U64), ("pad_h", _U64), ("pad_w", _U64),
-                ("out_features", _U64), ("weights_blob", C.c_char_p)]
+                ("out_features", _U64), ("weights_blob", C.c_char_p), ("kernel", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 _SIGS = {
@@ -96,6 +98,16 @@ _SIGS = {
     "bnn_net_logits": (_SZ, [_P]),
     "bnn_net_num_layers": (_SZ, [_P]),
     "bnn_net_layer_params": (_I, [_P, _SZ, _P, C.POINTER(_SZ), C.POINTER(_SZ), _P, _P, _P]),
+    "bnn_net_layer_data": (_I, [_P, _SZ, _P, _P, _P, _P, _P]),
+    "bnn_net_set_layer_data": (_I, [_P, _SZ, _P, _P, _P, _P, _P]),
+    "bnn_net_set_layer_kernel": (_I, [_P, _SZ, _I]),
+    "bnn_im2col_f32": (_I, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P]),
+    "bnn_col2im_f32": (_I, [_P, _SZ, _SZ, _P, _SZ, _SZ, _P, C.POINTER(_SZ), C.POINTER(_SZ), _P]),
+    "bnn_conv_forward_naive_f32": (_I, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P, _P]),
+    "bnn_max_abs_diff_f32": (_I, [_P, _P, _SZ, C.POINTER(C.c_double), _P]),
+    "bnn_run_verify": (_I, [C.c_char_p, _SZ, _U64, C.c_char_p, C.POINTER(C.c_double), C.POINTER(_SZ),
+                            C.POINTER(_I), C.POINTER(_I)]),
+    "bnn_run_benchmark": (_I, [C.c_char_p, _SZ, _SZ, _SZ, _U64, _I, _I, C.c_char_p]),
     "bnn_net_forward": (_I, [_P, _P, _SZ, _P, _P]),
     "bnn_net_last_launches": (_SZ, [_P]),
     "bnn_net_set_engine": (_I, [_P, _I]),
@@ -127,6 +139,7 @@ _SIGS = {
     "bnn_net_device_bytes": (_SZ, [_P]),
     "bnn_probe_popc_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
     "bnn_probe_bmma_peak": (_I, [C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
+    "bnn_probe_umma_peak": (_I, [_I, _I, C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
     "bnn_host_sign_pack": (_I, [_P, _SZ, _SZ, _I, _I, _P]),
     "bnn_host_xnor_gemm": (_I, [_P, _SZ, _P, _SZ, _SZ, _P]),
     "bnn_host_conv_forward_binary": (_I, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),

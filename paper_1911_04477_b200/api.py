@@ -10,14 +10,17 @@ Reference → here:
     sign / htanh (binarize.hpp:9-16)             sign / htanh
     pack_rows / pack_cols (binarize.hpp:19-23)   pack_rows / pack_cols (strict: EncodingError)
     unpack (binarize.hpp:27)                     unpack
-    im2col (lowering.hpp:11)                     im2col_sign_pack (the binary im2col, K2)
+    im2col / col2im (lowering.hpp:11-18)         im2col / col2im (float), im2col_sign_pack (K2)
     xnor_gemm (kernels.hpp:53-54)                xnor_gemm
     conv_forward_binary (network.hpp:117-119)    conv_forward_binary
     linear_forward_packed (network.hpp:133-134)  linear_forward_packed
-    linear_forward (network.hpp:130-132)         linear_forward (kernel="binary")
+    linear_forward (network.hpp:130-132)         linear_forward (kernel "binary" / "float")
+    float_gemm, conv_forward_float (kernels.hpp:44, network.hpp:114-116)
+    conv_forward_binary_reference, linear_forward_binary_reference, conv_forward_naive
     maxpool2 / affine_norm / flatten_to_columns  maxpool2 / affine_norm / flatten_to_columns
     fill_random* / mix64 / unit_random           fill_random / mix64 / unit_random
-    build_network + network_forward (Binary)     Network
+    build_network + network_forward (ExecKernel) Network (engine "auto"/"float"/"binary_reference"/...)
+    verify_network (bench.cpp:172-191)           Network.verify
 """
 from __future__ import annotations
 
@@ -263,16 +266,75 @@ def xnor_gemm(w: PackedBitMatrix, x: PackedBitMatrix, inner_len: int, threads: i
 
 
 def to_float(m: np.ndarray) -> np.ndarray:
-    """kernels.cpp:90-95."""
-    return np.asarray(m, np.int32).astype(np.float32)
+    """kernels.cpp:90-95, on the device."""
+    import torch
+
+    m = np.ascontiguousarray(m, np.int32)
+    dm = _dev(m)
+    out = torch.empty(m.shape, dtype=torch.float32, device="cuda")
+    check(load().bnn_to_float_s32(dm.data_ptr(), m.size, out.data_ptr(), _stream()))
+    return out.cpu().numpy()
 
 
 def bias_add(a: np.ndarray, bias) -> np.ndarray:
-    """kernels.cpp:97-107."""
+    """kernels.cpp:97-107, on the device: a[d, j] += bias[d]."""
+    a = _f32(a)
     bias = _f32(bias)
     if bias.size != a.shape[0]:
         raise ShapeError(f"bias_add: bias length {bias.size} does not match {a.shape[0]} rows")
-    return (a + bias[:, None]).astype(np.float32)
+    da, db = _dev(a), _dev(bias)
+    check(load().bnn_bias_add_f32(da.data_ptr(), a.shape[0], a.size // max(1, a.shape[0]), db.data_ptr(),
+                                  _stream()))
+    return da.cpu().numpy()
+
+
+def float_gemm(w, x, threads: int = 1) -> np.ndarray:
+    """kernels.cpp:33-51 (the control group's float GEMM), on the CUDA cores: the reference's
+    k-ascending FMA chain per output, bit-identical."""
+    import torch
+
+    w, x = _f32(w), _f32(x)
+    if w.shape[1] != x.shape[0]:
+        raise ShapeError(f"float_gemm: inner extents differ, {w.shape[1]} vs {x.shape[0]}")
+    dw, dx = _dev(w), _dev(x)
+    out = torch.empty((w.shape[0], x.shape[1]), dtype=torch.float32, device="cuda")
+    check(load().bnn_float_gemm_f32(dw.data_ptr(), w.shape[0], w.shape[1], dx.data_ptr(), x.shape[1], None, 0,
+                                    out.data_ptr(), _stream()))
+    return out.cpu().numpy()
+
+
+def im2col(x, batch_index: int, geom) -> np.ndarray:
+    """lowering.cpp:7-43: the float [K, oh*ow] patch matrix of batch slice ``batch_index``."""
+    import torch
+
+    x = _f32(x)
+    g = ConvGeometry.of(geom)
+    if x.shape[1] != g.in_channels:
+        raise ShapeError(f"im2col: input has {x.shape[1]} channels, geometry expects {g.in_channels}")
+    oh, ow = output_dims(g, x.shape[2], x.shape[3])
+    out = torch.empty((g.patch_len(), oh * ow), dtype=torch.float32, device="cuda")
+    gc = g.c()
+    dx = _dev(x)
+    check(load().bnn_im2col_f32(dx.data_ptr(), *x.shape, batch_index, 1, C.byref(gc), out.data_ptr(), _stream()))
+    return out.cpu().numpy()
+
+
+def col2im(m, geom, out_h: int, out_w: int) -> np.ndarray:
+    """lowering.cpp:45-84, the adjoint of im2col: [K, out_h*out_w] -> [1, C, in_h, in_w]."""
+    import torch
+
+    m = _f32(m)
+    g = ConvGeometry.of(geom)
+    gc = g.c()
+    ih, iw = C.c_size_t(), C.c_size_t()
+    lib = load()
+    check(lib.bnn_col2im_f32(None, m.shape[0], m.shape[1], C.byref(gc), out_h, out_w, None, C.byref(ih), C.byref(iw),
+                             None))
+    out = torch.empty((1, g.in_channels, ih.value, iw.value), dtype=torch.float32, device="cuda")
+    dm = _dev(m)
+    check(lib.bnn_col2im_f32(dm.data_ptr(), m.shape[0], m.shape[1], C.byref(gc), out_h, out_w, out.data_ptr(), None,
+                             None, _stream()))
+    return out.cpu().numpy()
 
 
 # --------------------------------------------------------------------- layers
@@ -315,10 +377,74 @@ def linear_forward_packed(x, packed_w: PackedBitMatrix, bias, threads: int = 1) 
 
 
 def linear_forward(x, w, bias, kernel: str = "binary", threads: int = 1) -> np.ndarray:
-    """network.cpp:113-119; only the binary kernel is on the device hot path."""
-    if kernel != "binary":
-        raise ConfigError("only the binary kernel runs on the B200 path")
-    return linear_forward_packed(x, sign_pack_rows(w), bias, threads)
+    """network.cpp:113-119: binary packs the weights per call; float (and naive) run float_gemm."""
+    if kernel == "binary":
+        return linear_forward_packed(x, sign_pack_rows(w), bias, threads)
+    if kernel not in ("float", "naive"):
+        raise ConfigError(f"unknown kernel choice '{kernel}', expected binary|float|naive")
+    return bias_add(float_gemm(w, x), bias)
+
+
+def linear_forward_binary_reference(x, w_pm1, bias, threads: int = 1) -> np.ndarray:
+    """network.cpp:128-131: float_gemm(w_pm1, sign(x)) + bias, on the device."""
+    return bias_add(float_gemm(w_pm1, sign(x)), bias)
+
+
+def conv_forward_float(x, w_flat, bias, geom, threads: int = 1) -> np.ndarray:
+    """network.cpp:50-63: float im2col + float_gemm + bias on the device (bit-identical)."""
+    import torch
+
+    x, w_flat, bias = _f32(x), _f32(w_flat), _f32(bias)
+    g = ConvGeometry.of(geom)
+    oh, ow = output_dims(g, x.shape[2], x.shape[3])
+    if w_flat.shape[1] != g.patch_len():
+        raise ShapeError(f"float_gemm: inner extents differ, {w_flat.shape[1]} vs {g.patch_len()}")
+    if bias.size != w_flat.shape[0]:
+        raise ShapeError(f"bias_add: bias length {bias.size} does not match {w_flat.shape[0]} rows")
+    out = torch.empty((x.shape[0], g.out_channels, oh, ow), dtype=torch.float32, device="cuda")
+    dx, dw, db = _dev(x), _dev(w_flat), _dev(bias)
+    gc = g.c()
+    check(load().bnn_conv_forward_float_f32(dx.data_ptr(), *x.shape, dw.data_ptr(), db.data_ptr(), C.byref(gc),
+                                            out.data_ptr(), _stream()))
+    return out.cpu().numpy()
+
+
+def conv_forward_binary_reference(x, w_pm1, bias, geom, threads: int = 1) -> np.ndarray:
+    """network.cpp:81-94: sign(im2col(x)) then float_gemm(w_pm1) + bias, on the device."""
+    import torch
+
+    x, w_pm1, bias = _f32(x), _f32(w_pm1), _f32(bias)
+    g = ConvGeometry.of(geom)
+    oh, ow = output_dims(g, x.shape[2], x.shape[3])
+    B, K, N = x.shape[0], g.patch_len(), x.shape[0] * oh * ow
+    lib = load()
+    dx, dw, db = _dev(x), _dev(w_pm1), _dev(bias)
+    cols = torch.empty((K, N), dtype=torch.float32, device="cuda")
+    gc = g.c()
+    st = _stream()
+    check(lib.bnn_im2col_f32(dx.data_ptr(), *x.shape, 0, B, C.byref(gc), cols.data_ptr(), st))
+    check(lib.bnn_sign_f32(cols.data_ptr(), K * N, cols.data_ptr(), st))
+    out = torch.empty((B, g.out_channels, oh, ow), dtype=torch.float32, device="cuda")
+    check(lib.bnn_float_gemm_f32(dw.data_ptr(), w_pm1.shape[0], K, cols.data_ptr(), N, db.data_ptr(), oh * ow,
+                                 out.data_ptr(), st))
+    return out.cpu().numpy()
+
+
+def conv_forward_naive(x, w, bias, geom) -> np.ndarray:
+    """network.cpp:96-111: direct convolution (w [D, C, kH, kW]) + bias, on the device."""
+    import torch
+
+    x, w, bias = _f32(x), _f32(w), _f32(bias)
+    g = ConvGeometry.of(geom)
+    oh, ow = output_dims(g, x.shape[2], x.shape[3])
+    if bias.size != g.out_channels:
+        raise ShapeError("conv: bias length does not match output channels")
+    out = torch.empty((x.shape[0], g.out_channels, oh, ow), dtype=torch.float32, device="cuda")
+    dx, dw, db = _dev(x), _dev(w), _dev(bias)
+    gc = g.c()
+    check(load().bnn_conv_forward_naive_f32(dx.data_ptr(), *x.shape, dw.data_ptr(), db.data_ptr(), C.byref(gc),
+                                            out.data_ptr(), _stream()))
+    return out.cpu().numpy()
 
 
 def maxpool2(x) -> np.ndarray:
@@ -366,12 +492,12 @@ def flatten_to_columns(x) -> np.ndarray:
 
 
 def fnv1a_hash(m: np.ndarray) -> int:
-    """bench.cpp:23-33 (host arithmetic over the float bytes)."""
-    h = 1469598103934665603
-    for b in np.ascontiguousarray(m, np.float32).tobytes():
-        h ^= b
-        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
-    return h
+    """bench.cpp:23-33: FNV-1a over the float bytes (bnn_fnv1a_f32)."""
+    m = _f32(m)
+    h = C.c_uint64()
+    dm = _dev(m.reshape(-1))
+    check(load().bnn_fnv1a_f32(dm.data_ptr(), m.size, C.byref(h), _stream()))
+    return int(h.value)
 
 
 # --------------------------------------------------------------------- network
@@ -387,7 +513,10 @@ def _pair(v, default):
     return int(v), int(v)
 
 
-def layer_specs(layers) -> "C.Array":
+KERNELS = {"float": 0, "binary": 1, "naive": 2}
+
+
+def layer_specs(layers, default_kernel: str = "binary") -> "C.Array":
     """Layer dicts in the reference NetworkSpec JSON vocabulary (network.cpp:487-536)."""
     arr = (LayerSpec * len(layers))()
     for i, l in enumerate(layers):
@@ -395,6 +524,10 @@ def layer_specs(layers) -> "C.Array":
         if k not in KINDS:
             raise ConfigError(f"unknown layer kind '{k}'")
         arr[i].kind = KINDS[k]
+        kern = l.get("kernel", default_kernel)
+        if kern not in KERNELS:
+            raise ConfigError(f"unknown kernel choice '{kern}', expected binary|float|naive")
+        arr[i].kernel = KERNELS[kern]
         if "seed" in l:
             arr[i].has_seed, arr[i].seed = 1, int(l["seed"])
         arr[i].stride_h = arr[i].stride_w = 1
@@ -520,9 +653,16 @@ class Network:
     def handle(self):
         return self._h
 
+    def _check_input(self, shape) -> None:
+        """network.cpp:332-337: the input must be [B, C, H, W] with the network's C, H, W."""
+        if len(shape) != 4 or tuple(int(v) for v in shape[1:]) != self.input_chw or int(shape[0]) < 1:
+            got = "x".join(str(int(v)) for v in shape[1:]) if len(shape) == 4 else f"a {len(shape)}-d array"
+            raise ShapeError(f"network input is {got}, network expects " + "x".join(str(v) for v in self.input_chw))
+
     def forward(self, x) -> np.ndarray:
         """Host buffers in and out (H2D, forward, D2H): [B, C, H, W] -> [features, B]."""
         x = _f32(x)
+        self._check_input(x.shape)
         out = np.empty((self.logits, x.shape[0]), np.float32)
         check(load().bnn_host_net_forward(self._h, _p(x), x.shape[0], _p(out)))
         return out
@@ -531,28 +671,97 @@ class Network:
         """torch CUDA tensors in and out, stream-ordered."""
         import torch
 
+        self._check_input(tuple(x.shape))
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise ShapeError("forward_device: x must be a contiguous float32 CUDA tensor")
         B = x.shape[0]
         if out is None:
             out = torch.empty((self.logits, B), dtype=torch.float32, device=x.device)
+        elif out.dtype != torch.float32 or not out.is_cuda or not out.is_contiguous() or out.numel() < self.logits * B:
+            raise ShapeError(f"forward_device: out must be a contiguous float32 CUDA tensor of {self.logits}x{B}")
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         check(load().bnn_net_forward(self._h, x.data_ptr(), B, out.data_ptr(), st))
         return out
 
-    ENGINES = {"auto": 0, "generic": 1, "fused": 2, "float": 3}
+    ENGINES = {"auto": 0, "generic": 1, "fused": 2, "float": 3, "binary_reference": 4, "naive": 5,
+               "per_layer": 6}
 
     def pipeline(self, batch: int, depth: int = 3) -> "Pipeline":
         """A serving pipeline of host-buffer batches (bnn_pipe_*)."""
         return Pipeline(self, batch, depth)
 
     def set_engine(self, name: str) -> None:
-        """Select the device engine: "fused" (one tcgen05 launch per weighted layer, packed-bit
-        activations), "generic" (one kernel per reference op) or "auto" (fused when the topology
-        allows it). Both are bit-exact with the reference."""
+        """Select the device engine (the reference's ExecKernel): "fused" (Binary: one tcgen05
+        launch per weighted layer, packed-bit activations), "generic" (Binary, one kernel per
+        reference op), "auto" (fused when the topology allows it), "float" (ExecKernel::Float),
+        "binary_reference" (ExecKernel::BinaryReference), "naive" (ExecKernel::Naive) or
+        "per_layer" (each layer's own kernel). All are bit-exact with the reference."""
+        if name not in self.ENGINES:
+            raise ConfigError(f"unknown engine '{name}'")
         check(load().bnn_net_set_engine(self._h, self.ENGINES[name]))
 
     @property
     def engine(self) -> str:
-        return {1: "generic", 2: "fused", 3: "float"}[int(load().bnn_net_engine(self._h))]
+        names = {v: k for k, v in self.ENGINES.items()}
+        return names[int(load().bnn_net_engine(self._h))]
+
+    def forward_with(self, x, engine: str) -> np.ndarray:
+        """network_forward(net, x, {ExecKernel}) with the engine switched for this call only."""
+        prev = int(load().bnn_net_engine(self._h))
+        prev_name = "auto" if prev in (1, 2) else {v: k for k, v in self.ENGINES.items()}[prev]
+        self.set_engine(engine)
+        try:
+            return self.forward(x)
+        finally:
+            self.set_engine(prev_name)
+
+    def verify(self, x, tolerance: float = 1e-4) -> dict:
+        """verify_network (bench.cpp:172-191): Binary (the fused engine) against BinaryReference
+        (sign(im2col) + float_gemm on sign(weights)), both on the device; the max |delta logit|
+        is reduced on the device (bnn_max_abs_diff_f32)."""
+        import torch
+
+        x = _f32(x)
+        self._check_input(x.shape)
+        dx = _dev(x)
+        got = torch.empty((self.logits, x.shape[0]), dtype=torch.float32, device="cuda")
+        want = torch.empty_like(got)
+        st = _stream()
+        self.forward_device(dx, got, st)
+        lib = load()
+        prev = int(lib.bnn_net_engine(self._h))
+        check(lib.bnn_net_set_engine(self._h, self.ENGINES["binary_reference"]))
+        try:
+            check(lib.bnn_net_forward(self._h, dx.data_ptr(), x.shape[0], want.data_ptr(), st))
+        finally:
+            lib.bnn_net_set_engine(self._h, 0 if prev in (1, 2) else prev)
+        dev = C.c_double()
+        check(lib.bnn_max_abs_diff_f32(got.data_ptr(), want.data_ptr(), got.numel(), C.byref(dev), st))
+        return {"batch": int(x.shape[0]), "compared": int(got.numel()), "max_abs_deviation": dev.value,
+                "tolerance": tolerance, "pass": dev.value <= tolerance}
+
+    def layer_data(self, i: int):
+        """BuiltLayer parameters of layer i: (packed words, float weights, bias, scale, shift)."""
+        lib = load()
+        rows, cols = C.c_size_t(), C.c_size_t()
+        check(lib.bnn_net_layer_params(self._h, i, None, C.byref(rows), C.byref(cols), None, None, None))
+        r, c = rows.value, cols.value
+        packed = np.zeros((r, words_per_line(c) if c else 0), np.uint32)
+        weights = np.zeros((r, c), np.float32)
+        bias = np.zeros(r, np.float32)
+        n_aff = self._affine_width(i) if self.layers[i]["kind"] == "affine_norm" else 0
+        scale, shift = np.zeros(n_aff, np.float32), np.zeros(n_aff, np.float32)
+        check(lib.bnn_net_layer_data(self._h, i, _p(packed) if r else None, _p(weights) if r else None,
+                                     _p(bias) if r else None, _p(scale) if n_aff else None,
+                                     _p(shift) if n_aff else None))
+        return packed, weights, bias, scale, shift
+
+    def set_layer_data(self, i: int, packed=None, weights=None, bias=None, scale=None, shift=None) -> None:
+        """Replace layer i's parameters on the device (the reference's net.layers[i] test hook)."""
+        arrs = [None if a is None else np.ascontiguousarray(a, dt)
+                for a, dt in ((packed, np.uint32), (weights, np.float32), (bias, np.float32), (scale, np.float32),
+                              (shift, np.float32))]
+        check(load().bnn_net_set_layer_data(self._h, i, *[None if a is None else _p(a) for a in arrs]))
 
     def last_launches(self) -> int:
         return int(load().bnn_net_last_launches(self._h))

@@ -7,58 +7,19 @@
 // lowering.cpp:87-102) stay host memcpys like the reference's.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "bnn_b200.hpp"
 #include "bnn_cuda.h"
+#include "cpp_internal.hpp"
 
 namespace bnn {
 namespace {
 
-[[noreturn]] void raise(int rc) {
-    const std::string msg = bnn_last_error();
-    switch (rc) {
-        case BNN_E_SHAPE: throw ShapeError(msg);
-        case BNN_E_ENCODING: throw EncodingError(msg);
-        case BNN_E_CONFIG: throw ConfigError(msg);
-        case BNN_E_IO: throw IoError(msg);
-        default: throw CudaError(msg);
-    }
-}
-
-inline void check(int rc) {
-    if (rc != BNN_OK) raise(rc);
-}
-
-inline void cuda(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-// Device buffer; synchronous copies on the legacy default stream (the stream every call here uses).
-class Dev {
-public:
-    explicit Dev(std::size_t bytes) { cuda(cudaMalloc(&p_, bytes ? bytes : 16), "cudaMalloc"); }
-    ~Dev() { cudaFree(p_); }
-    Dev(const Dev&) = delete;
-    Dev& operator=(const Dev&) = delete;
-    template <class T>
-    T* as() const { return static_cast<T*>(p_); }
-    void put(const void* src, std::size_t bytes) { cuda(cudaMemcpy(p_, src, bytes, cudaMemcpyHostToDevice), "H2D"); }
-    void get(void* dst, std::size_t bytes) const { cuda(cudaMemcpy(dst, p_, bytes, cudaMemcpyDeviceToHost), "D2H"); }
-
-private:
-    void* p_ = nullptr;
-};
-
-void check_extent(std::size_t v, const char* name) {  // tensor.cpp:11-13
-    if (v == 0) throw ShapeError(std::string("extent '") + name + "' must be >= 1");
-}
-
-bnn_conv_geom to_c(const ConvGeometry& g) {
-    return bnn_conv_geom{g.kernel_h, g.kernel_w, g.stride_h, g.stride_w, g.pad_h, g.pad_w, g.in_channels,
-                         g.out_channels};
-}
+using namespace cppi;
 
 // unary elementwise op (0 sign, 1 htanh) on the device
 std::vector<float> unary(const std::vector<float>& x, int op) {
@@ -270,10 +231,10 @@ FloatMatrix linear_forward_packed(const FloatMatrix& x, const PackedBitMatrix& p
 }
 
 FloatMatrix linear_forward(const FloatMatrix& x, const FloatMatrix& w, std::span<const float> bias,
-                           KernelChoice kernel, unsigned threads) {
-    if (kernel != KernelChoice::Binary)
-        throw ConfigError("linear_forward: only KernelChoice::Binary runs on the B200 path");
-    return linear_forward_packed(x, sign_pack_rows(w), bias, threads);  // packs per call, network.cpp:116-117
+                           KernelChoice kernel, unsigned threads) {  // network.cpp:113-120
+    if (kernel == KernelChoice::Binary)
+        return linear_forward_packed(x, pack_rows(sign(w)), bias, threads);  // packs per call
+    return bias_add(float_gemm(w, x, threads), bias);
 }
 
 FloatTensor maxpool2(const FloatTensor& x) {
@@ -331,7 +292,7 @@ NetworkSpec build_default_network(KernelChoice kernel, std::uint64_t seed) {
     bnn_layer_spec buf[64];
     const std::size_t n = bnn_default_spec(buf, 64);
     NetworkSpec spec;
-    spec.name = "bnn-cifar10-vgg-small";
+    spec.name = "bnn-cifar10";
     spec.seed = seed;
     for (std::size_t i = 0; i < n; ++i) {
         LayerSpec l;
@@ -350,9 +311,8 @@ NetworkSpec build_default_network(KernelChoice kernel, std::uint64_t seed) {
 DeviceNetwork::DeviceNetwork(const NetworkSpec& spec) {
     std::vector<bnn_layer_spec> layers;
     for (const LayerSpec& l : spec.layers) {
-        if ((l.kind == LayerKind::Conv || l.kind == LayerKind::Linear) && l.kernel != KernelChoice::Binary)
-            throw ConfigError("DeviceNetwork: weighted layers must use KernelChoice::Binary");
         bnn_layer_spec c{};
+        c.kernel = static_cast<std::uint32_t>(l.kernel);
         c.kind = static_cast<std::uint32_t>(l.kind);
         c.has_seed = l.seed.has_value() ? 1 : 0;
         c.seed = l.seed.value_or(0);
@@ -421,15 +381,5 @@ FloatMatrix DeviceNetwork::forward(const FloatTensor& x) {
 }
 
 FloatMatrix network_forward(DeviceNetwork& net, const FloatTensor& x) { return net.forward(x); }
-
-std::uint64_t fnv1a_hash(std::span<const float> values) {  // bench.cpp:23-33
-    std::uint64_t h = 1469598103934665603ull;  // the reference's basis (not the standard 14695981039346656037)
-    const auto* p = reinterpret_cast<const unsigned char*>(values.data());
-    for (std::size_t i = 0; i < values.size() * sizeof(float); ++i) {
-        h ^= p[i];
-        h *= 1099511628211ull;
-    }
-    return h;
-}
 
 }  // namespace bnn

@@ -131,6 +131,20 @@ int launch_affine_scale(float* v, size_t n, cudaStream_t s) {
     return launch_check("affine_scale_kernel");
 }
 
+// max |a[i] - b[i]| (verify_network's deviation, bench.cpp:178-181): each thread folds its
+// elements, the warp reduces, one atomicMax per warp on the float's bits (non-negative floats
+// order like their unsigned bit patterns). NaN deviations map to +inf.
+__global__ void max_abs_diff_kernel(const float* __restrict__ a, const float* __restrict__ b, size_t n,
+                                    unsigned* __restrict__ out) {
+    float m = 0.0f;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const float d = fabsf(a[i] - b[i]);
+        m = d != d ? __int_as_float(0x7f800000) : fmaxf(m, d);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
 }  // namespace bnnk
 
 using namespace bnnk;
@@ -175,6 +189,24 @@ int bnn_fill_random_f32(uint64_t seed, uint64_t offset, size_t n, float* out, bn
 }
 
 uint64_t bnn_mix64(uint64_t seed, uint64_t counter) { return mix64(seed, counter); }
+
+int bnn_max_abs_diff_f32(const float* a, const float* b, size_t n, double* out, bnn_stream_t s) {
+    BNN_TRY(require_sm100());
+    Scratch m;
+    BNN_TRY(m.alloc(sizeof(unsigned), S(s)));
+    BNN_CUDA(cudaMemsetAsync(m.p, 0, sizeof(unsigned), S(s)));
+    if (n) {
+        max_abs_diff_kernel<<<grid_for(n, 256), 256, 0, S(s)>>>(a, b, n, m.as<unsigned>());
+        BNN_TRY(launch_check("max_abs_diff_kernel"));
+    }
+    unsigned h = 0;
+    BNN_CUDA(cudaMemcpyAsync(&h, m.p, sizeof h, cudaMemcpyDeviceToHost, S(s)));
+    BNN_CUDA(cudaStreamSynchronize(S(s)));
+    float f;
+    memcpy(&f, &h, 4);
+    *out = double(f);
+    return BNN_OK;
+}
 
 int bnn_fnv1a_f32(const float* x, size_t n, uint64_t* hash, bnn_stream_t s) {
     std::vector<float> h(n);

@@ -22,6 +22,7 @@
 
 #include <nlohmann/json.hpp>
 
+#include "bnn_b200.hpp"
 #include "bnn_cuda.h"
 
 namespace bnnk {
@@ -64,77 +65,53 @@ int write_file(const char* path, const std::string& buf) {
     return BNN_OK;
 }
 
-// kernel_size / stride / pad: a number or a [h, w] pair (network.cpp pair_field)
-std::pair<uint64_t, uint64_t> pair_field(const json& lj, const char* key, uint64_t dflt) {
-    if (!lj.contains(key)) return {dflt, dflt};
-    const json& v = lj.at(key);
-    if (v.is_array()) {
-        if (v.size() != 2) throw std::runtime_error(std::string(key) + " must be a number or a pair");
-        return {v[0].get<uint64_t>(), v[1].get<uint64_t>()};
-    }
-    const uint64_t s = v.get<uint64_t>();
-    return {s, s};
-}
-
 struct ParsedSpec {
-    std::string name;
-    uint64_t shape[4] = {1, 3, 32, 32};
-    uint64_t seed = 1;
-    int binarize = 0;
+    bnn::NetworkSpec spec;
     std::vector<bnn_layer_spec> layers;
-    std::vector<std::string> blobs;  // per layer ("" = seeded weights)
 };
 
+// load_network_spec with its exceptions mapped onto the C ABI's status codes.
 int parse_spec(const char* path, ParsedSpec& out) {
-    std::ifstream is(path);
-    if (!is) return bnnk::fail(BNN_E_CONFIG, std::string("cannot open network spec: ") + path);
-    json j;
     try {
-        j = json::parse(is);
-    } catch (const json::parse_error& e) {
-        return bnnk::fail(BNN_E_CONFIG, std::string("parse error in ") + path + ": " + e.what());
-    }
-    try {
-        out.name = j.value("name", std::string("unnamed"));
-        if (j.contains("input_shape")) {
-            const json& s = j.at("input_shape");
-            if (!s.is_array() || s.size() != 4)
-                return bnnk::fail(BNN_E_CONFIG, "input_shape must be [batch, channels, height, width]");
-            for (int i = 0; i < 4; ++i) out.shape[i] = s[i].get<uint64_t>();
-        }
-        out.seed = j.value("seed", uint64_t{1});
-        out.binarize = j.value("binarize_weights", false) ? 1 : 0;
-        if (!j.contains("layers") || !j.at("layers").is_array())
-            return bnnk::fail(BNN_E_CONFIG, "spec needs a 'layers' array");
-        static const char* kinds[] = {"conv", "linear", "maxpool", "affine_norm", "sign", "htanh"};
-        for (const json& lj : j.at("layers")) {
-            bnn_layer_spec l{};
-            l.stride_h = l.stride_w = 1;
-            const std::string k = lj.at("kind").get<std::string>();
-            int kind = -1;
-            for (int i = 0; i < 6; ++i)
-                if (k == kinds[i]) kind = i;
-            if (kind < 0) return bnnk::fail(BNN_E_CONFIG, "unknown layer kind '" + k + "'");
-            l.kind = uint32_t(kind);
-            if (kind == BNN_LAYER_CONV) {
-                l.out_channels = lj.at("out_channels").get<uint64_t>();
-                std::tie(l.kernel_h, l.kernel_w) = pair_field(lj, "kernel_size", 0);
-                if (l.kernel_h == 0) return bnnk::fail(BNN_E_CONFIG, "conv layer needs kernel_size");
-                std::tie(l.stride_h, l.stride_w) = pair_field(lj, "stride", 1);
-                std::tie(l.pad_h, l.pad_w) = pair_field(lj, "pad", 0);
-            } else if (kind == BNN_LAYER_LINEAR) {
-                l.out_features = lj.at("out_features").get<uint64_t>();
-            }
-            std::string blob;
-            if (kind == BNN_LAYER_CONV || kind == BNN_LAYER_LINEAR) blob = lj.value("weights_blob", std::string{});
-            if (lj.contains("seed")) l.has_seed = 1, l.seed = lj.at("seed").get<uint64_t>();
-            out.layers.push_back(l);
-            out.blobs.push_back(blob);
-        }
+        out.spec = bnn::load_network_spec(path);
+    } catch (const bnn::ConfigError& e) {
+        return bnnk::fail(BNN_E_CONFIG, e.what());
+    } catch (const bnn::ShapeError& e) {
+        return bnnk::fail(BNN_E_SHAPE, e.what());
+    } catch (const bnn::IoError& e) {
+        return bnnk::fail(BNN_E_IO, e.what());
     } catch (const std::exception& e) {
-        return bnnk::fail(BNN_E_CONFIG, std::string("bad network spec ") + path + ": " + e.what());
+        return bnnk::fail(BNN_E_CONFIG, e.what());
     }
+    for (const bnn::LayerSpec& l : out.spec.layers) {
+        bnn_layer_spec c{};
+        c.kind = uint32_t(l.kind);
+        c.has_seed = l.seed ? 1 : 0;
+        c.seed = l.seed.value_or(0);
+        c.out_channels = l.out_channels;
+        c.kernel_h = l.kernel_h, c.kernel_w = l.kernel_w;
+        c.stride_h = l.stride_h, c.stride_w = l.stride_w;
+        c.pad_h = l.pad_h, c.pad_w = l.pad_w;
+        c.out_features = l.out_features;
+        c.kernel = uint32_t(l.kernel);
+        out.layers.push_back(c);
+    }
+    for (size_t i = 0; i < out.layers.size(); ++i)  // pointers into out.spec, which outlives the calls below
+        out.layers[i].weights_blob = out.spec.layers[i].weights_blob.empty() ? nullptr : out.spec.layers[i].weights_blob.c_str();
     return BNN_OK;
+}
+
+// kernel_size / stride / pad: a number or a [h, w] pair (network.cpp:470-482). A malformed
+// pair is a ConfigError with the reference's own text (not wrapped: it is not a json error).
+std::pair<size_t, size_t> pair_field(const json& lj, const char* key, size_t dflt) {
+    if (!lj.contains(key)) return {dflt, dflt};
+    const json& v = lj.at(key);
+    if (!v.is_array()) {
+        const size_t s = v.get<size_t>();
+        return {s, s};
+    }
+    if (v.size() != 2) throw bnn::ConfigError(std::string(key) + " must be a scalar or [h, w]");
+    return {v[0].get<size_t>(), v[1].get<size_t>()};
 }
 
 }  // namespace
@@ -228,18 +205,128 @@ int bnn_load_tensor_blob(const char* path, uint64_t shape[4], float* data, size_
 int bnn_net_create_from_spec(const char* path, int binarize_override, bnn_net** out) {
     ParsedSpec sp;
     if (int rc = parse_spec(path, sp)) return rc;
-    for (size_t i = 0; i < sp.layers.size(); ++i) sp.layers[i].weights_blob = sp.blobs[i].empty() ? nullptr : sp.blobs[i].c_str();
-    const int bin = binarize_override >= 0 ? binarize_override : sp.binarize;
-    return bnn_net_create(sp.layers.data(), sp.layers.size(), sp.shape[1], sp.shape[2], sp.shape[3], sp.seed, bin, out);
+    const int bin = binarize_override >= 0 ? binarize_override : (sp.spec.binarize_weights ? 1 : 0);
+    const auto& s = sp.spec.input_shape;
+    return bnn_net_create(sp.layers.data(), sp.layers.size(), s[1], s[2], s[3], sp.spec.seed, bin, out);
 }
 
 // Spec header for callers that build their own inputs: input_shape and layer count.
 int bnn_spec_info(const char* path, uint64_t input_shape[4], size_t* n_layers) {
     ParsedSpec sp;
     if (int rc = parse_spec(path, sp)) return rc;
-    for (int i = 0; i < 4; ++i) input_shape[i] = sp.shape[i];
+    for (int i = 0; i < 4; ++i) input_shape[i] = sp.spec.input_shape[i];
     if (n_layers) *n_layers = sp.layers.size();
     return BNN_OK;
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ C++ API: the NetworkSpec schema
+namespace bnn {
+
+const char* to_string(LayerKind k) {  // network.cpp:10-20
+    static const char* names[] = {"conv", "linear", "maxpool", "affine_norm", "sign", "htanh"};
+    const unsigned i = unsigned(k);
+    return i < 6 ? names[i] : "?";
+}
+
+const char* to_string(KernelChoice k) {  // network.cpp:22-29
+    static const char* names[] = {"float", "binary", "naive"};
+    const unsigned i = unsigned(k);
+    return i < 3 ? names[i] : "?";
+}
+
+LayerKind parse_layer_kind(const std::string& s) {  // network.cpp:31-39
+    for (unsigned i = 0; i < 6; ++i)
+        if (s == to_string(LayerKind(i))) return LayerKind(i);
+    throw ConfigError("unknown layer kind '" + s + "'");
+}
+
+KernelChoice parse_kernel_choice(const std::string& s) {  // network.cpp:41-46
+    for (unsigned i = 0; i < 3; ++i)
+        if (s == to_string(KernelChoice(i))) return KernelChoice(i);
+    throw ConfigError("unknown kernel choice '" + s + "', expected binary|float|naive");
+}
+
+// load_network_spec (network.cpp:487-536): the same schema, defaults and error behaviour -- json
+// type / missing-key errors become ConfigError("bad network spec <path>: ..."), the schema's own
+// ConfigErrors (bad shape, unknown kind or kernel, malformed pair) pass through unwrapped.
+NetworkSpec load_network_spec(const std::string& path) {
+    std::ifstream is(path);
+    if (!is) throw ConfigError("cannot open network spec: " + path);
+    json j;
+    try {
+        j = json::parse(is);
+    } catch (const json::parse_error& e) {
+        throw ConfigError("parse error in " + path + ": " + e.what());
+    }
+    try {
+        NetworkSpec spec;
+        spec.name = j.value("name", std::string("unnamed"));
+        if (j.contains("input_shape")) {
+            const json& sh = j.at("input_shape");
+            if (!sh.is_array() || sh.size() != 4) throw ConfigError("input_shape must be [batch, channels, height, width]");
+            for (size_t i = 0; i < 4; ++i) spec.input_shape[i] = sh[i].get<size_t>();
+        }
+        spec.seed = j.value("seed", uint64_t{1});
+        spec.binarize_weights = j.value("binarize_weights", false);
+        const KernelChoice fallback = parse_kernel_choice(j.value("kernel", std::string("float")));
+        if (!j.contains("layers") || !j.at("layers").is_array()) throw ConfigError("spec needs a 'layers' array");
+        for (const json& lj : j.at("layers")) {
+            LayerSpec l;
+            l.kind = parse_layer_kind(lj.at("kind").get<std::string>());
+            const bool weighted = l.kind == LayerKind::Conv || l.kind == LayerKind::Linear;
+            if (l.kind == LayerKind::Conv) {
+                l.out_channels = lj.at("out_channels").get<size_t>();
+                std::tie(l.kernel_h, l.kernel_w) = pair_field(lj, "kernel_size", 0);
+                if (l.kernel_h == 0) throw ConfigError("conv layer needs kernel_size");
+                std::tie(l.stride_h, l.stride_w) = pair_field(lj, "stride", 1);
+                std::tie(l.pad_h, l.pad_w) = pair_field(lj, "pad", 0);
+            } else if (l.kind == LayerKind::Linear) {
+                l.out_features = lj.at("out_features").get<size_t>();
+            }
+            if (weighted) {
+                l.kernel = lj.contains("kernel") ? parse_kernel_choice(lj.at("kernel").get<std::string>()) : fallback;
+                l.weights_blob = lj.value("weights_blob", std::string{});
+            }
+            if (lj.contains("seed")) l.seed = lj.at("seed").get<uint64_t>();
+            spec.layers.push_back(std::move(l));
+        }
+        return spec;
+    } catch (const json::exception& e) {
+        throw ConfigError("bad network spec " + path + ": " + e.what());
+    }
+}
+
+void save_network_spec(const NetworkSpec& spec, const std::string& path) {  // network.cpp:538-567
+    json j;
+    j["name"] = spec.name;
+    j["input_shape"] = spec.input_shape;
+    j["seed"] = spec.seed;
+    j["binarize_weights"] = spec.binarize_weights;
+    json layers = json::array();
+    for (const LayerSpec& l : spec.layers) {
+        json lj;
+        lj["kind"] = to_string(l.kind);
+        if (l.kind == LayerKind::Conv) {
+            lj["out_channels"] = l.out_channels;
+            lj["kernel_size"] = json::array({l.kernel_h, l.kernel_w});
+            lj["stride"] = json::array({l.stride_h, l.stride_w});
+            lj["pad"] = json::array({l.pad_h, l.pad_w});
+        } else if (l.kind == LayerKind::Linear) {
+            lj["out_features"] = l.out_features;
+        }
+        if (l.kind == LayerKind::Conv || l.kind == LayerKind::Linear) {
+            lj["kernel"] = to_string(l.kernel);
+            if (!l.weights_blob.empty()) lj["weights_blob"] = l.weights_blob;
+        }
+        if (l.seed) lj["seed"] = *l.seed;
+        layers.push_back(std::move(lj));
+    }
+    j["layers"] = std::move(layers);
+    std::ofstream os(path);
+    if (!os) throw IoError("cannot open for writing: " + path);
+    os << j.dump(2) << '\n';
+}
+
+}  // namespace bnn

@@ -44,6 +44,8 @@ int launch_unary(int, const float*, size_t, float*, cudaStream_t);
 int make_tmap_2d_s8(CUtensorMap* map, const void* base, size_t rows, size_t K, size_t ld, uint32_t box_rows);
 int launch_float_gemm(const float*, const float*, size_t, size_t, size_t, const float*, size_t, float*, cudaStream_t);
 int launch_im2col_f32(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*, float*, cudaStream_t);
+int launch_naive_conv(const float*, size_t, size_t, size_t, size_t, const float*, const float*, const bnn_conv_geom*,
+                      float*, cudaStream_t);
 
 namespace {
 
@@ -80,6 +82,7 @@ struct Layer {
     size_t rows = 0, cols = 0, wpl = 0;  // packed weights: rows lines x wpl words, L = cols
     DevBuf wf;                           // float weights [rows, cols] (the float control group)
     DevBuf packed, bias, scale, shift;
+    DevBuf wpm1;                         // sign(wf), made on first use by the BinaryReference graph
     size_t n_affine = 0;
     size_t in_c = 0, in_h = 0, in_w = 0;  // input shape (per image)
     bool in_flat = false;
@@ -111,6 +114,7 @@ struct FusedStage {
 struct bnn_net {
     std::vector<std::unique_ptr<bnnk::Layer>> layers;
     size_t in_c = 0, in_h = 0, in_w = 0, logits = 0;
+    bool binarize = false;          // NetworkSpec::binarize_weights
     size_t max_act_per_image = 0;   // floats
     size_t max_lines_words_per_image = 0;
     // activation arena
@@ -127,7 +131,7 @@ struct bnn_net {
     std::vector<double> layer_ms, gemm_ms;
     std::vector<size_t> gemm_launches;
     // fused engine (fused.cu): one launch per weighted layer, packed-bit activations
-    int engine_policy = 0;  // BNN_ENGINE_AUTO / GENERIC / FUSED
+    int engine_policy = 0;  // BNN_ENGINE_*
     bool fusable = false;
     std::string unfusable_why;
     std::vector<std::unique_ptr<bnnk::FusedStage>> stages;
@@ -142,7 +146,7 @@ struct bnn_net {
         size_t launches = 0;
         int epoch = 0, arena = 0;
     };
-    std::array<Graph, 4> graphs;
+    std::array<Graph, 8> graphs;  // >= the serving pipe's maximum depth: each buffer set keeps its graph
     size_t graph_next = 0;
     int arena_epoch = 0;  // bumped whenever an internal buffer is reallocated (graphs hold pointers)
     void drop_graphs() {
@@ -251,6 +255,8 @@ int build(bnn_net* net, const bnn_layer_spec* specs, size_t n, uint64_t seed, cu
             } else {
                 BNN_TRY(fill(tmp.as<float>(), nw, mix64(base, 1), s));
             }
+            // network.cpp:245,268: binarize_weights applies sign to the generated (or loaded) weights
+            if (net->binarize) BNN_TRY(launch_unary(0, tmp.as<float>(), nw, tmp.as<float>(), s));
             BNN_TRY(L->wf.alloc(nw * 4));  // network.cpp:246,269: layer.weights, kept for ExecKernel::Float
             BNN_CUDA(cudaMemcpyAsync(L->wf.p, tmp.p, nw * 4, cudaMemcpyDeviceToDevice, s));
             BNN_TRY(L->packed.alloc(L->rows * L->wpl * 4));
@@ -285,6 +291,8 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         net->stages.clear();
         return BNN_OK;
     };
+    net->stages.clear();
+    net->fusable = false;
     size_t i = 0;
     size_t max_words = 0;
     DevBuf bad;
@@ -505,97 +513,40 @@ struct EventPair {
     }
 };
 
-int forward_generic(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
-    BNN_TRY(ensure_arena(net, B));
-    size_t launches = 0;
-    const float* cur = x;
-    int which = 0;
-    auto next = [&]() { float* o = net->act[which].as<float>(); which ^= 1; return o; };
-    for (size_t li = 0; li < net->layers.size(); ++li) {
-        Layer& L = *net->layers[li];
-        EventPair layer_ev(net, li, 0, s);
-        switch (L.spec.kind) {
-            case BNN_LAYER_CONV: {
-                float* out = next();
-                BNN_TRY(launch_im2col_sign_pack(cur, B, L.in_c, L.in_h, L.in_w, &L.geom,
-                                                net->lines.as<uint32_t>(), L.wpl, s));
-                EventPair gemm_ev(net, li, 1, s);
-                BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl,
-                                 L.rows, B * L.out_h * L.out_w, L.cols, L.bias.as<float>(),
-                                 L.out_h * L.out_w, out, s));
-                gemm_ev.close();
-                launches += 2;
-                cur = out;
-                break;
-            }
-            case BNN_LAYER_LINEAR: {
-                if (!L.in_flat) {  // flatten_to_columns: [B, F] -> [F, B]
-                    float* t = next();
-                    BNN_TRY(launch_transpose(cur, B, L.cols, t, s));
-                    ++launches;
-                    cur = t;
-                }
-                float* out = next();
-                BNN_TRY(launch_pack_cols(cur, L.cols, B, net->lines.as<uint32_t>(), L.wpl, nullptr, s));
-                EventPair gemm_ev(net, li, 1, s);
-                BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl,
-                                 L.rows, B, L.cols, L.bias.as<float>(), B, out, s));
-                gemm_ev.close();
-                launches += 2;
-                cur = out;
-                break;
-            }
-            case BNN_LAYER_MAXPOOL: {
-                float* out = next();
-                BNN_TRY(launch_maxpool2(cur, B, L.in_c, L.in_h, L.in_w, out, s));
-                ++launches;
-                cur = out;
-                break;
-            }
-            case BNN_LAYER_AFFINE: {
-                float* out = next();
-                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
-                const size_t plane = L.in_flat ? B : L.in_h * L.in_w;
-                BNN_TRY(launch_affine(cur, n, L.in_c, plane, L.scale.as<float>(),
-                                      L.shift.as<float>(), out, s));
-                ++launches;
-                cur = out;
-                break;
-            }
-            case BNN_LAYER_SIGN:
-            case BNN_LAYER_HTANH: {
-                float* out = next();
-                const size_t n = L.in_flat ? L.in_c * B : B * L.in_c * L.in_h * L.in_w;
-                BNN_TRY(launch_unary(L.spec.kind == BNN_LAYER_SIGN ? 0 : 1, cur, n, out, s));
-                ++launches;
-                cur = out;
-                break;
-            }
-        }
-        layer_ev.close();
+// Per-layer execution of a weighted layer in the layer-by-layer engine (ExecKernel,
+// network.hpp:89-91, resolved as resolve_exec does at network.cpp:318-327).
+enum LayerExec { EXEC_BINARY = 0, EXEC_FLOAT = 1, EXEC_BINREF = 2, EXEC_NAIVE = 3 };
+
+int layer_exec(const bnn_net* net, const Layer& L) {
+    switch (net->engine_policy) {
+        case BNN_ENGINE_FLOAT: return EXEC_FLOAT;
+        case BNN_ENGINE_BINARY_REFERENCE: return EXEC_BINREF;
+        case BNN_ENGINE_NAIVE: return EXEC_NAIVE;
+        case BNN_ENGINE_PER_LAYER:  // the layer's own KernelChoice (network.cpp:318-325)
+            return L.spec.kernel == BNN_KERNEL_BINARY ? EXEC_BINARY
+                   : L.spec.kernel == BNN_KERNEL_NAIVE ? EXEC_NAIVE
+                                                       : EXEC_FLOAT;
+        default: return EXEC_BINARY;
     }
-    const Layer& last = *net->layers.back();
-    if (last.out_flat) {
-        BNN_CUDA(cudaMemcpyAsync(logits, cur, net->logits * B * 4, cudaMemcpyDeviceToDevice, s));
-    } else {
-        BNN_TRY(launch_transpose(cur, B, net->logits, logits, s));
-        ++launches;
-    }
-    net->last_launches = launches;
-    return BNN_OK;
 }
 
+// sign(layer.weights) for the BinaryReference graph (network.cpp:357,380), made once per layer.
+int ensure_wpm1(Layer& L, cudaStream_t s) {
+    if (L.wpm1.p) return BNN_OK;
+    BNN_TRY(L.wpm1.alloc(L.rows * L.cols * 4));
+    return launch_unary(0, L.wf.as<float>(), L.rows * L.cols, L.wpm1.as<float>(), s);
+}
 
-// bnn_set_fused_chain / BNN_FUSED_CHAIN: 1 one chained launch, 0 (default) one launch per
-// weighted layer. The chained kernel removes the ~3-4 us launch boundaries but its stages run
-// slower (one register allocation for all roles and stage shapes, 128 per thread), so at
-// the measured batches the per-layer launches win (profiles/r01_chain_*).
-int g_chain = -1;
-int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
-
-// The float control group (network_forward with ExecKernel::Float, network.cpp:350-420): the
-// same graph with conv_forward_float / linear_forward(Float) on the float weights (control.cu).
-int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
+// network_forward (network.cpp:330-420), one reference operator (or fused pair) per kernel,
+// float activations ping-ponging between two arena buffers. Weighted layers run as
+//   binary: K2 binary im2col / K1 pack_cols(sign) + K3 xnor GEMM with the bias epilogue
+//           (conv_forward_binary, linear_forward_packed: network.cpp:65-79, 121-126)
+//   float : float im2col + float_gemm on the float weights (conv_forward_float,
+//           linear_forward Float: network.cpp:50-63, 113-120; control.cu)
+//   binref: sign(im2col) / sign(x) + float_gemm on sign(weights) (conv_forward_binary_reference,
+//           linear_forward_binary_reference: network.cpp:81-94, 128-131) -- the verify oracle
+//   naive : direct convolution (conv_forward_naive, network.cpp:96-111); linear as float
+int forward_layerwise(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     BNN_TRY(ensure_arena(net, B));
     size_t launches = 0;
     const float* cur = x;
@@ -604,17 +555,42 @@ int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     for (size_t li = 0; li < net->layers.size(); ++li) {
         Layer& L = *net->layers[li];
         EventPair layer_ev(net, li, 0, s);
+        const int ex = layer_exec(net, L);
         switch (L.spec.kind) {
             case BNN_LAYER_CONV: {
                 float* out = next();
-                const size_t N = B * L.out_h * L.out_w;
-                if (net->fcols.bytes < L.cols * N * 4) BNN_TRY(net->fcols.alloc(L.cols * N * 4));
-                BNN_TRY(launch_im2col_f32(cur, B, L.in_c, L.in_h, L.in_w, &L.geom, net->fcols.as<float>(), s));
-                EventPair gemm_ev(net, li, 1, s);
-                BNN_TRY(launch_float_gemm(L.wf.as<float>(), net->fcols.as<float>(), L.rows, N, L.cols,
-                                          L.bias.as<float>(), L.out_h * L.out_w, out, s));
-                gemm_ev.close();
-                launches += 2;
+                const size_t N = B * L.out_h * L.out_w, P = L.out_h * L.out_w;
+                if (ex == EXEC_BINARY) {
+                    BNN_TRY(launch_im2col_sign_pack(cur, B, L.in_c, L.in_h, L.in_w, &L.geom,
+                                                    net->lines.as<uint32_t>(), L.wpl, s));
+                    EventPair gemm_ev(net, li, 1, s);
+                    BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl, L.rows, N,
+                                     L.cols, L.bias.as<float>(), P, out, s));
+                    gemm_ev.close();
+                    launches += 2;
+                } else if (ex == EXEC_NAIVE) {
+                    EventPair gemm_ev(net, li, 1, s);
+                    BNN_TRY(launch_naive_conv(cur, B, L.in_c, L.in_h, L.in_w, L.wf.as<float>(), L.bias.as<float>(),
+                                              &L.geom, out, s));
+                    gemm_ev.close();
+                    ++launches;
+                } else {
+                    if (net->fcols.bytes < L.cols * N * 4) BNN_TRY(net->fcols.alloc(L.cols * N * 4));
+                    float* cols = net->fcols.as<float>();
+                    BNN_TRY(launch_im2col_f32(cur, B, L.in_c, L.in_h, L.in_w, &L.geom, cols, s));
+                    ++launches;
+                    const float* w = L.wf.as<float>();
+                    if (ex == EXEC_BINREF) {
+                        BNN_TRY(launch_unary(0, cols, L.cols * N, cols, s));  // sign(im2col(x))
+                        BNN_TRY(ensure_wpm1(L, s));
+                        w = L.wpm1.as<float>();
+                        ++launches;
+                    }
+                    EventPair gemm_ev(net, li, 1, s);
+                    BNN_TRY(launch_float_gemm(w, cols, L.rows, N, L.cols, L.bias.as<float>(), P, out, s));
+                    gemm_ev.close();
+                    ++launches;
+                }
                 cur = out;
                 break;
             }
@@ -625,12 +601,32 @@ int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
                     ++launches;
                     cur = t;
                 }
-                float* out = next();
-                EventPair gemm_ev(net, li, 1, s);
-                BNN_TRY(launch_float_gemm(L.wf.as<float>(), cur, L.rows, B, L.cols, L.bias.as<float>(), B, out, s));
-                gemm_ev.close();
-                ++launches;
-                cur = out;
+                if (ex == EXEC_BINARY) {
+                    float* out = next();
+                    BNN_TRY(launch_pack_cols(cur, L.cols, B, net->lines.as<uint32_t>(), L.wpl, nullptr, s));
+                    EventPair gemm_ev(net, li, 1, s);
+                    BNN_TRY(gemm_f32(L.packed.as<uint32_t>(), L.wpl, net->lines.as<uint32_t>(), L.wpl, L.rows, B,
+                                     L.cols, L.bias.as<float>(), B, out, s));
+                    gemm_ev.close();
+                    launches += 2;
+                    cur = out;
+                } else {
+                    const float* w = L.wf.as<float>();
+                    if (ex == EXEC_BINREF) {
+                        float* t = next();
+                        BNN_TRY(launch_unary(0, cur, L.cols * B, t, s));  // sign(x)
+                        BNN_TRY(ensure_wpm1(L, s));
+                        w = L.wpm1.as<float>();
+                        ++launches;
+                        cur = t;
+                    }
+                    float* out = next();
+                    EventPair gemm_ev(net, li, 1, s);
+                    BNN_TRY(launch_float_gemm(w, cur, L.rows, B, L.cols, L.bias.as<float>(), B, out, s));
+                    gemm_ev.close();
+                    ++launches;
+                    cur = out;
+                }
                 break;
             }
             case BNN_LAYER_MAXPOOL: {
@@ -671,6 +667,14 @@ int forward_float(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     net->last_launches = launches;
     return BNN_OK;
 }
+
+
+// bnn_set_fused_chain / BNN_FUSED_CHAIN: 1 one chained launch, 0 (default) one launch per
+// weighted layer. The chained kernel removes the ~3-4 us launch boundaries but its stages run
+// slower (one register allocation for all roles and stage shapes, 128 per thread), so at
+// the measured batches the per-layer launches win (profiles/r01_chain_*).
+int g_chain = -1;
+int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
 
 // Swapped-operand conv kernel (fused_swap_kernel: channels on the MMA's M, positions on N)
 // for conv layers with a packed-bit epilogue. BNN_FUSED_SWAP / bnn_set_fused_swap: 1 (default)
@@ -858,8 +862,16 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     return BNN_OK;
 }
 
+// The fused engine serves ExecKernel::Binary: engine AUTO / FUSED, or PER_LAYER with every
+// weighted layer's KernelChoice Binary.
 bool use_fused(const bnn_net* net) {
-    return net->fusable && net->engine_policy != BNN_ENGINE_GENERIC;
+    if (!net->fusable) return false;
+    if (net->engine_policy == BNN_ENGINE_AUTO || net->engine_policy == BNN_ENGINE_FUSED) return true;
+    if (net->engine_policy != BNN_ENGINE_PER_LAYER) return false;
+    for (const auto& L : net->layers)
+        if ((L->spec.kind == BNN_LAYER_CONV || L->spec.kind == BNN_LAYER_LINEAR) && L->spec.kernel != BNN_KERNEL_BINARY)
+            return false;
+    return true;
 }
 
 // The fused forward is a fixed sequence of ~10 launches; for a repeated (x, B, logits, stream)
@@ -914,9 +926,8 @@ int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaS
 
 int forward(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (B == 0) return fail(BNN_E_CONFIG, "batch must be >= 1");
-    if (net->engine_policy == BNN_ENGINE_FLOAT) return forward_float(net, x, B, logits, s);
     if (use_fused(net)) return forward_graphed(net, x, B, logits, s);
-    return forward_generic(net, x, B, logits, s);
+    return forward_layerwise(net, x, B, logits, s);
 }
 }  // namespace
 }  // namespace bnnk
@@ -930,6 +941,7 @@ size_t bnn_default_spec(bnn_layer_spec* out, size_t cap) {  // network.cpp:422-4
     auto conv = [&](uint64_t d) {
         bnn_layer_spec s{};
         s.kind = BNN_LAYER_CONV;
+        s.kernel = BNN_KERNEL_BINARY;
         s.out_channels = d;
         s.kernel_h = s.kernel_w = 3;
         s.stride_h = s.stride_w = 1;
@@ -945,6 +957,7 @@ size_t bnn_default_spec(bnn_layer_spec* out, size_t cap) {  // network.cpp:422-4
     auto linear = [&](uint64_t f) {
         bnn_layer_spec s{};
         s.kind = BNN_LAYER_LINEAR;
+        s.kernel = BNN_KERNEL_BINARY;
         s.out_features = f;
         s.stride_h = s.stride_w = 1;
         l.push_back(s);
@@ -969,12 +982,12 @@ size_t bnn_default_spec(bnn_layer_spec* out, size_t cap) {  // network.cpp:422-4
 
 int bnn_net_create(const bnn_layer_spec* layers, size_t n_layers, size_t in_c, size_t in_h,
                    size_t in_w, uint64_t seed, int binarize_weights, bnn_net** out) {
-    (void)binarize_weights;  // sign(sign(w)) == sign(w): packed bits do not depend on it
     BNN_TRY(require_sm100());
     if (n_layers == 0) return fail(BNN_E_SHAPE, "network has no layers");
     if (in_c == 0 || in_h == 0 || in_w == 0) return fail(BNN_E_SHAPE, "input extents must be >= 1");
     auto net = std::make_unique<bnn_net>();
     net->in_c = in_c, net->in_h = in_h, net->in_w = in_w;
+    net->binarize = binarize_weights != 0;  // float weights sign()ed; packed bits are the same either way
     cudaStream_t s;
     BNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     int rc = build(net.get(), layers, n_layers, seed, s);
@@ -998,7 +1011,7 @@ void bnn_net_destroy(bnn_net* net) {
 size_t bnn_net_logits(const bnn_net* net) { return net->logits; }
 
 int bnn_net_set_engine(bnn_net* net, int policy) {
-    if (policy < BNN_ENGINE_AUTO || policy > BNN_ENGINE_FLOAT)
+    if (policy < BNN_ENGINE_AUTO || policy > BNN_ENGINE_PER_LAYER)
         return fail(BNN_E_CONFIG, "bad engine policy");
     if (policy == BNN_ENGINE_FUSED && !net->fusable)
         return fail(BNN_E_CONFIG, "network is not fusable: " + net->unfusable_why);
@@ -1033,7 +1046,7 @@ int bnn_set_fused_split(int split) {
 int bnn_debug_timeline(int op) { return fused_timeline(op); }
 
 const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer) {
-    if (net->engine_policy != BNN_ENGINE_FLOAT && use_fused(net))
+    if (use_fused(net))
         for (const auto& st : net->stages)
             if (st->layer == layer) return st->kname;
     return "";
@@ -1083,8 +1096,14 @@ int bnn_set_fused_tmem_a(int enabled) {
 }
 
 int bnn_net_engine(const bnn_net* net) {
-    if (net->engine_policy == BNN_ENGINE_FLOAT) return BNN_ENGINE_FLOAT;
-    return use_fused(net) ? BNN_ENGINE_FUSED : BNN_ENGINE_GENERIC;
+    if (use_fused(net)) return BNN_ENGINE_FUSED;
+    switch (net->engine_policy) {
+        case BNN_ENGINE_FLOAT:
+        case BNN_ENGINE_BINARY_REFERENCE:
+        case BNN_ENGINE_NAIVE:
+        case BNN_ENGINE_PER_LAYER: return net->engine_policy;
+        default: return BNN_ENGINE_GENERIC;
+    }
 }
 size_t bnn_net_num_layers(const bnn_net* net) { return net->layers.size(); }
 size_t bnn_net_last_launches(const bnn_net* net) { return net->last_launches; }
@@ -1103,6 +1122,56 @@ int bnn_net_layer_params(const bnn_net* net, size_t i, uint32_t* packed, size_t*
     if (bias && L.rows) BNN_CUDA(cudaMemcpy(bias, L.bias.p, L.rows * 4, cudaMemcpyDeviceToHost));
     if (scale && L.n_affine) BNN_CUDA(cudaMemcpy(scale, L.scale.p, L.n_affine * 4, cudaMemcpyDeviceToHost));
     if (shift && L.n_affine) BNN_CUDA(cudaMemcpy(shift, L.shift.p, L.n_affine * 4, cudaMemcpyDeviceToHost));
+    return BNN_OK;
+}
+
+int bnn_net_layer_data(const bnn_net* net, size_t i, uint32_t* packed, float* weights, float* bias, float* scale,
+                       float* shift) {
+    if (i >= net->layers.size()) return fail(BNN_E_CONFIG, "layer index out of range");
+    const Layer& L = *net->layers[i];
+    if (weights && L.rows) BNN_CUDA(cudaMemcpy(weights, L.wf.p, L.rows * L.cols * 4, cudaMemcpyDeviceToHost));
+    return bnn_net_layer_params(net, i, packed, nullptr, nullptr, bias, scale, shift);
+}
+
+int bnn_net_set_layer_data(bnn_net* net, size_t i, const uint32_t* packed, const float* weights, const float* bias,
+                           const float* scale, const float* shift) {
+    if (i >= net->layers.size()) return fail(BNN_E_CONFIG, "layer index out of range");
+    Layer& L = *net->layers[i];
+    BNN_CUDA(cudaDeviceSynchronize());  // no forward in flight reads the old parameters
+    if (L.rows) {
+        if (packed) BNN_CUDA(cudaMemcpy(L.packed.p, packed, L.rows * L.wpl * 4, cudaMemcpyHostToDevice));
+        if (weights) {
+            BNN_CUDA(cudaMemcpy(L.wf.p, weights, L.rows * L.cols * 4, cudaMemcpyHostToDevice));
+            if (L.wpm1.p) {  // re-derived on next use
+                cudaFree(L.wpm1.p);
+                L.wpm1.p = nullptr, L.wpm1.bytes = 0;
+            }
+        }
+        if (bias) BNN_CUDA(cudaMemcpy(L.bias.p, bias, L.rows * 4, cudaMemcpyHostToDevice));
+    }
+    if (L.n_affine) {
+        if (scale) BNN_CUDA(cudaMemcpy(L.scale.p, scale, L.n_affine * 4, cudaMemcpyHostToDevice));
+        if (shift) BNN_CUDA(cudaMemcpy(L.shift.p, shift, L.n_affine * 4, cudaMemcpyHostToDevice));
+    }
+    if (packed || bias || scale || shift) {  // the fused engine's prepared operands derive from these
+        net->drop_graphs();
+        cudaStream_t s;
+        BNN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const int rc = plan_fused(net, s);
+        cudaStreamDestroy(s);
+        BNN_TRY(rc);
+        if (net->engine_policy == BNN_ENGINE_FUSED && !net->fusable) net->engine_policy = BNN_ENGINE_AUTO;
+    }
+    return BNN_OK;
+}
+
+int bnn_net_set_layer_kernel(bnn_net* net, size_t i, int kernel) {
+    if (i >= net->layers.size()) return fail(BNN_E_CONFIG, "layer index out of range");
+    if (kernel < BNN_KERNEL_FLOAT || kernel > BNN_KERNEL_NAIVE) return fail(BNN_E_CONFIG, "bad kernel choice");
+    if (net->layers[i]->spec.kernel != uint32_t(kernel)) {
+        net->layers[i]->spec.kernel = uint32_t(kernel);
+        net->drop_graphs();
+    }
     return BNN_OK;
 }
 
@@ -1214,26 +1283,36 @@ int bnn_pipe_create(bnn_net* net, size_t batch, int depth, bnn_pipe** out) {
     auto p = std::make_unique<bnn_pipe>();
     p->net = net, p->batch = batch, p->depth = depth;
     p->nx = batch * net->in_c * net->in_h * net->in_w, p->ny = batch * net->logits;
-    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
-    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_run, cudaStreamNonBlocking));
-    BNN_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
-    for (int k = 0; k < depth; ++k) {
-        float *x = nullptr, *y = nullptr;
-        BNN_CUDA(cudaMalloc(&x, p->nx * 4));
-        p->dx.push_back(x);
-        BNN_CUDA(cudaMalloc(&y, p->ny * 4));
-        p->dy.push_back(y);
-        cudaEvent_t e[3];
-        for (auto& ev : e) BNN_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        p->ev_in.push_back(e[0]), p->ev_run.push_back(e[1]), p->ev_out.push_back(e[2]);
+    auto build = [&]() -> int {
+        BNN_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+        BNN_CUDA(cudaStreamCreateWithFlags(&p->s_run, cudaStreamNonBlocking));
+        BNN_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+        for (int k = 0; k < depth; ++k) {
+            float *x = nullptr, *y = nullptr;
+            BNN_CUDA(cudaMalloc(&x, p->nx * 4));
+            p->dx.push_back(x);
+            BNN_CUDA(cudaMalloc(&y, p->ny * 4));
+            p->dy.push_back(y);
+            for (auto* evs : {&p->ev_in, &p->ev_run, &p->ev_out}) {
+                cudaEvent_t e = nullptr;
+                BNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                evs->push_back(e);
+            }
+        }
+        return BNN_OK;
+    };
+    if (int rc = build()) {  // release whatever was created before the failure
+        bnn_pipe_destroy(p.release());
+        return rc;
     }
     *out = p.release();
     return BNN_OK;
 }
 
 // Enqueue one batch: x [batch, C, H, W] and logits [features, batch] are host buffers (pinned
-// for asynchronous copies). Returns its sequence number in *seq. The caller must not reuse
-// `logits` before bnn_pipe_wait(seq), nor have more than `depth` batches outstanding.
+// for asynchronous copies). Returns its sequence number in *seq. The H2D copy of `x` and the D2H
+// copy into `logits` are asynchronous: the caller must not modify `x` nor read or reuse `logits`
+// before bnn_pipe_wait(seq) returns, nor have more than `depth` batches outstanding.
 int bnn_pipe_submit(bnn_pipe* p, const float* x, float* logits, uint64_t* seq) {
     if (!p) return fail(BNN_E_CONFIG, "pipe: null");
     const int k = int(p->submitted % uint64_t(p->depth));

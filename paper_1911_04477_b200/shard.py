@@ -45,3 +45,10 @@ def gather_logits(local, global_batch: int, group=None):
     dist.all_gather(parts, buf, group=group)
     out = torch.cat([p[:, :shard_range(global_batch, world, r)[1]] for r, p in enumerate(parts)], dim=1)
     return out
+
+
+def assemble_gathered(gathered):
+    """[world, F, B] (all_gather_into_tensor of equal [F, B] shards, rank-major) -> the global
+    [F, world*B] logits in the reference's [features, batch] layout, images in rank order."""
+    world, F, B = gathered.shape
+    return gathered.permute(1, 0, 2).reshape(F, world * B)

@@ -72,3 +72,24 @@ def test_two_rank_shard_and_gather_equals_full_batch(gb):
     orc = Oracle()
     full = orc.fill_random((gb, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     assert np.array_equal(got, orc.net(seed=1).forward(full))
+
+
+def test_bench_driver_two_ranks_gloo_stub():
+    """bench.py's own N > 1 path (shards, per-step logits gather, max-over-ranks timing, global
+    assembly and the parity of the timed output) under torchrun with 2 CPU ranks over gloo, the
+    device forward replaced by the reference (--stub-oracle): one well-formed line, parity true."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(root, "bench.py"),
+           "--stub-oracle", "--gpus", "2", "--batch", "2", "--steps", "2", "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 4 and d["value"] > 0
+    assert d["parity_vs_oracle"] is True, d["parity"]
