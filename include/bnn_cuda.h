@@ -315,6 +315,11 @@ const char* bnn_net_layer_kernel(const bnn_net* net, size_t layer);
  * swapped-operand conv kernel: 0 off, 1 (default) every conv with a packed-bit input, 2 also
  * the pixel-input first conv. Bit-exact in every mode. */
 int bnn_set_fused_fp4(int mode);
+/* Fused engine: the halo-tile FP4 conv (halo4_kernel) for "same" convs (3x3 pad 1, 1x1, ...,
+ * stride 1) with a packed-bit input whose weights fit in shared memory: each input pixel is
+ * expanded to e2m1 once per tile instead of once per tap. 0 off (fused_swap4_kernel), 1
+ * (default) on. Bit-exact either way. */
+int bnn_set_fused_halo(int enabled);
 /* Fused engine: FP4 swapped conv on CTA pairs (cta_group::2, 256 channels per pair: each SM
  * expands half the activation rows) for layers with >= 256 channels: 0 off, 1 (default) on.
  * Positions per tile (pairs and the 128-channel kernel): 192 or 224, whichever needs fewer

@@ -60,6 +60,28 @@ struct FusedGeom {
     int kb4, kq4;             // FP4 path: 256-element K blocks, 64-element K steps in the last
 };
 
+// Halo-tile FP4 conv (halo.cu): "same" convs with packed-bit input, weights resident in shared
+// memory, activations expanded once per pixel into a padded-canvas halo tile.
+constexpr int kHaloMaxSteps = 128;  // K / 64 (K <= 8192)
+struct HaloGeom {
+    const uint32_t* in;  // packed NHWC bits [B, H, W, Cw]
+    uint32_t* out;       // packed NHWC bits [B, OH', OW', Dw] (pooled or not)
+    const int4* prm;     // per-channel (Tu, flip, ...) from prep_params_kernel
+    int B, H, W, Cw, D, Dw, pool;
+    int G, S, Q, P;      // canvas: images per canvas row, rows per image, columns per image, pitch
+    int TR, N, NH, nst;  // canvas rows per tile, MMA N, halo rows, halo stages
+    int n_tiles, m_tiles, total_rows, grid;
+    int steps, KB4;      // K / 64 MMA steps, 256-element weight blocks
+    size_t smem;
+    FastDiv dP, dS, dQ, dWh, dG;
+    unsigned long long* dbg;  // BNN_HALO_PROFILE counters, else null
+    int dbg_mode;             // profiling experiments (results invalid): 1 no epilogue, 2 no halo fill, 4 no MMA
+    int taps, cpt;            // taps (<= 9), K64 steps per tap (C / 64)
+    int toff[9];              // canvas shift of tap t, in pixels (= 16-byte halo rows)
+};
+bool halo4_plan(const FusedGeom& g, HaloGeom& h);
+int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s);
+
 // Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.
 constexpr int kChainMaxStages = 10;
 struct ChainStage {

@@ -706,6 +706,16 @@ bool use_fp4(const bnn_net* net, const FusedStage& st, int cg) {
     return g_fp4 == 2 || st.in_mode == FIN_BITS;
 }
 
+// Halo-tile FP4 conv (halo.cu, halo4_kernel): BNN_FUSED_HALO / bnn_set_fused_halo: 0 off, 1
+// (default) every "same" conv with a packed-bit input whose weight slice fits in shared memory;
+// the others keep fused_swap4_kernel.
+int g_halo = -1;
+
+bool use_halo(const bnn_net* net, const FusedStage& st, int cg) {
+    if (g_halo < 0) g_halo = getenv("BNN_FUSED_HALO") ? atoi(getenv("BNN_FUSED_HALO")) : 1;
+    return g_halo != 0 && use_fp4(net, st, cg) && st.in_mode == FIN_BITS;
+}
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -816,6 +826,8 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             if (pix_f32) gp.in = x;
             BNN_TRY(launch_pix_popc(gp, st.pix, pix_f32, s));
         }
+        else if (HaloGeom hg; use_halo(net, st, plans[i].cg) && halo4_plan(g, hg))
+            BNN_TRY(launch_halo4(st.tm4, hg, s));
         else if (use_fp4(net, st, plans[i].cg))
             BNN_TRY(launch_swap4(st.in_mode, st.tm4, g, s));
         else if (use_swap(net, st, plans[i].cg))
@@ -879,7 +891,7 @@ bool use_fused(const bnn_net* net) {
 // with per-layer timing (events), the profiling mode, or the legacy default stream (which
 // cannot be captured).
 int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
-    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
+    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr || getenv("BNN_HALO_PROFILE") != nullptr;
     const bool graphable = net->use_graphs && !net->timing && !prof && s != nullptr;
     if (!graphable) return forward_fused(net, x, B, logits, s);
     // small cache: a pipelined caller alternates input/output buffers
@@ -1069,6 +1081,13 @@ int bnn_set_fused_fp4(int mode) {
     if (mode < 0 || mode > 2) return fail(BNN_E_CONFIG, "fused fp4: 0 (off), 1 (swapped layers) or 2 (all convs)");
     g_fp4 = mode;
     ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_set_fused_halo(int enabled) {
+    if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused halo: 0 (off) or 1 (on)");
+    g_halo = enabled;
+    ++g_tiling_epoch;  // captured graphs hold the other kernels
     return BNN_OK;
 }
 
