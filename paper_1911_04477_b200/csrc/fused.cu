@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     wc.wait(&full[stage], phase, 1);
                     tc_fence_after();
-                    if (lane == 0) {
+                    {  // the converged warp issues (one elected lane): see mma_i8_w
                         const uint32_t a0 = smem_u32(sA + size_t(stage) * kRows * kKB);
                         const uint32_t b0 = smem_u32(sB + size_t(stage) * BH * kKB);
                         // K steps past the layer's K in its last block multiply zeros: skip them
@@ -475,21 +475,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = 0; k < kKB / 32; ++k) {
                             if (k >= nk) break;
                             if (ATM)
-                                mma_i8_ts(d_tmem, tmem_base + uint32_t(TP::kACol + stage * TP::kAStage + 8 * k),
-                                          sdesc_k_sw128(b0 + 32 * k), idesc, (kb != kb0 || k != 0));
+                                mma_i8_ts_w(d_tmem, tmem_base + uint32_t(TP::kACol + stage * TP::kAStage + 8 * k),
+                                            sdesc_k_sw128(b0 + 32 * k), idesc, (kb != kb0 || k != 0));
                             else if (CG == 2)
-                                mma_i8_cg2(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                           (kb != kb0 || k != 0));
+                                mma_i8_cg2_w(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                             (kb != kb0 || k != 0));
                             else
-                                mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                                       (kb != kb0 || k != 0));
+                                mma_i8_w(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                         (kb != kb0 || k != 0));
                         }
                         if (CG == 2) {
-                            mma_commit_cg2_mc(&empty[stage], 3);  // both CTAs' slots free
-                            if (kb == kb1 - 1) mma_commit_cg2_mc(&tfull[acc], 3);
+                            mma_commit_cg2_mc_w(&empty[stage], 3);  // both CTAs' slots free
+                            if (kb == kb1 - 1) mma_commit_cg2_mc_w(&tfull[acc], 3);
                         } else {
-                            mma_commit(&empty[stage]);
-                            if (kb == kb1 - 1) mma_commit(&tfull[acc]);
+                            mma_commit_w(&empty[stage]);
+                            if (kb == kb1 - 1) mma_commit_w(&tfull[acc]);
                         }
                     }
                     __syncwarp();
@@ -1467,18 +1467,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < KB; ++kb) {
                 wc.wait(&full[stage], phase, 1);
                 tc_fence_after();
-                if (lane == 0) {
+                {  // the converged warp issues (one elected lane): see mma_i8_w
                     const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
                     const uint32_t b0 = smem_u32(sX + size_t(stage) * kSwN * kKB);
                     const int nk = kb == KB - 1 ? g.kq_last : kKB / 32;  // K steps past K: zeros
 #pragma unroll
                     for (int k = 0; k < kKB / 32; ++k) {
                         if (k >= nk) break;
-                        mma_i8(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
-                               (kb != 0 || k != 0));
+                        mma_i8_w(d_tmem, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                 (kb != 0 || k != 0));
                     }
-                    mma_commit(&empty[stage]);
-                    if (kb == KB - 1) mma_commit(&tfull[acc]);
+                    mma_commit_w(&empty[stage]);
+                    if (kb == KB - 1) mma_commit_w(&tfull[acc]);
                 }
                 __syncwarp();
                 if (++stage == kStages) stage = 0, phase ^= 1;
@@ -1924,22 +1924,25 @@ __device__ __forceinline__ void put_word4(uint32_t tile, int r, int chunk, uint3
               (w >> 2) & 0x22222222u);
 }
 
+// Issued by the whole converged warp (one elected lane), see mma_i8_w in umma.cuh.
 template <int CG = 1>
 __device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
     if constexpr (CG == 2) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\t"
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
                 d_tmem),
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
             : "memory");
     } else {
         asm volatile(
-            "{\n\t.reg .pred p;\n\t"
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
                 d_tmem),
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
             : "memory");
@@ -2094,7 +2097,7 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
             for (int kb = 0; kb < KB; ++kb) {
                 wc.wait(&full[stage], phase, 1);
                 tc_fence_after();
-                if (lane == 0) {
+                {  // the converged warp issues (one elected lane): see mma_i8_w
                     const uint32_t a0 = smem_u32(sW + size_t(stage) * kRows * kKB);
                     const uint32_t b0 = smem_u32(sX + size_t(stage) * kBH * kKB);
                     const int nk = kb == KB - 1 ? g.kq4 : kKB / 32;  // 64-element K steps past K: zeros
@@ -2106,11 +2109,11 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
                                      (kb != 0 || k != 0));
                     }
                     if (CG == 2) {
-                        mma_commit_cg2_mc(&empty[stage], 3);  // both CTAs' slots free
-                        if (kb == KB - 1) mma_commit_cg2_mc(&tfull[acc], 3);
+                        mma_commit_cg2_mc_w(&empty[stage], 3);  // both CTAs' slots free
+                        if (kb == KB - 1) mma_commit_cg2_mc_w(&tfull[acc], 3);
                     } else {
-                        mma_commit(&empty[stage]);
-                        if (kb == KB - 1) mma_commit(&tfull[acc]);
+                        mma_commit_w(&empty[stage]);
+                        if (kb == KB - 1) mma_commit_w(&tfull[acc]);
                     }
                 }
                 __syncwarp();
