@@ -320,6 +320,11 @@ int bnn_set_fused_fp4(int mode);
  * expanded to e2m1 once per tile instead of once per tap. 0 off (fused_swap4_kernel), 1
  * (default) on. Bit-exact either way. */
 int bnn_set_fused_halo(int enabled);
+/* Fused engine: linear layers on the FP4 tensor-core kernel (lin4_kernel: e2m1 weights by TMA,
+ * packed input bits expanded in shared memory, K split over CTAs with an exact integer
+ * reduction in lin_finish_kernel) instead of the int8 fused_layer_kernel. 0 off, 1 (default)
+ * on. Bit-exact either way. */
+int bnn_set_fused_lin4(int enabled);
 /* Fused engine: FP4 swapped conv on CTA pairs (cta_group::2, 256 channels per pair: each SM
  * expands half the activation rows) for layers with >= 256 channels: 0 off, 1 (default) on.
  * Positions per tile (pairs and the 128-channel kernel): 192 or 224, whichever needs fewer

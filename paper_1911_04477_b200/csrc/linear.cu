@@ -1,0 +1,389 @@
+// FP4 (kind::mxf4) binary linear layer with split-K, for the fused engine's linear stages:
+//
+//   linear_forward_packed (network.cpp:113-126) = xnor_gemm(W, pack_cols(sign x)) -> to_float
+//   -> bias_add, then (between layers) affine_norm -> htanh -> sign (network.cpp:151-175)
+//
+// The operands are the same exact e2m1 encodings as the FP4 conv kernels (fused.cu, halo.cu):
+// weights {-1.0, +1.0} (prep_weights4, engine K order), activations {0.0, 1.0} (the packed bits
+// of the previous layer, expanded in shared memory), block scales 2^0, so the f32 accumulator
+// is the exact integer u = sum bit * w and the reference's xnor value is 2u - S_d.
+//
+// Tiles: 128 output features (UMMA M, the weight rows, TMA SW128) x NB images (UMMA N, the
+// batch rows, expanded by the producer warps) x a K slice. The small-batch layers of the default
+// network have few (feature, image) tiles and a deep K (fc 8192 -> 1024 at batch 256: 8 tiles),
+// so K is split over CTAs: each slice writes its partial integer sums u (exact) to a workspace
+// [split][B][Dpad] and lin_finish_kernel adds the slices and applies the epilogue: the next
+// layer's packed bits (u >= Tu) ^ flip, or the logits float(2u - S_d) + bias in the reference's
+// [features, batch] layout. Integer sums are order-independent, so the split is bit-exact.
+// Without a split the tile's epilogue is final.
+//
+// CTA anatomy (448 threads): warp 0 weight TMA, warp 1 TMEM allocator + MMA issuer (the
+// converged warp, one elected lane), warps 2-5 epilogue (lane = output feature), warps 6-13
+// producers (thread = image row of the tile: its packed words -> e2m1 nibbles, SW128).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "bnn_common.cuh"
+#include "fused.cuh"
+#include "umma.cuh"
+
+namespace bnnk {
+
+using namespace umma;
+
+namespace {
+
+constexpr int kLThreads = 448;
+constexpr int kLStages = 4;
+constexpr int kLSfCol = 496;
+constexpr int kLPre = 4;  // producer prefetch depth in K blocks
+constexpr size_t kLSmem = 1024 + size_t(kLStages) * (16384 + 256 * 128) + 256;
+
+__host__ __device__ constexpr uint32_t idesc_mxf4_m128(int N) {
+    return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_mxf4_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf)
+        : "memory");
+}
+
+// 32 activation bits -> 16 bytes of e2m1 nibbles at 16-byte chunk `chunk` of 128-byte row r of a
+// SW128 tile (element 8s + n holds bit 4n + s: put_word4's order, matched by prep_weights4).
+__device__ __forceinline__ void put_word4_sw(uint32_t tile, int r, int chunk, uint32_t w) {
+    st_shared_v4(tile + uint32_t(r) * 128u + (uint32_t(chunk ^ (r & 7)) << 4), (w << 1) & 0x22222222u,
+                 w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kLThreads, 1)
+    lin4_kernel(const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ LinGeom g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sA = smem_raw + (base - raw);                       // [kLStages][128 rows x 128 B] weights
+    uint8_t* sB = sA + size_t(kLStages) * 16384;                  // [kLStages][NB rows x 128 B] images
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kLStages) * g.NB * 128);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kLStages;
+    uint64_t* tfull = bars + 2 * kLStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int units = g.m_tiles * g.n_tiles * g.ksplit;
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmW4);
+        for (int s = 0; s < kLStages; ++s) {
+            mbar_init(&full[s], 1 + 8);  // TMA arrive (expect_tx) + 8 producer warps
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 4);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp >= 2 && warp < 6) {  // block scales: every byte of columns [496, 512) = 2^0
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+        const uint32_t lb = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
+        tmem_st8(lb + kLSfCol, v);
+        tmem_st8(lb + kLSfCol + 8, v);
+        tmem_st_wait();
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // unit u -> (k slice, image tile, feature tile); slices of one tile are adjacent CTAs
+    auto decode = [&](int u, int& mt, int& nt, int& ks) {
+        ks = u % g.ksplit;
+        const int t = u / g.ksplit;
+        mt = t % g.m_tiles;
+        nt = t / g.m_tiles;
+    };
+    auto kb_range = [&](int ks, int& kb0, int& kb1) {
+        kb0 = ks * g.kbs;
+        kb1 = min(g.KB4, kb0 + g.kbs);
+    };
+
+    if (warp == 0) {
+        // weights: build-time constants, loaded ahead of the grid dependency
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int mt, nt, ks, kb0, kb1;
+                decode(u, mt, nt, ks);
+                kb_range(ks, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], 16384);
+                    tma_load_2d(&tmW4, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
+                    if (++stage == kLStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = idesc_mxf4_m128(g.NB);
+        int stage = 0, i = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            int mt, nt, ks, kb0, kb1;
+            decode(u, mt, nt, ks);
+            kb_range(ks, kb0, kb1);
+            mbar_wait(tempty, (i & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sA + size_t(stage) * 16384);
+                const uint32_t b0 = smem_u32(sB + size_t(stage) * g.NB * 128);
+                const int nk = kb == g.KB4 - 1 ? g.kq_last : 4;  // 64-element steps past K: zeros
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= nk) break;
+                    mma_mxf4_w(tmem_base, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                               tmem_base + kLSfCol, (kb != kb0 || k != 0));
+                }
+                mma_commit_w(&empty[stage]);
+                if (kb == kb1 - 1) mma_commit_w(tfull);
+                __syncwarp();
+                if (++stage == kLStages) stage = 0, phase ^= 1;
+            }
+        }
+        mbar_wait(tempty, (i & 1) ^ 1);  // the epilogue has read the last accumulator
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    } else if (warp < 6) {
+        // epilogue: lane = output feature d, TMEM columns = images
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const int q = warp & 3;
+        int i = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            int mt, nt, ks;
+            decode(u, mt, nt, ks);
+            const int d0 = mt * 128 + q * 32, d = d0 + lane, b0 = nt * g.NB;
+            const bool dvalid = d < g.D;
+            mbar_wait(tfull, i & 1);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16);
+            int4 pd = make_int4(0x7fffffff, 0, 0, 0);
+            if (g.ksplit == 1 && dvalid) pd = __ldg(g.prm + d);
+            const float Tf = float(pd.x);
+            const bool flip = pd.y != 0;
+            for (int c = 0; c < g.NB / 32 + ((g.NB & 31) ? 1 : 0); ++c) {
+                uint32_t v[32];
+                tmem_ld32(tb + uint32_t(32 * c), v);
+                tmem_ld_wait();
+                const int bc = b0 + 32 * c;
+                if (g.ksplit > 1) {
+                    // partial sums: ws[ks][b][d], one coalesced 128-byte row per image
+                    int* dst = g.ws + (size_t(ks) * g.B + bc) * g.Dpad + d;
+                    if (d < g.Dpad) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (bc + j < g.B && bc + j < b0 + g.NB) dst[size_t(j) * g.Dpad] = int(__uint_as_float(v[j]));
+                    }
+                } else if (g.epi == FEPI_BITS) {
+                    uint32_t mk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t w = __ballot_sync(0xffffffffu, (__uint_as_float(v[j]) >= Tf) != flip);
+                        if (lane == j) mk[j & 3] = w;
+                    }
+                    const uint32_t mine = (mk[0] | mk[1]) | (mk[2] | mk[3]);
+                    if (d0 < g.D && bc + lane < g.B && lane < g.NB - 32 * c)
+                        g.out_bits[size_t(bc + lane) * g.Dw + (d0 >> 5)] = mine;
+                } else {
+                    // to_float(a) + bias (kernels.cpp:90-107): one rounding of an exact integer
+                    if (dvalid) {
+                        const float bias = __int_as_float(pd.w);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (bc + j < g.B && 32 * c + j < g.NB)
+                                g.out_f32[size_t(d) * g.ldo + bc + j] =
+                                    __fadd_rn(__int2float_rn(2 * int(__uint_as_float(v[j])) - pd.z), bias);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+        }
+    } else {
+        // producers: thread = image row r of the tile; per 256-element K block its 8 packed words
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const int r = int(threadIdx.x) - 6 * 32;  // 0..255
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int mt, nt, ks, kb0, kb1;
+            decode(u, mt, nt, ks);
+            kb_range(ks, kb0, kb1);
+            const int b = nt * g.NB + r;
+            const bool live = r < g.NB;
+            const bool real = live && b < g.B;
+            const uint32_t* src = g.in + size_t(real ? b : 0) * g.Kw;
+            const bool vec = (g.Kw & 3) == 0;
+            // the slice's words are loaded kLPre blocks ahead of their stage (one L2 round trip
+            // per kLPre blocks instead of one per block)
+            uint32_t pf[kLPre][8];
+            auto load_block = [&](int kb, uint32_t (&w)[8]) {
+                const int wq = 8 * kb;
+                if (real && vec && wq + 8 <= g.Kw) {
+                    const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + wq));
+                    const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + wq + 4));
+                    w[0] = lo.x, w[1] = lo.y, w[2] = lo.z, w[3] = lo.w, w[4] = hi.x, w[5] = hi.y, w[6] = hi.z, w[7] = hi.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) w[k] = (real && kb < kb1 && wq + k < g.Kw) ? __ldg(src + wq + k) : 0u;
+                }
+            };
+#pragma unroll
+            for (int p = 0; p < kLPre; ++p)
+                if (kb0 + p < kb1) load_block(kb0 + p, pf[p]);
+            for (int kb = kb0; kb < kb1; kb += kLPre) {
+#pragma unroll
+                for (int p = 0; p < kLPre; ++p) {
+                    if (kb + p >= kb1) break;
+                    uint32_t w[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) w[k] = pf[p][k];
+                    if (kb + p + kLPre < kb1) load_block(kb + p + kLPre, pf[p]);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t tile = smem_u32(sB + size_t(stage) * g.NB * 128);
+                    if (live) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) put_word4_sw(tile, r, k, w[k]);
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[stage]);
+                    if (++stage == kLStages) stage = 0, phase ^= 1;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+}
+
+// Split-K completion: u = sum of the slices' partial sums (exact), then the bits or logits
+// epilogue. Thread = (image, feature); a warp covers 32 consecutive features of one image.
+__global__ void __launch_bounds__(256) lin_finish_kernel(const LinGeom g) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = size_t(g.B) * g.Dpad;
+    if (i >= total) return;  // whole warps (Dpad % 32 == 0)
+    const int b = int(i / g.Dpad), d = int(i % g.Dpad);
+    int u = 0;
+    for (int s = 0; s < g.ksplit; ++s) u += __ldcg(g.ws + (size_t(s) * g.B + b) * g.Dpad + d);
+    if (g.epi == FEPI_BITS) {
+        const int4 pd = d < g.D ? __ldg(g.prm + d) : make_int4(0x7fffffff, 0, 0, 0);
+        const uint32_t w = __ballot_sync(0xffffffffu, (u >= pd.x) != (pd.y != 0));
+        if ((threadIdx.x & 31) == 0 && d < g.D) g.out_bits[size_t(b) * g.Dw + (d >> 5)] = w;
+    } else if (d < g.D) {
+        const int4 pd = __ldg(g.prm + d);
+        g.out_f32[size_t(d) * g.ldo + b] = __fadd_rn(__int2float_rn(2 * u - pd.z), __int_as_float(pd.w));
+    }
+}
+
+// Host plan: images per tile (NB, <= 256, a multiple of 16), feature tiles of 128 and the K
+// split that gives ~one wave of CTAs (at least 2 K blocks per slice, at most 8 slices).
+bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
+    if (fg.KH != 1 || fg.KW != 1 || fg.H != 1 || fg.W != 1) return false;
+    if (epi != FEPI_BITS && epi != FEPI_LOGITS) return false;
+    if (fg.Cw * 32 < fg.K || fg.kb4 <= 0) return false;
+    const int sms = num_sms();
+    l.in = static_cast<const uint32_t*>(fg.in);
+    l.B = fg.B, l.K = fg.K, l.Kw = fg.Cw, l.D = fg.D, l.Dw = (fg.D + 31) / 32;
+    l.KB4 = fg.kb4, l.kq_last = fg.kq4;
+    l.m_tiles = (fg.D + 127) / 128;
+    // (NB, split) by a cycle model per CTA: MMA steps x max(48, NB/2) cycles (the measured
+    // dispatch cost, tools/halo_probe.cu), the weight slice streamed at ~100 B/cycle, and
+    // ~6000 cycles for the partial-sum round trip and lin_finish_kernel when K is split. Small
+    // batches prefer narrow image tiles over a K split (fc 8192 -> 1024 at batch 256: 128 CTAs
+    // of 16 images instead of 8 tiles x 8 slices).
+    long best = -1;
+    for (int nb = 256; nb >= 16; nb /= 2) {
+        if (nb > 16 && nb / 2 >= (fg.B + 15) / 16 * 16) continue;  // narrower than the batch already
+        const int nbr = std::min(nb, (fg.B + 15) / 16 * 16);
+        const int nt = (fg.B + nbr - 1) / nbr;
+        const int tiles = l.m_tiles * nt;
+        for (int ks = 1; ks <= 8; ks *= 2) {
+            if (ks > 1 && (l.KB4 + ks - 1) / ks < 2) break;
+            const int kbs = (l.KB4 + ks - 1) / ks;
+            const long units = long(tiles) * ((l.KB4 + kbs - 1) / kbs);
+            const long rounds = (units + sms - 1) / sms;
+            const long mma = long(kbs) * 4 * std::max(48, nbr / 2);
+            const long wts = long(kbs) * 16384 / 100;
+            const long cost = rounds * std::max(mma, wts) + (ks > 1 ? 6000 : 0);
+            if (best < 0 || cost < best) {
+                best = cost;
+                l.NB = nbr, l.n_tiles = nt, l.kbs = kbs, l.ksplit = (l.KB4 + kbs - 1) / kbs;
+            }
+        }
+    }
+    l.Dpad = (fg.D + 31) / 32 * 32;
+    l.prm = fg.prm;
+    l.epi = epi;
+    l.out_bits = fg.out_bits;
+    l.out_f32 = fg.out_f32;
+    l.ldo = fg.ldo;
+    l.ws = nullptr;
+    return true;
+}
+
+size_t lin4_ws_bytes(const LinGeom& l) { return l.ksplit > 1 ? size_t(l.ksplit) * l.B * l.Dpad * sizeof(int) : 0; }
+
+int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(lin4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLSmem)));
+        attr_set = true;
+    }
+    const int units = l.m_tiles * l.n_tiles * l.ksplit;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min(units, num_sms())));
+    cfg.blockDim = dim3(unsigned(kLThreads));
+    cfg.dynamicSmemBytes = 1024 + size_t(kLStages) * (16384 + size_t(l.NB) * 128) + 256;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, l));
+    BNN_TRY(launch_check("lin4_kernel"));
+    if (l.ksplit > 1) {
+        const size_t total = size_t(l.B) * l.Dpad;
+        cfg.gridDim = dim3(unsigned(ceil_div(total, 256)));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = 0;
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin_finish_kernel, l));
+        BNN_TRY(launch_check("lin_finish_kernel"));
+    }
+    set_last_gemm("lin4_kernel");
+    return BNN_OK;
+}
+
+}  // namespace bnnk

@@ -157,6 +157,7 @@ struct bnn_net {
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix, ws, sem;
+    bnnk::DevBuf lin_ws;  // split-K partial sums of the FP4 linear kernel (lin4)
     bnnk::DevBuf chain_done;
     bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
 };
@@ -383,7 +384,8 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
         const int bns[5] = {16, 32, 64, 128, 256};
         for (int b = 0; b < 5; ++b)
             BNN_TRY(fused_make_tmap(&st->tm[b], st->w8.as<int8_t>(), st->Dpad, st->Kpad, bns[b]));
-        if (kind == BNN_LAYER_CONV && st->epi == FEPI_BITS && st->in_mode != FIN_F32) {  // FP4 operands
+        if ((kind == BNN_LAYER_CONV && st->epi == FEPI_BITS && st->in_mode != FIN_F32) ||
+            kind == BNN_LAYER_LINEAR) {  // FP4 operands (conv: swap4 / halo4; linear: lin4)
             const int Kpad4 = int(round_up(size_t(g.K), 256));
             g.kb4 = Kpad4 / 256;
             g.kq4 = (g.K - 256 * (g.kb4 - 1) + 63) / 64;
@@ -716,6 +718,17 @@ bool use_halo(const bnn_net* net, const FusedStage& st, int cg) {
     return g_halo != 0 && use_fp4(net, st, cg) && st.in_mode == FIN_BITS;
 }
 
+// FP4 linear layers (linear.cu, lin4_kernel + lin_finish_kernel): BNN_FUSED_LIN4 /
+// bnn_set_fused_lin4: 0 off (int8 fused_layer_kernel), 1 (default) every linear stage except the
+// CUDA-core logits layer.
+int g_lin4 = -1;
+
+bool use_lin4(const bnn_net* net, const FusedStage& st) {
+    if (g_lin4 < 0) g_lin4 = getenv("BNN_FUSED_LIN4") ? atoi(getenv("BNN_FUSED_LIN4")) : 1;
+    return g_lin4 != 0 && st.fp4_ok && g_forced_cg <= 0 && g_forced_bn <= 0 &&
+           net->layers[st.layer]->spec.kind == BNN_LAYER_LINEAR && st.in_mode == FIN_BITS;
+}
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -733,9 +746,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     struct Plan {
         FusedGeom g;
         int cg, bn;
+        bool lin4 = false;
+        LinGeom lg{};
     };
     std::vector<Plan> plans;
     size_t ws_need = 0, sem_need = 0;  // the largest split-K workspace of any stage
+    size_t lin_ws_need = 0;            // the largest lin4 partial-sum workspace
     const void* in = x;
     int which = 0;
     (void)prof;
@@ -767,7 +783,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             g.ldo = int(B);
         }
         if (st.in_mode == FIN_PIX || st.pre_encode) g.in = net->pix.as<uint32_t>();
-        plans.push_back({g, cg, bn});
+        Plan pl{g, cg, bn};
+        if (use_lin4(net, st) && !(st.small_logits && g_small_logits) && lin4_plan(g, st.epi, pl.lg)) {
+            pl.lin4 = true;
+            lin_ws_need = std::max(lin_ws_need, lin4_ws_bytes(pl.lg));
+        }
+        plans.push_back(pl);
         in = g.out_bits;
     }
     // Chained tail: stages [first_chained, n) run in ONE persistent launch (fused_chain_kernel),
@@ -797,8 +818,14 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         BNN_TRY(net->sem.alloc(sem_need));
         BNN_CUDA(cudaMemsetAsync(net->sem.p, 0, sem_need, s));  // kernels leave them at 0
     }
-    for (auto& pl : plans)
+    if (net->lin_ws.bytes < lin_ws_need) {
+        BNN_TRY(net->lin_ws.alloc(lin_ws_need));
+        ++net->arena_epoch;
+    }
+    for (auto& pl : plans) {
         if (pl.g.ksplit > 1) pl.g.ws = net->ws.as<int>(), pl.g.sem = net->sem.as<unsigned>();
+        if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>();
+    }
     size_t launches = 0;
     for (size_t i = 0; i < first_chained; ++i) {
         FusedStage& st = *net->stages[i];
@@ -826,6 +853,8 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             if (pix_f32) gp.in = x;
             BNN_TRY(launch_pix_popc(gp, st.pix, pix_f32, s));
         }
+        else if (plans[i].lin4)
+            BNN_TRY(launch_lin4(st.tm4, plans[i].lg, s));
         else if (HaloGeom hg; use_halo(net, st, plans[i].cg) && halo4_plan(g, hg))
             BNN_TRY(launch_halo4(st.tm4, hg, s));
         else if (use_fp4(net, st, plans[i].cg))
@@ -1081,6 +1110,13 @@ int bnn_set_fused_fp4(int mode) {
     if (mode < 0 || mode > 2) return fail(BNN_E_CONFIG, "fused fp4: 0 (off), 1 (swapped layers) or 2 (all convs)");
     g_fp4 = mode;
     ++g_tiling_epoch;
+    return BNN_OK;
+}
+
+int bnn_set_fused_lin4(int enabled) {
+    if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused lin4: 0 (off) or 1 (on)");
+    g_lin4 = enabled;
+    ++g_tiling_epoch;  // captured graphs hold the other kernels
     return BNN_OK;
 }
 
