@@ -83,23 +83,27 @@ bool halo4_plan(const FusedGeom& g, HaloGeom& h);
 int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s);
 
 // FP4 linear layer with split-K (linear.cu): weights [Dpad, Kpad4/2] e2m1 via tm4, input bits
-// [B, Kw]; ksplit > 1 writes partial sums to ws [ksplit][B][Dpad] and lin_finish_kernel applies
-// the epilogue.
+// [B, Kw]; ksplit > 1 writes partial sums to ws [ksplit][B][Dpad] and the tile's slices reduce
+// them in the same launch (counters sem, 2 per tile, zero between launches).
 struct LinGeom {
     const uint32_t* in;
     int B, K, Kw, D, Dw, Dpad;
     int KB4, kq_last;          // 256-element K blocks, 64-element steps in the last one
     int m_tiles, n_tiles, NB;  // 128-feature tiles, image tiles of NB (UMMA N)
     int ksplit, kbs;           // K slices, K blocks per slice
+    int nst;                   // smem ring stages (weights 16 KB + images NB x 128 B each)
     const int4* prm;
     int epi;                   // FEPI_BITS or FEPI_LOGITS
     uint32_t* out_bits;        // [B, Dw]
     float* out_f32;            // [D, ldo]
     int ldo;
     int* ws;
+    unsigned* sem;
+    unsigned long long* dbg;  // BNN_LIN4_PROFILE phase stamps, else null
 };
 bool lin4_plan(const FusedGeom& g, int epi, LinGeom& l);
 size_t lin4_ws_bytes(const LinGeom& l);
+size_t lin4_sem_count(const LinGeom& l);
 int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s);
 
 // Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.

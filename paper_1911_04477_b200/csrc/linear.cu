@@ -35,10 +35,10 @@ using namespace umma;
 namespace {
 
 constexpr int kLThreads = 448;
-constexpr int kLStages = 4;
+constexpr int kLStages = 12;  // maximum ring depth (the weight stream is latency-bound at small NB)
 constexpr int kLSfCol = 496;
 constexpr int kLPre = 4;  // producer prefetch depth in K blocks
-constexpr size_t kLSmem = 1024 + size_t(kLStages) * (16384 + 256 * 128) + 256;
+constexpr size_t kLSmem = 232448;  // 227 KB opt-in per CTA
 
 __host__ __device__ constexpr uint32_t idesc_mxf4_m128(int N) {
     return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
@@ -62,6 +62,18 @@ __device__ __forceinline__ void put_word4_sw(uint32_t tile, int r, int chunk, ui
                  w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
 }
 
+__device__ __forceinline__ unsigned long long lgtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kLThreads, 1)
@@ -69,9 +81,10 @@ __global__ void __launch_bounds__(kLThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t* sA = smem_raw + (base - raw);                       // [kLStages][128 rows x 128 B] weights
-    uint8_t* sB = sA + size_t(kLStages) * 16384;                  // [kLStages][NB rows x 128 B] images
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kLStages) * g.NB * 128);
+    const int nst = g.nst;
+    uint8_t* sA = smem_raw + (base - raw);                  // [nst][128 rows x 128 B] weights
+    uint8_t* sB = sA + size_t(nst) * 16384;                 // [nst][NB rows x 128 B] images
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(nst) * g.NB * 128);
     uint64_t* full = bars;
     uint64_t* empty = bars + kLStages;
     uint64_t* tfull = bars + 2 * kLStages;
@@ -81,9 +94,14 @@ __global__ void __launch_bounds__(kLThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     const int units = g.m_tiles * g.n_tiles * g.ksplit;
+    const unsigned long long t_start = g.dbg ? lgtimer() : 0;
+    // BNN_LIN4_PROFILE: per-phase times (ns since the CTA started, summed over CTAs)
+    auto stamp = [&](int k) {
+        if (g.dbg) atomicAdd(g.dbg + k, lgtimer() - t_start);
+    };
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW4);
-        for (int s = 0; s < kLStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1 + 8);  // TMA arrive (expect_tx) + 8 producer warps
             mbar_init(&empty[s], 1);
         }
@@ -136,7 +154,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], 16384);
                     tma_load_2d(&tmW4, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
-                    if (++stage == kLStages) stage = 0, phase ^= 1;
+                    if (++stage == nst) stage = 0, phase ^= 1;
                 }
             }
         }
@@ -165,7 +183,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 mma_commit_w(&empty[stage]);
                 if (kb == kb1 - 1) mma_commit_w(tfull);
                 __syncwarp();
-                if (++stage == kLStages) stage = 0, phase ^= 1;
+                if (++stage == nst) stage = 0, phase ^= 1;
             }
         }
         mbar_wait(tempty, (i & 1) ^ 1);  // the epilogue has read the last accumulator
@@ -181,7 +199,9 @@ __global__ void __launch_bounds__(kLThreads, 1)
             decode(u, mt, nt, ks);
             const int d0 = mt * 128 + q * 32, d = d0 + lane, b0 = nt * g.NB;
             const bool dvalid = d < g.D;
+            if (warp == 2 && lane == 0) stamp(0);
             mbar_wait(tfull, i & 1);
+            if (warp == 2 && lane == 0) stamp(1);
             tc_fence_after();
             const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16);
             int4 pd = make_int4(0x7fffffff, 0, 0, 0);
@@ -226,7 +246,9 @@ __global__ void __launch_bounds__(kLThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
+            if (warp == 2 && lane == 0) stamp(5);
         }
+        if (g.ksplit > 1) __threadfence();  // partial sums visible GPU-wide before the arrival
     } else {
         // producers: thread = image row r of the tile; per 256-element K block its 8 packed words
         asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -276,7 +298,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full[stage]);
-                    if (++stage == kLStages) stage = 0, phase ^= 1;
+                    if (++stage == nst) stage = 0, phase ^= 1;
                 }
             }
         }
@@ -284,27 +306,68 @@ __global__ void __launch_bounds__(kLThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
-}
-
-// Split-K completion: u = sum of the slices' partial sums (exact), then the bits or logits
-// epilogue. Thread = (image, feature); a warp covers 32 consecutive features of one image.
-__global__ void __launch_bounds__(256) lin_finish_kernel(const LinGeom g) {
-    asm volatile("griddepcontrol.launch_dependents;");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const size_t total = size_t(g.B) * g.Dpad;
-    if (i >= total) return;  // whole warps (Dpad % 32 == 0)
-    const int b = int(i / g.Dpad), d = int(i % g.Dpad);
-    int u = 0;
-    for (int s = 0; s < g.ksplit; ++s) u += __ldcg(g.ws + (size_t(s) * g.B + b) * g.Dpad + d);
-    if (g.epi == FEPI_BITS) {
-        const int4 pd = d < g.D ? __ldg(g.prm + d) : make_int4(0x7fffffff, 0, 0, 0);
-        const uint32_t w = __ballot_sync(0xffffffffu, (u >= pd.x) != (pd.y != 0));
-        if ((threadIdx.x & 31) == 0 && d < g.D) g.out_bits[size_t(b) * g.Dw + (d >> 5)] = w;
-    } else if (d < g.D) {
-        const int4 pd = __ldg(g.prm + d);
-        g.out_f32[size_t(d) * g.ldo + b] = __fadd_rn(__int2float_rn(2 * u - pd.z), __int_as_float(pd.w));
+    if (g.ksplit > 1) {
+        // Split-K completion in the same launch (one unit per CTA when split: lin4_plan). Once
+        // every slice of this (feature, image) tile has written its partial sums, slice ks
+        // reduces images [ks*chunk, (ks+1)*chunk) of the tile with all 14 warps: a warp takes one
+        // image, lane = 4 consecutive features (16-byte loads), 3 shuffles assemble each 32-feature
+        // word. All slices are co-resident (grid <= SMs, one CTA per SM, and the dependent launch
+        // waits until every CTA has started), so the spin cannot hang.
+        int mt, nt, ks;
+        decode(blockIdx.x, mt, nt, ks);
+        unsigned* arrive = g.sem + 2 * (blockIdx.x / g.ksplit);
+        if (threadIdx.x == 0) {
+            stamp(2);
+            __threadfence();  // this CTA's partial sums (the epilogue warps' stores, ordered by the barrier)
+            atomicAdd(arrive, 1u);
+            while (ld_acquire(arrive) < unsigned(g.ksplit)) __nanosleep(32);
+            stamp(3);
+        }
+        __syncthreads();
+        const int b0 = nt * g.NB, m0 = mt * 128;
+        const int chunk = (g.NB + g.ksplit - 1) / g.ksplit;
+        const int bb0 = b0 + ks * chunk, bb1 = min(min(b0 + g.NB, g.B), bb0 + chunk);
+        const int d = m0 + 4 * lane;  // this lane's 4 features
+        const bool dv = d < g.Dpad;
+        int4 p4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p4[k] = d + k < g.D ? __ldg(g.prm + d + k) : make_int4(0x7fffffff, 0, 0, 0);
+        for (int b = bb0 + warp; b < bb1; b += kLThreads / 32) {
+            int4 acc = make_int4(0, 0, 0, 0);
+            if (dv) {
+                for (int sl = 0; sl < g.ksplit; ++sl) {
+                    const int4 v = __ldcg(reinterpret_cast<const int4*>(g.ws + (size_t(sl) * g.B + b) * g.Dpad + d));
+                    acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+                }
+            }
+            const int uu[4] = {acc.x, acc.y, acc.z, acc.w};
+            if (g.epi == FEPI_BITS) {
+                uint32_t bits = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) bits |= uint32_t((uu[k] >= p4[k].x) != (p4[k].y != 0)) << k;
+                uint32_t w = bits << (4 * (lane & 7));
+                w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                w |= __shfl_xor_sync(0xffffffffu, w, 4);
+                if ((lane & 7) == 0 && d < g.D) g.out_bits[size_t(b) * g.Dw + (d >> 5)] = w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (d + k < g.D)
+                        g.out_f32[size_t(d + k) * g.ldo + b] =
+                            __fadd_rn(__int2float_rn(2 * uu[k] - p4[k].z), __int_as_float(p4[k].w));
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            stamp(4);
+            if (atomicAdd(arrive + 1, 1u) == unsigned(g.ksplit - 1)) {
+                arrive[0] = 0;  // every slice of the tile is past its wait and its reads
+                arrive[1] = 0;
+            }
+        }
     }
+    if (threadIdx.x == 0) stamp(6);
 }
 
 // Host plan: images per tile (NB, <= 256, a multiple of 16), feature tiles of 128 and the K
@@ -319,30 +382,37 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     l.KB4 = fg.kb4, l.kq_last = fg.kq4;
     l.m_tiles = (fg.D + 127) / 128;
     // (NB, split) by a cycle model per CTA: MMA steps x max(48, NB/2) cycles (the measured
-    // dispatch cost, tools/halo_probe.cu), the weight slice streamed at ~100 B/cycle, and
-    // ~6000 cycles for the partial-sum round trip and lin_finish_kernel when K is split. Small
-    // batches prefer narrow image tiles over a K split (fc 8192 -> 1024 at batch 256: 128 CTAs
-    // of 16 images instead of 8 tiles x 8 slices).
+    // dispatch cost, tools/halo_probe.cu), the CTA's weight slice streamed at ~24 B/cycle, and
+    // the partial-sum round trip of the in-kernel split-K completion.
     long best = -1;
     for (int nb = 256; nb >= 16; nb /= 2) {
         if (nb > 16 && nb / 2 >= (fg.B + 15) / 16 * 16) continue;  // narrower than the batch already
         const int nbr = std::min(nb, (fg.B + 15) / 16 * 16);
         const int nt = (fg.B + nbr - 1) / nbr;
         const int tiles = l.m_tiles * nt;
-        for (int ks = 1; ks <= 8; ks *= 2) {
+        for (int ks = 1; ks <= 16; ks *= 2) {
             if (ks > 1 && (l.KB4 + ks - 1) / ks < 2) break;
             const int kbs = (l.KB4 + ks - 1) / ks;
             const long units = long(tiles) * ((l.KB4 + kbs - 1) / kbs);
+            if (ks > 1 && units > sms) break;  // split slices must all be co-resident (one round)
             const long rounds = (units + sms - 1) / sms;
             const long mma = long(kbs) * 4 * std::max(48, nbr / 2);
-            const long wts = long(kbs) * 16384 / 100;
-            const long cost = rounds * std::max(mma, wts) + (ks > 1 ? 6000 : 0);
+            // per CTA: the mainloop (MMA dispatch, or the weight slice streamed at ~24 B/cycle, plus
+            // ~3000 cycles of first-load latency), the epilogue (~500 cycles per 32 images), and
+            // when split: partial sums out (~32 B/cycle), the spin, and the reduction (14 warps,
+            // ~1000 cycles per image each)
+            const long wts = long(kbs) * 16384 / 24;
+            const long main = std::max(mma, wts) + 3000;
+            const long epi = ks > 1 ? long(nbr) * 128 * 4 / 32 + 1500 + ((nbr + ks - 1) / ks + 13) / 14 * 1000
+                                    : long((nbr + 31) / 32) * 500;
+            const long cost = rounds * (main + epi);
             if (best < 0 || cost < best) {
                 best = cost;
                 l.NB = nbr, l.n_tiles = nt, l.kbs = kbs, l.ksplit = (l.KB4 + kbs - 1) / kbs;
             }
         }
     }
+    l.nst = int(std::min<size_t>(kLStages, (kLSmem - 1024 - 256) / (16384 + size_t(l.NB) * 128)));
     l.Dpad = (fg.D + 31) / 32 * 32;
     l.prm = fg.prm;
     l.epi = epi;
@@ -350,8 +420,12 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     l.out_f32 = fg.out_f32;
     l.ldo = fg.ldo;
     l.ws = nullptr;
+    l.sem = nullptr;
+    l.dbg = nullptr;
     return true;
 }
+
+size_t lin4_sem_count(const LinGeom& l) { return l.ksplit > 1 ? size_t(2) * l.m_tiles * l.n_tiles : 0; }
 
 size_t lin4_ws_bytes(const LinGeom& l) { return l.ksplit > 1 ? size_t(l.ksplit) * l.B * l.Dpad * sizeof(int) : 0; }
 
@@ -365,22 +439,41 @@ int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(std::min(units, num_sms())));
     cfg.blockDim = dim3(unsigned(kLThreads));
-    cfg.dynamicSmemBytes = 1024 + size_t(kLStages) * (16384 + size_t(l.NB) * 128) + 256;
+    cfg.dynamicSmemBytes = 1024 + size_t(l.nst) * (16384 + size_t(l.NB) * 128) + 256;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, l));
-    BNN_TRY(launch_check("lin4_kernel"));
-    if (l.ksplit > 1) {
-        const size_t total = size_t(l.B) * l.Dpad;
-        cfg.gridDim = dim3(unsigned(ceil_div(total, 256)));
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = 0;
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin_finish_kernel, l));
-        BNN_TRY(launch_check("lin_finish_kernel"));
+    static const bool prof = getenv("BNN_LIN4_PROFILE") != nullptr;
+    if (!prof) {
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, l));
+        BNN_TRY(launch_check("lin4_kernel"));
+    } else {  // synchronous, not capturable: tools only
+        LinGeom lp = l;
+        BNN_CUDA(cudaMalloc(&lp.dbg, 8 * sizeof(unsigned long long)));
+        BNN_CUDA(cudaMemset(lp.dbg, 0, 8 * sizeof(unsigned long long)));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, lp));
+        cudaEventRecord(e1, s);
+        BNN_TRY(launch_check("lin4_kernel"));
+        BNN_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long d[8];
+        BNN_CUDA(cudaMemcpy(d, lp.dbg, sizeof d, cudaMemcpyDeviceToHost));
+        cudaFree(lp.dbg);
+        const double n = double(cfg.gridDim.x) * 1e3;
+        fprintf(stderr,
+                "[lin4 B=%d K=%d D=%d | NB=%d m=%d n=%d split=%d kbs=%d nst=%d grid=%u] %.1f us | per-CTA us since start: "
+                "epi ready %.2f, acc full %.2f, epilogue done %.2f, partials out %.2f, slices in %.2f, reduced %.2f, "
+                "CTA end %.2f\n",
+                l.B, l.K, l.D, l.NB, l.m_tiles, l.n_tiles, l.ksplit, l.kbs, l.nst, cfg.gridDim.x, ms * 1e3, d[0] / n,
+                d[1] / n, d[5] / n, d[2] / n, d[3] / n, d[4] / n, d[6] / n);
     }
     set_last_gemm("lin4_kernel");
     return BNN_OK;

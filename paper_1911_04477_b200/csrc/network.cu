@@ -157,7 +157,8 @@ struct bnn_net {
     size_t bits_words_per_image = 0;
     size_t bits_batch = 0;
     bnnk::DevBuf bits[2], pix, ws, sem;
-    bnnk::DevBuf lin_ws;  // split-K partial sums of the FP4 linear kernel (lin4)
+    bnnk::DevBuf lin_ws;   // split-K partial sums of the FP4 linear kernel (lin4)
+    bnnk::DevBuf lin_sem;  // its per-tile counters (zeroed once; the kernel leaves them at 0)
     bnnk::DevBuf chain_done;
     bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
 };
@@ -751,7 +752,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     };
     std::vector<Plan> plans;
     size_t ws_need = 0, sem_need = 0;  // the largest split-K workspace of any stage
-    size_t lin_ws_need = 0;            // the largest lin4 partial-sum workspace
+    size_t lin_ws_need = 0, lin_sem_need = 0;  // the largest lin4 workspace and counter array
     const void* in = x;
     int which = 0;
     (void)prof;
@@ -787,6 +788,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         if (use_lin4(net, st) && !(st.small_logits && g_small_logits) && lin4_plan(g, st.epi, pl.lg)) {
             pl.lin4 = true;
             lin_ws_need = std::max(lin_ws_need, lin4_ws_bytes(pl.lg));
+            lin_sem_need = std::max(lin_sem_need, lin4_sem_count(pl.lg) * sizeof(unsigned));
         }
         plans.push_back(pl);
         in = g.out_bits;
@@ -822,9 +824,14 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         BNN_TRY(net->lin_ws.alloc(lin_ws_need));
         ++net->arena_epoch;
     }
+    if (net->lin_sem.bytes < lin_sem_need) {
+        BNN_TRY(net->lin_sem.alloc(lin_sem_need));
+        BNN_CUDA(cudaMemsetAsync(net->lin_sem.p, 0, lin_sem_need, s));
+        ++net->arena_epoch;
+    }
     for (auto& pl : plans) {
         if (pl.g.ksplit > 1) pl.g.ws = net->ws.as<int>(), pl.g.sem = net->sem.as<unsigned>();
-        if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>();
+        if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>(), pl.lg.sem = net->lin_sem.as<unsigned>();
     }
     size_t launches = 0;
     for (size_t i = 0; i < first_chained; ++i) {
@@ -920,7 +927,8 @@ bool use_fused(const bnn_net* net) {
 // with per-layer timing (events), the profiling mode, or the legacy default stream (which
 // cannot be captured).
 int forward_graphed(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
-    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr || getenv("BNN_HALO_PROFILE") != nullptr;
+    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr || getenv("BNN_HALO_PROFILE") != nullptr ||
+                             getenv("BNN_LIN4_PROFILE") != nullptr;
     const bool graphable = net->use_graphs && !net->timing && !prof && s != nullptr;
     if (!graphable) return forward_fused(net, x, B, logits, s);
     // small cache: a pipelined caller alternates input/output buffers

@@ -137,7 +137,8 @@ def test_report_schema_and_hashes_match_reference(bnn, ref, tmp_path, spec):
     path = None if spec is None else os.path.join(GOLD, f"{spec}.json")
     batch = 2 if spec is None else 4
     ours, theirs = tmp_path / "ours.json", tmp_path / "ref.json"
-    check(bnn.load().bnn_run_benchmark(None if path is None else path.encode(), batch, 2, 1, 1, 3, 1,
+    # iterations 2, warmup 0 (the reference run below: 1 and 0; iterations is not compared)
+    check(bnn.load().bnn_run_benchmark(None if path is None else path.encode(), batch, 2, 0, 1, 3, 1,
                                        str(ours).encode()))
     ref.run_benchmark(theirs, path, batch=batch, iterations=1, warmup=0, seed=1, kernels_mask=3)
     n, h = ref.parse_report(ours)  # the reference's parser accepts our report

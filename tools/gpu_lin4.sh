@@ -16,5 +16,5 @@ rows=[r for r in csv.reader(open('gpurun_out/lin4_launches.csv')) if len(r)>10]
 h=rows[0]; ki=h.index('Kernel Name'); vi=h.index('Metric Value')
 for r in rows[1:12]: print(r[ki][:70], r[vi])
 PY
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lin4|lin_finish" -c 2 -o gpurun_out/lin4_b256 -f python tools/prof_net.py 256 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lin4" -c 2 -o gpurun_out/lin4_b256 -f python tools/prof_net.py 256 > /dev/null 2>&1
 echo "ncu rc=$?"
