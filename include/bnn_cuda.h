@@ -318,7 +318,8 @@ int bnn_set_fused_fp4(int mode);
 /* Fused engine: the halo-tile FP4 conv (halo4_kernel) for "same" convs (3x3 pad 1, 1x1, ...,
  * stride 1) with a packed-bit input whose weights fit in shared memory: each input pixel is
  * expanded to e2m1 once per tile instead of once per tap. 0 off (fused_swap4_kernel), 1
- * (default) on. Bit-exact either way. */
+ * (default) on, 2 also for convs whose weights do not fit (streamed through a ring of shared-
+ * memory slots; slower than fused_swap4_kernel for VGG-small). Bit-exact in every mode. */
 int bnn_set_fused_halo(int enabled);
 /* Fused engine: linear layers on the FP4 tensor-core kernel (lin4_kernel: e2m1 weights by TMA,
  * packed input bits expanded in shared memory, K split over CTAs with an exact integer

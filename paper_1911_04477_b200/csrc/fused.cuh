@@ -72,6 +72,7 @@ struct HaloGeom {
     int TR, N, NH, nst;  // canvas rows per tile, MMA N, halo rows, halo stages
     int n_tiles, m_tiles, total_rows, grid;
     int steps, KB4;      // K / 64 MMA steps, 256-element weight blocks
+    int wst;             // 0: weights resident in shared memory; else ring slots of streamed blocks
     size_t smem;
     FastDiv dP, dS, dQ, dWh, dG;
     unsigned long long* dbg;  // BNN_HALO_PROFILE counters, else null

@@ -56,6 +56,7 @@ constexpr int kHProdThreads = kHProdWarps * 32;
 constexpr int kHSfCol = 496;
 constexpr int kHMaxN = 240;
 constexpr int kHMaxStages = 4;
+constexpr int kHMaxWst = 8;  // streamed-weight ring slots
 constexpr size_t kHSmemMax = 232448;  // 227 KB opt-in per CTA
 
 // K-major, no swizzle: core matrix = 8 rows x 16 bytes, 8-row groups 128 B apart (SBO), the two
@@ -107,6 +108,34 @@ __device__ __forceinline__ void issue_tile(uint32_t d, uint32_t alo0, uint32_t a
             const int s = t * CPT + c;
             mma_mxf4_lohi(d, alo0 + uint32_t((s >> 2) * 1024 + (s & 3) * 2), ahi, blo0 + toff[t] + uint32_t(c) * step16,
                           bhi, idesc, sf, s != 0);
+        }
+    }
+}
+
+// Streamed weights: the same steps, each block of 4 steps from ring slot ws (waited on wfull,
+// released by a commit to wempty).
+template <int CPT>
+__device__ __forceinline__ void issue_tile_stream(uint32_t d, uint32_t alo0, uint32_t ahi, uint32_t blo0, uint32_t bhi,
+                                                  uint32_t idesc, uint32_t sf, const uint32_t (&toff)[9], int taps,
+                                                  uint32_t step16, uint64_t* wfull, uint64_t* wempty, int wst, int& ws,
+                                                  uint32_t& wph) {
+    const int steps = taps * CPT;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        if (t >= taps) break;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const int st = t * CPT + c;
+            if ((st & 3) == 0) {
+                mbar_wait(&wfull[ws], wph);
+                tc_fence_after();
+            }
+            mma_mxf4_lohi(d, alo0 + uint32_t(ws) * 1024u + uint32_t(st & 3) * 2u, ahi,
+                          blo0 + toff[t] + uint32_t(c) * step16, bhi, idesc, sf, st != 0);
+            if ((st & 3) == 3 || st == steps - 1) {
+                mma_commit_w(&wempty[ws]);
+                if (++ws == wst) ws = 0, wph ^= 1;
+            }
         }
     }
 }
@@ -254,13 +283,15 @@ struct HClock {
 
 }  // namespace
 
+template <bool STREAM>
 __global__ void __launch_bounds__(kHThreads, 1)
     halo4_kernel(const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ HaloGeom g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;  // weights: KB4 blocks of 128 rows x 128 B (SW128)
+    // weights: KB4 resident blocks of 128 rows x 128 B (SW128), or a ring of wst blocks (streamed)
+    const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sW = smem_raw + (base - raw);
-    const uint32_t wbytes = uint32_t(g.KB4) * 16384u;
+    const uint32_t wbytes = uint32_t(STREAM ? g.wst : g.KB4) * 16384u;
     const uint32_t lbo = uint32_t(g.NH) * 16u;         // K-chunk stride of a halo stage
     const uint32_t hbytes = uint32_t(g.Cw) * lbo;      // one halo stage
     const uint32_t sH = base + wbytes;
@@ -270,7 +301,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
     uint64_t* tfull = bars + 2 * kHMaxStages;
     uint64_t* tempty = tfull + 2;
     uint64_t* wbar = tempty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+    uint64_t* wfull = wbar + 1;                 // streamed weights: [kHMaxWst] ring slots
+    uint64_t* wempty = wfull + kHMaxWst;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + kHMaxWst);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
@@ -292,6 +325,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
             mbar_init(&tempty[a], kHEpiWarps);
         }
         mbar_init(wbar, 1);
+        for (int w = 0; w < (STREAM ? g.wst : 0); ++w) {
+            mbar_init(&wfull[w], 1);
+            mbar_init(&wempty[w], 1);
+        }
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -300,7 +337,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (warp == 0 && lane == 0) {
+    if (warp == 0 && lane == 0 && !STREAM) {
         // the resident weights are build-time constants: load them before the grid dependency
         mbar_arrive_expect_tx(wbar, wbytes);
         for (int kb = 0; kb < g.KB4; ++kb) tma_load_2d(&tmW4, wbar, sW + size_t(kb) * 16384, kb * 128, mt * 128);
@@ -322,17 +359,30 @@ __global__ void __launch_bounds__(kHThreads, 1)
     const long long k_main = prof ? hclock() : 0;
     if (prof && threadIdx.x == 0) atomicAdd(g.dbg + 12, (unsigned long long)(k_main - k_start));
 
-    if (warp == 1) {
+    if (warp == 0 && STREAM) {
+        // streamed weights: every tile walks the layer's KB4 blocks through the ring
+        if (lane == 0) {
+            int ws = 0;
+            uint32_t wph = 0;
+            for (int nt = n0; nt < g.n_tiles; nt += nstride)
+                for (int kb = 0; kb < g.KB4; ++kb) {
+                    mbar_wait(&wempty[ws], wph ^ 1);
+                    mbar_arrive_expect_tx(&wfull[ws], 16384);
+                    tma_load_2d(&tmW4, &wfull[ws], sW + size_t(ws) * 16384, kb * 128, mt * 128);
+                    if (++ws == g.wst) ws = 0, wph ^= 1;
+                }
+        }
+    } else if (warp == 1) {
         const uint32_t idesc = idesc_mxf4_m128(g.N);
         const uint32_t lbo16 = lbo >> 4;
         uint32_t toff[9];  // tap shifts on the canvas, in 16-byte units
 #pragma unroll
         for (int t = 0; t < 9; ++t) toff[t] = uint32_t(g.toff[t]);
         HClock cw, ct, cf;
-        cw.wait(prof, wbar, 0);
+        if (!STREAM) cw.wait(prof, wbar, 0);
         tc_fence_after();
-        int hs = 0, i = 0;
-        uint32_t hph = 0;
+        int hs = 0, i = 0, ws = 0;
+        uint32_t hph = 0, wph = 0;
         for (int nt = n0; nt < g.n_tiles; nt += nstride, ++i) {
             const int acc = i & 1;
             ct.wait(prof, &tempty[acc], ((i >> 1) & 1) ^ 1);
@@ -347,11 +397,20 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 const uint32_t blo = uint32_t(bd0), bhi = uint32_t(bd0 >> 32);
                 const int taps = (g.dbg_mode & 4) ? 0 : g.taps;
                 const uint32_t sf = tmem_base + kHSfCol, step16 = 2u * lbo16;
-                switch (g.cpt) {
+                if constexpr (STREAM) {
+                    switch (g.cpt) {
+                        case 1: issue_tile_stream<1>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16, wfull, wempty, g.wst, ws, wph); break;
+                        case 2: issue_tile_stream<2>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16, wfull, wempty, g.wst, ws, wph); break;
+                        case 4: issue_tile_stream<4>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16, wfull, wempty, g.wst, ws, wph); break;
+                        default: issue_tile_stream<8>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16, wfull, wempty, g.wst, ws, wph); break;
+                    }
+                } else {
+                    switch (g.cpt) {
                     case 1: issue_tile<1>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16); break;
                     case 2: issue_tile<2>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16); break;
                     case 4: issue_tile<4>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16); break;
                     default: issue_tile<8>(d, alo, ahi, blo, bhi, idesc, sf, toff, taps, step16); break;
+                    }
                 }
                 mma_commit_warp(&empty[hs]);
                 mma_commit_warp(&tfull[acc]);
@@ -507,38 +566,49 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
     const int K = fg.KH * fg.KW * fg.C;
     if (K != fg.K || K / 64 > kHaloMaxSteps) return false;
     const int KB4 = (K + 255) / 256;
-    const size_t wbytes = size_t(KB4) * 16384;
     const int m_tiles = (fg.D + 127) / 128;
     const int sms = num_sms();
     if (sms < m_tiles) return false;
     const int per_m = sms / m_tiles;
+    const int cpt = fg.C / 64;
     long best = -1;
-    for (int G = 1; G <= 16; G *= 2) {
-        if (G > 1 && G > fg.B) break;
-        const int S = fg.pool ? fg.H + 2 : fg.H + 1;
-        const int Q = fg.pool ? fg.W + 2 : fg.W + 1;
-        const int P = fg.pool ? G * Q : G * Q + 1;
-        const int rstep = fg.pool ? 2 : 1;
-        if (rstep * P > kHMaxN) break;
-        const int n_groups = (fg.B + G - 1) / G;
-        const int total_rows = n_groups * S;
-        for (int TR = rstep; TR * P <= kHMaxN; TR += rstep) {
-            const int N = round_up_i(TR * P, 16);
-            const int NH = round_up_i(N + 2 * P + 2, 8);
-            const size_t hbytes = size_t(fg.Cw) * NH * 16;
-            const size_t avail = kHSmemMax - 1024 - 256;
-            if (wbytes + 2 * hbytes > avail) continue;
-            const int n_tiles = (total_rows + TR - 1) / TR;
-            const int ctas = std::min(per_m, n_tiles);
-            const long rounds = (n_tiles + ctas - 1) / ctas;
-            // MMA columns per CTA plus a fixed per-tile cost (barriers, epilogue tail)
-            const long cost = rounds * (N + 16);
-            if (best < 0 || cost < best) {
-                best = cost;
-                h.G = G, h.S = S, h.Q = Q, h.P = P, h.TR = TR, h.N = N, h.NH = NH;
-                h.n_tiles = n_tiles, h.total_rows = total_rows;
-                h.nst = int(std::min<size_t>(kHMaxStages, (avail - wbytes) / hbytes));
-                h.grid = ctas * m_tiles;
+    // weights resident (wst = 0) when the CTA's slice fits next to two halo stages, else a ring of
+    // kHMaxWst streamed blocks (K chunks per tap a power of two)
+    for (int wst : {0, kHMaxWst}) {
+        if (best >= 0) break;  // a resident plan exists
+        if (wst && (cpt & (cpt - 1))) break;
+        const size_t wbytes = size_t(wst ? wst : KB4) * 16384;
+        for (int G = 1; G <= 16; G *= 2) {
+            if (G > 1 && G > fg.B) break;
+            const int S = fg.pool ? fg.H + 2 : fg.H + 1;
+            const int Q = fg.pool ? fg.W + 2 : fg.W + 1;
+            const int P = fg.pool ? G * Q : G * Q + 1;
+            const int rstep = fg.pool ? 2 : 1;
+            if (rstep * P > kHMaxN) break;
+            const int n_groups = (fg.B + G - 1) / G;
+            const int total_rows = n_groups * S;
+            for (int TR = rstep; TR * P <= kHMaxN; TR += rstep) {
+                const int N = round_up_i(TR * P, 16);
+                const int NH = round_up_i(N + 2 * P + 2, 8);
+                const size_t hbytes = size_t(fg.Cw) * NH * 16;
+                const size_t avail = kHSmemMax - 1024 - 256;
+                if (wbytes + 2 * hbytes > avail) continue;
+                const int n_tiles = (total_rows + TR - 1) / TR;
+                const int ctas = std::min(per_m, n_tiles);
+                const long rounds = (n_tiles + ctas - 1) / ctas;
+                // MMA cycles per CTA (N/2 per step, plus a fixed per-tile cost); streamed: the
+                // tile's weight blocks at ~40 B/cycle
+                const long steps = K / 64;
+                const long mma = steps * (N + 16) / 2;
+                const long cost = rounds * (wst ? std::max(mma, long(KB4) * 16384 / 40) : mma);
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    h.G = G, h.S = S, h.Q = Q, h.P = P, h.TR = TR, h.N = N, h.NH = NH;
+                    h.n_tiles = n_tiles, h.total_rows = total_rows;
+                    h.nst = int(std::min<size_t>(kHMaxStages, (avail - wbytes) / hbytes));
+                    h.grid = ctas * m_tiles;
+                    h.wst = wst;
+                }
             }
         }
     }
@@ -559,7 +629,7 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
         const int ky = t / fg.KW, kx = t % fg.KW;
         h.toff[t] = t < h.taps ? (ky - fg.PH + 1) * h.P + (kx - fg.PW + 1) : 0;
     }
-    h.smem = 1024 + wbytes + size_t(h.nst) * fg.Cw * h.NH * 16 + 256;
+    h.smem = 1024 + size_t(h.wst ? h.wst : KB4) * 16384 + size_t(h.nst) * fg.Cw * h.NH * 16 + 256;
     h.dWh = FastDiv::make(uint32_t(std::max(1, fg.W / 2)));
     h.dG = FastDiv::make(uint32_t(h.G));
     h.dbg = nullptr;
@@ -570,7 +640,8 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
 int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(halo4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHSmemMax)));
+        BNN_CUDA(cudaFuncSetAttribute(halo4_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHSmemMax)));
+        BNN_CUDA(cudaFuncSetAttribute(halo4_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kHSmemMax)));
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -585,7 +656,7 @@ int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
     cfg.numAttrs = 1;
     static const bool prof = getenv("BNN_HALO_PROFILE") != nullptr;
     if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, halo4_kernel, tm4, h));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, h.wst ? halo4_kernel<true> : halo4_kernel<false>, tm4, h));
         BNN_TRY(launch_check("halo4_kernel"));
     } else {  // synchronous, not capturable: tools only
         HaloGeom hp = h;
@@ -594,7 +665,7 @@ int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
         unsigned long long init[16] = {};
         init[14] = ~0ull;
         BNN_CUDA(cudaMemcpy(hp.dbg, init, sizeof init, cudaMemcpyHostToDevice));
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, halo4_kernel, tm4, hp));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, h.wst ? halo4_kernel<true> : halo4_kernel<false>, tm4, hp));
         BNN_TRY(launch_check("halo4_kernel"));
         unsigned long long d[16];
         BNN_CUDA(cudaMemcpy(d, hp.dbg, sizeof d, cudaMemcpyDeviceToHost));

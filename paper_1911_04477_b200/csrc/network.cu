@@ -711,7 +711,8 @@ bool use_fp4(const bnn_net* net, const FusedStage& st, int cg) {
 
 // Halo-tile FP4 conv (halo.cu, halo4_kernel): BNN_FUSED_HALO / bnn_set_fused_halo: 0 off, 1
 // (default) every "same" conv with a packed-bit input whose weight slice fits in shared memory;
-// the others keep fused_swap4_kernel.
+// 2 also the others with the weights streamed through a ring (measured slower than
+// fused_swap4_kernel for VGG-small's conv 512 -> 512: 40 vs 32 us per layer at batch 256).
 int g_halo = -1;
 
 bool use_halo(const bnn_net* net, const FusedStage& st, int cg) {
@@ -862,7 +863,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         }
         else if (plans[i].lin4)
             BNN_TRY(launch_lin4(st.tm4, plans[i].lg, s));
-        else if (HaloGeom hg; use_halo(net, st, plans[i].cg) && halo4_plan(g, hg))
+        else if (HaloGeom hg; use_halo(net, st, plans[i].cg) && halo4_plan(g, hg) && (!hg.wst || g_halo == 2))
             BNN_TRY(launch_halo4(st.tm4, hg, s));
         else if (use_fp4(net, st, plans[i].cg))
             BNN_TRY(launch_swap4(st.in_mode, st.tm4, g, s));
@@ -1129,7 +1130,8 @@ int bnn_set_fused_lin4(int enabled) {
 }
 
 int bnn_set_fused_halo(int enabled) {
-    if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused halo: 0 (off) or 1 (on)");
+    if (enabled < 0 || enabled > 2)
+        return fail(BNN_E_CONFIG, "fused halo: 0 (off), 1 (resident weights only) or 2 (also streamed weights)");
     g_halo = enabled;
     ++g_tiling_epoch;  // captured graphs hold the other kernels
     return BNN_OK;

@@ -67,7 +67,7 @@ FUSABLE = {
 CHAINED = {"chain", "chain_nosplit", "chain_split16"}
 
 
-@pytest.fixture(params=["auto", "nohalo", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
+@pytest.fixture(params=["auto", "nohalo", "halostream", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
                         "chain_split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -90,7 +90,7 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_pix_popc({"auto": 3, "pixf32": 1, "pixpacked": 2}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_fp4({"fp4": 1, "fp4all": 2, "nofp4": 0}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_fp4_pair({"nopair": 0, "pair224": 3}.get(p, 1)))
-    bnn._lib.check(lib.bnn_set_fused_halo(0 if p == "nohalo" else 1))
+    bnn._lib.check(lib.bnn_set_fused_halo({"nohalo": 0, "halostream": 2}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_lin4(0 if p == "nolin4" else 1))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
