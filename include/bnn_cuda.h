@@ -242,12 +242,6 @@ int bnn_net_set_graphs(bnn_net* net, int enabled);
 /* Fused engine split-K for few, K-deep output tiles (the linear layers at small batch): 0 auto
  * (default), 1 off, or a forced power of two <= 16. Process-wide; bit-exact either way. */
 int bnn_set_fused_split(int split);
-/* Fused engine: keep the activation operand in TMEM (tcgen05.st + the TS-form MMA, default 1)
- * or stage it in shared memory (0). Process-wide; both are bit-exact. */
-int bnn_set_fused_tmem_a(int enabled);
-/* Fused engine: run every stage of the network in ONE persistent chained launch (1) or one
- * launch per weighted layer (0, default). Process-wide; both are bit-exact. */
-int bnn_set_fused_chain(int enabled);
 /* Fused engine: conv layers with a packed-bit output use the swapped-operand kernel (output
  * channels on the tensor-core M, positions on N: full rate for 128-channel layers): 1 (default)
  * for layers of <= 128 channels, 2 for all, 0 never. Process-wide; all are bit-exact. */

@@ -114,9 +114,7 @@ _SIGS = {
     "bnn_net_engine": (_I, [_P]),
     "bnn_net_set_graphs": (_I, [_P, _I]),
     "bnn_set_fused_tiling": (_I, [_I, _I]),
-    "bnn_set_fused_tmem_a": (_I, [_I]),
     "bnn_set_fused_split": (_I, [_I]),
-    "bnn_set_fused_chain": (_I, [_I]),
     "bnn_debug_timeline": (_I, [_I]),
     "bnn_set_fused_swap": (_I, [_I]),
     "bnn_set_fused_small_logits": (_I, [_I]),

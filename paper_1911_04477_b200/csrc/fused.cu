@@ -127,12 +127,8 @@ struct RowCtx {
 // cw} for K word q (cw < 0: K padding). One 16-byte load when the block is one tap of
 // contiguous channels (Cw % 4 == 0), else word by word.
 // Activation loads. A single-layer launch uses the read-only path (ld.global.nc), predicated.
-// The chained kernel's activation buffers are written by other CTAs during the launch, so it
-// uses coherent loads (ld.global.ca, volatile asm: never moved across the stage hand-off's
-// acquire and barrier). The producers' ld.acquire.gpu of the stage counter invalidates the
-// SM's L1 (SASS: CCTL.IVALL), so cached loads after it see those writes. The coherent loads
-// are issued unconditionally from a clamped address (padding positions read the buffer's
-// first word and discard it): a conditional volatile load compiles to a branch per load.
+// Coherent = true (ld.global.ca, volatile asm) is for activations written during the same launch
+// by other CTAs; the per-layer kernels use the read-only path.
 __device__ __forceinline__ uint4 ld_ca4(const uint32_t* p) {
     uint4 v;
     asm volatile("ld.global.ca.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
@@ -832,526 +828,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-// Chained engine: ONE persistent launch runs every fused stage of a network (conv/linear +
-// glue, as above), instead of one launch per weighted layer.
-//
-// Why: at the benchmark batch the per-layer kernels are short (10-70 us) and each paid ~10 us
-// of launch, prologue (barriers, TMEM allocation, threshold tables), pipeline fill and tail.
-// Here the roles persist across stages and their pipelines run straight through the stage
-// boundaries: the weight TMA warp streams the next stage's weights (they do not depend on
-// the activations) while the current stage's MMAs and epilogues finish, and the TMEM ring,
-// the shared-memory ring and their barrier phases carry over.
-//
-// The one cross-CTA dependency is the activation hand-off: stage s+1 reads every pixel
-// stage s wrote. Each CTA's epilogue warps publish "stage s done" (per-thread
-// __threadfence, a named barrier, one release-add on done[s]); the producer warps of every
-// CTA wait for done[s] == gridDim.x (acquire) before their first activation load of stage
-// s+1; that acquire invalidates the SM's L1, so the coherent activation loads after it see
-// no stale line of a buffer rewritten since the SM last read it. Write-after-read on the ping-pong activation
-// buffers is ordered by the same chain (stage s+1 writes only after its own producers passed
-// done[s], which follows every read of stage s-1). The grid is one CTA per SM (smem- and
-// register-limited to 1 CTA/SM), all co-resident, so the spin-waits cannot deadlock.
-//
-// Restrictions (else the per-layer launches above run): CTA-local M=128 tiles (cta_group::1),
-// A operand in TMEM, packed-bit or pixel-packed inputs (no float im2col stage), epilogues
-// writing packed bits or logits.
-//
-// TMEM (512 columns): accumulator slot a at column 256a (BN <= 128: two slots, the epilogue
-// of tile i overlaps the MMAs of tile i+1; BN = 256: slot 0 only), A stages at 384 + 32s.
-
-constexpr int kChainA = 384;
-constexpr size_t kChainSmem = 1024 + size_t(kStages) * 256 * kKB + 256 + kMaxQ * 8 + kMaxD * 4 + kMaxD / 8;
-
-// Profiling aid (ChainParams::dbg, BNN_FUSED_PROFILE=1): per stage and role, the cycles spent
-// blocked in two wait classes and the role's cycles in the stage. Slots dbg[s*16 + role*4 +
-// {0, 1, 3}]; roles 0 TMA, 1 MMA, 2 epilogue, 3 producer.
-struct StageClock {
-    long long w0 = 0, w1 = 0, t0;
-    __device__ __forceinline__ StageClock() : t0(dclock()) {}
-    __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int slot) {
-        const long long a = dclock();
-        mbar_wait(bar, parity);
-        (slot ? w1 : w0) += dclock() - a;
-    }
-    __device__ __forceinline__ void flush(unsigned long long* dbg, int s, int role, bool reporter) {
-        const long long now = dclock();
-        if (dbg && reporter) {
-            atomicAdd(dbg + s * 16 + role * 4 + 0, (unsigned long long)w0);
-            atomicAdd(dbg + s * 16 + role * 4 + 1, (unsigned long long)w1);
-            atomicAdd(dbg + s * 16 + role * 4 + 3, (unsigned long long)(now - t0));
-        }
-        w0 = w1 = 0;
-        t0 = now;
-    }
-};
-
-struct ChainTiles {
-    int S, n_tiles, tiles, KB;
-    __device__ __forceinline__ explicit ChainTiles(const FusedGeom& g) : S(g.ksplit), n_tiles(g.n_tiles), KB(g.KB) {
-        tiles = ((g.rows + kRows - 1) / kRows) * n_tiles * S;
-    }
-    __device__ __forceinline__ int kb_begin(int t) const { return (t % S) * KB / S; }
-    __device__ __forceinline__ int kb_end(int t) const { return (t % S + 1) * KB / S; }
-    __device__ __forceinline__ int n(int t) const { return (t / S) % n_tiles; }
-    __device__ __forceinline__ int m(int t) const { return (t / S) / n_tiles; }
-};
-
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }   // 8 epilogue warps
-__device__ __forceinline__ void prod_bar() { asm volatile("bar.sync 2, 128;" ::: "memory"); }  // 4 producer warps
-
-// Epilogue of one stage (warps 2-5 and 10-13): the same conversion as fused_layer_kernel.
-// Bit a of euse is the tfull parity of accumulator slot a (flipped at every use).
-template <int BN, int EPI>
-__device__ __forceinline__ void chain_epilogue(const FusedGeom& g, uint64_t* tfull, uint64_t* tempty,
-                                               uint32_t tmem_base, const int* tu_s, const uint32_t* flip_s,
-                                               uint32_t& euse, int warp, int lane, StageClock& sc) {
-    static_assert(EPI == FEPI_BITS || EPI == FEPI_LOGITS, "chained epilogues: bits or logits");
-    const ChainTiles ct(g);
-    const int S = ct.S;
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    constexpr int NC = BN / 32;
-    constexpr int kAcc = BN <= 128 ? 2 : 1;
-    const int c_lo = warp >= 10 ? (NC + 1) / 2 : 0, c_hi = warp >= 10 ? NC : (NC + 1) / 2;
-    const int et = (warp < 6 ? warp - 2 : warp - 6) * 32 + lane;
-    int i = 0;
-    for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x, ++i) {
-        const int acc = kAcc == 2 ? (i & 1) : 0;
-        const int mt = ct.m(t), nt = ct.n(t);
-        const int row = mt * kRows + r;
-        const int n0 = nt * BN;
-        const bool valid = row < g.rows;
-        sc.wait(&tfull[acc], (euse >> acc) & 1u, 0);
-        euse ^= 1u << acc;
-        tc_fence_after();
-        uint32_t words[NC];
-        const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * 256);
-        // 16-column TMEM loads, double-buffered (32-column buffers, as in fused_layer_kernel,
-        // spill here: the chained kernel holds every role's state in one register allocation,
-        // at most 128 per thread with 14 warps)
-        uint32_t va[16], vb[16];
-        uint32_t wacc = 0;  // the 32-channel word under construction
-        auto convert = [&](const uint32_t(&v)[16], int h) {
-            const int c = h >> 1, hb = (h & 1) * 16;
-            const int col = n0 + h * 16;
-            if (S > 1) {
-                int4* dst = reinterpret_cast<int4*>(g.ws + ((size_t(t % S) * g.ws_rows + row) * g.ws_ld + col));
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    dst[j] = make_int4(int(v[4 * j]), int(v[4 * j + 1]), int(v[4 * j + 2]), int(v[4 * j + 3]));
-                return;
-            }
-            if (EPI == FEPI_BITS) {
-                const int4* t4 = reinterpret_cast<const int4*>(tu_s + col);
-#pragma unroll
-                for (int j = 0; j < 16; j += 4) {
-                    const int4 th = t4[j >> 2];
-                    wacc |= ((uint32_t(int(v[j]) >= th.x) << j) | (uint32_t(int(v[j + 1]) >= th.y) << (j + 1)) |
-                             (uint32_t(int(v[j + 2]) >= th.z) << (j + 2)) | (uint32_t(int(v[j + 3]) >= th.w) << (j + 3)))
-                            << hb;
-                }
-                if (h & 1) {
-                    uint32_t w = wacc;
-                    wacc = 0;
-                    if (g.pool) {
-                        w |= __shfl_xor_sync(0xffffffffu, w, 1);
-                        w |= __shfl_xor_sync(0xffffffffu, w, 2);
-                    }
-                    w ^= flip_s[(n0 >> 5) + c];
-#pragma unroll
-                    for (int cc = 0; cc < NC; ++cc)
-                        if (cc == c) words[cc] = w;
-                }
-            } else {
-                const int4 pl = __ldg(g.prm + n0 + c * 32 + lane);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int d = col + j;
-                    const int sd = __shfl_sync(0xffffffffu, pl.z, hb + j);
-                    const float bias = __int_as_float(__shfl_sync(0xffffffffu, pl.w, hb + j));
-                    const float y = __fadd_rn(__int2float_rn(2 * int(v[j]) - sd), bias);
-                    if (valid && d < g.D) g.out_f32[size_t(d) * g.ldo + row] = y;
-                }
-            }
-        };
-        const int h_lo = 2 * c_lo, h_hi = 2 * c_hi;  // an even number of halves
-        if (h_lo < h_hi) tmem_ld16(tbase + uint32_t(h_lo * 16), va);
-#pragma unroll 1
-        for (int h = h_lo; h < h_hi; h += 2) {
-            tmem_ld_wait();
-            tmem_ld16(tbase + uint32_t((h + 1) * 16), vb);
-            convert(va, h);
-            tmem_ld_wait();
-            if (h + 2 < h_hi) tmem_ld16(tbase + uint32_t((h + 2) * 16), va);
-            convert(vb, h + 1);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (S > 1) {
-            // split-K completion, as in fused_layer_kernel: meet at the tile's counter, each
-            // K-slice CTA reduces 128/S rows, the last one out resets the counters
-            const int u = t / S, ks = t % S;
-            __threadfence();
-            epi_bar();
-            if (warp == 2 && lane == 0) {
-                atomicAdd(g.sem + 2 * u, 1u);
-                unsigned seen;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(g.sem + 2 * u) : "memory");
-                } while (seen < unsigned(S));
-                __threadfence();
-            }
-            __syncwarp();
-            epi_bar();
-            const int rp = kRows / S;
-            constexpr int C4 = BN / 4;
-            for (int i0 = 0; i0 < rp * C4; i0 += 256) {
-                const int ii = i0 + et;
-                const bool live = ii < rp * C4;
-                const int row2 = mt * kRows + ks * rp + (live ? ii / C4 : 0), c4 = ii % C4;
-                const int n = n0 + 4 * c4;
-                int4 sum = make_int4(0, 0, 0, 0);
-                if (live) {
-                    const int4* src = reinterpret_cast<const int4*>(g.ws + size_t(row2) * g.ws_ld + n);
-                    const size_t slice = size_t(g.ws_rows) * g.ws_ld / 4;
-#pragma unroll 4
-                    for (int s2 = 0; s2 < S; ++s2) {
-                        const int4 v4 = __ldcg(src + s2 * slice);
-                        sum.x += v4.x, sum.y += v4.y, sum.z += v4.z, sum.w += v4.w;
-                    }
-                }
-                const bool out = live && row2 < g.rows && n < g.D;
-                if (EPI == FEPI_BITS) {
-                    uint32_t w = 0;
-                    if (live) {
-                        const int4 t4 = *reinterpret_cast<const int4*>(tu_s + n);
-                        w = (uint32_t(sum.x >= t4.x) | (uint32_t(sum.y >= t4.y) << 1) | (uint32_t(sum.z >= t4.z) << 2) |
-                             (uint32_t(sum.w >= t4.w) << 3))
-                            << (4 * (c4 & 7));
-                    }
-                    w |= __shfl_xor_sync(0xffffffffu, w, 1);
-                    w |= __shfl_xor_sync(0xffffffffu, w, 2);
-                    w |= __shfl_xor_sync(0xffffffffu, w, 4);
-                    if (out && (c4 & 7) == 0) g.out_bits[size_t(row2) * g.Dw + (n >> 5)] = w ^ flip_s[n >> 5];
-                } else if (out) {
-                    const int sv[4] = {sum.x, sum.y, sum.z, sum.w};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int d = n + j;
-                        if (d >= g.D) break;
-                        const int4 pd = __ldg(g.prm + d);
-                        g.out_f32[size_t(d) * g.ldo + row2] = __fadd_rn(__int2float_rn(2 * sv[j] - pd.z), __int_as_float(pd.w));
-                    }
-                }
-            }
-            epi_bar();
-            if (warp == 2 && lane == 0 && atomicAdd(g.sem + 2 * u + 1, 1u) == unsigned(S - 1)) {
-                g.sem[2 * u] = 0;
-                g.sem[2 * u + 1] = 0;
-            }
-        } else if (EPI == FEPI_BITS && valid && (!g.pool || (lane & 3) == 0)) {
-            const int orow = g.pool ? (row >> 2) : row;
-            uint32_t* dst = g.out_bits + size_t(orow) * g.Dw + (n0 >> 5);
-            constexpr int H = (NC + 1) / 2;
-            if (H % 4 == 0 && (g.Dw & 3) == 0 && n0 + BN <= g.D) {
-#pragma unroll
-                for (int c = 0; c < NC; c += 4)
-                    if (c >= c_lo && c < c_hi)
-                        *reinterpret_cast<uint4*>(dst + c) = make_uint4(words[c], words[c + 1], words[c + 2], words[c + 3]);
-            } else {
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    if (c >= c_lo && c < c_hi && n0 + 32 * c < g.D) dst[c] = words[c];
-            }
-        }
-    }
-}
-
-// Activation producers of one stage (warps 6-9), A operand into TMEM; same as the ATM path
-// of fused_layer_kernel, with coherent loads. stage/phase: the shared ring position.
-template <int IN>
-__device__ __forceinline__ void chain_produce(const FusedGeom& g, const int2* ftab, uint64_t* full, uint64_t* empty,
-                                              uint32_t tmem_base, int& stage, uint32_t& phase, int warp, int lane,
-                                              StageClock& sc) {
-    const ChainTiles ct(g);
-    const int tiles = ct.tiles, unit = blockIdx.x, units = gridDim.x;
-    const int r = 32 * (warp & 3) + lane;
-    constexpr int kPF = 3;
-    using Raw = typename std::conditional<IN == FIN_BITS, uint4, PixRaw<>>::type;
-    int t_ld = unit, kb_ld = unit < tiles ? ct.kb_begin(unit) : 0;
-    int kb_ld_end = unit < tiles ? ct.kb_end(unit) : 0;
-    RowCtx rc;
-    auto set_row = [&]() {
-        int b = 0, oy = 0, ox = 0;
-        rc.valid = t_ld < tiles && decode_row(g, ct.m(t_ld) * kRows + r, b, oy, ox);
-        rc.pix = b * g.H, rc.y0 = oy * g.SH, rc.x0 = ox * g.SW;
-    };
-    set_row();
-    Raw pf[kPF];
-    bool pv[kPF];
-    auto next_load = [&](Raw& dst, bool& v) {
-        v = rc.valid;
-        if constexpr (IN == FIN_BITS) {
-            dst = t_ld < tiles ? load_bits<true>(g, ftab, rc, kb_ld) : make_uint4(0, 0, 0, 0);
-        } else {
-            dst = load_pix<false>(g, ftab, rc);  // the pixel encoder's output: read-only in this launch
-        }
-        if (t_ld < tiles && ++kb_ld == kb_ld_end) {
-            t_ld += units;
-            kb_ld = t_ld < tiles ? ct.kb_begin(t_ld) : 0;
-            kb_ld_end = t_ld < tiles ? ct.kb_end(t_ld) : 0;
-            set_row();
-        }
-    };
-#pragma unroll
-    for (int i = 0; i < kPF; ++i) next_load(pf[i], pv[i]);
-    for (int t = unit; t < tiles; t += units) {
-        const int kb1 = ct.kb_end(t);
-        for (int kb = ct.kb_begin(t); kb < kb1; ++kb) {
-            uint4 u;
-            if constexpr (IN == FIN_BITS)
-                u = pf[0];
-            else
-                u = gather_pix(g, pf[0], pv[0]);
-#pragma unroll
-            for (int i = 0; i < kPF - 1; ++i) pf[i] = pf[i + 1], pv[i] = pv[i + 1];
-            next_load(pf[kPF - 1], pv[kPF - 1]);
-            sc.wait(&empty[stage], phase ^ 1, 0);
-            uint32_t v[32];
-            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int s8 = 0; s8 < 8; ++s8) v[8 * i + s8] = (w4[i] >> s8) & 0x01010101u;
-            tc_fence_after();
-            tmem_st32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(kChainA + stage * 32), v);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[stage]);
-            if (++stage == kStages) stage = 0, phase ^= 1;
-        }
-    }
-}
-
-__device__ __forceinline__ void chain_epilogue_bn(const ChainStage& cs, uint64_t* tfull, uint64_t* tempty,
-                                                  uint32_t tmem_base, const int* tu_s, const uint32_t* flip_s,
-                                                  uint32_t& euse, int warp, int lane, StageClock& sc) {
-    const FusedGeom& g = cs.g;
-#define BNN_CHAIN_EPI(BN, EPI) chain_epilogue<BN, EPI>(g, tfull, tempty, tmem_base, tu_s, flip_s, euse, warp, lane, sc)
-    if (cs.epi == FEPI_BITS) {
-        switch (cs.bn) {
-            case 32: BNN_CHAIN_EPI(32, FEPI_BITS); break;
-            case 64: BNN_CHAIN_EPI(64, FEPI_BITS); break;
-            case 128: BNN_CHAIN_EPI(128, FEPI_BITS); break;
-            default: BNN_CHAIN_EPI(256, FEPI_BITS); break;
-        }
-    } else {
-        switch (cs.bn) {
-            case 32: BNN_CHAIN_EPI(32, FEPI_LOGITS); break;
-            case 64: BNN_CHAIN_EPI(64, FEPI_LOGITS); break;
-            case 128: BNN_CHAIN_EPI(128, FEPI_LOGITS); break;
-            default: BNN_CHAIN_EPI(256, FEPI_LOGITS); break;
-        }
-    }
-#undef BNN_CHAIN_EPI
-}
-
-__global__ void __launch_bounds__(kThreads, 1) fused_chain_kernel(const __grid_constant__ ChainParams P) {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t* sB = smem_raw + (base - raw);  // [kStages][256 * 128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(kStages) * 256 * kKB);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int2* ftab = reinterpret_cast<int2*>(bars + 32);
-    int* tu_s = reinterpret_cast<int*>(ftab + kMaxQ);
-    uint32_t* flip_s = reinterpret_cast<uint32_t*>(tu_s + kMaxD);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = P.n;
-    // timeline stamp k of stage s: 0 producers passed the hand-off, 1 kernel entry (s = 0),
-    // 2 epilogue finished the stage, 3 TMA issued the stage's last load
-    auto stamp = [&](int s, int k) {
-        if (P.tl) P.tl[(size_t(s) * gridDim.x + blockIdx.x) * 4 + k] = gtimer();
-    };
-
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (threadIdx.x == 0) stamp(0, 1);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 4 + 1);  // four producer warps + the TMA thread
-            mbar_init(&empty[s], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0 && lane == 0)
-        for (int s = 0; s < n; ++s) tma_prefetch(&P.st[s].tm);
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        // ------------------------------------------------------ weight TMA, all stages
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            StageClock sc;
-            for (int s = 0; s < n; ++s) {
-                const ChainStage& cs = P.st[s];
-                const ChainTiles ct(cs.g);
-                const uint32_t bytes = uint32_t(cs.bn) * kKB;
-                for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x) {
-                    const int nt = ct.n(t), kb1 = ct.kb_end(t);
-                    for (int kb = ct.kb_begin(t); kb < kb1; ++kb) {
-                        sc.wait(&empty[stage], phase ^ 1, 0);
-                        mbar_arrive_expect_tx(&full[stage], bytes);
-                        tma_load_2d(&cs.tm, &full[stage], sB + size_t(stage) * 256 * kKB, kb * kKB, nt * cs.bn);
-                        if (++stage == kStages) stage = 0, phase ^= 1;
-                    }
-                }
-                sc.flush(P.dbg, s, 0, true);
-                stamp(s, 3);
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------------ UMMA issuer, all stages
-        int stage = 0;
-        uint32_t phase = 0;
-        uint32_t ause = 0;  // bit a: tempty parity of accumulator slot a
-        StageClock sc;
-        for (int s = 0; s < n; ++s) {
-            const ChainStage& cs = P.st[s];
-            const ChainTiles ct(cs.g);
-            const uint32_t idesc = idesc_i8(kRows, cs.bn);
-            const int kAcc = cs.bn <= 128 ? 2 : 1;
-            int i = 0;
-            for (int t = blockIdx.x; t < ct.tiles; t += gridDim.x, ++i) {
-                const int acc = kAcc == 2 ? (i & 1) : 0;
-                sc.wait(&tempty[acc], ((ause >> acc) & 1u) ^ 1u, 0);
-                ause ^= 1u << acc;
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + uint32_t(acc * 256);
-                const int kb0 = ct.kb_begin(t), kb1 = ct.kb_end(t);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    sc.wait(&full[stage], phase, 1);
-                    tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t b0 = smem_u32(sB + size_t(stage) * 256 * kKB);
-#pragma unroll
-                        for (int k = 0; k < kKB / 32; ++k)
-                            mma_i8_ts(d_tmem, tmem_base + uint32_t(kChainA + stage * 32 + 8 * k), sdesc_k_sw128(b0 + 32 * k),
-                                      idesc, (kb != kb0 || k != 0));
-                        mma_commit(&empty[stage]);
-                        if (kb == kb1 - 1) mma_commit(&tfull[acc]);
-                    }
-                    __syncwarp();
-                    if (++stage == kStages) stage = 0, phase ^= 1;
-                }
-            }
-            sc.flush(P.dbg, s, 1, lane == 0);
-        }
-    } else if (warp < 6 || warp >= 10) {
-        // ------------------------------------------------------ epilogue, all stages
-        const int ew = warp < 6 ? warp - 2 : warp - 6;  // 0..7
-        const int et = ew * 32 + lane;
-        uint32_t euse = 0;
-        StageClock sc;
-        for (int s = 0; s < n; ++s) {
-            const ChainStage& cs = P.st[s];
-            const FusedGeom& g = cs.g;
-            const long long tb = dclock();
-            epi_bar();  // every epilogue warp is done with the previous stage's tables
-            if (cs.epi == FEPI_BITS) {
-                const int dp = g.n_tiles * cs.bn;
-                for (int d = et; d < dp; d += 256) tu_s[d] = __ldg(g.prm + d).x;
-                for (int d0 = ew * 32; d0 < dp; d0 += 256) {
-                    const uint32_t f = __ballot_sync(0xffffffffu, __ldg(g.prm + d0 + lane).y != 0);
-                    if (lane == 0) flip_s[d0 >> 5] = f;
-                }
-            }
-            epi_bar();
-            sc.w1 += dclock() - tb;
-            chain_epilogue_bn(cs, tfull, tempty, tmem_base, tu_s, flip_s, euse, warp, lane, sc);
-            if (s + 1 < n) {  // publish: this CTA's outputs of stage s are written
-                __threadfence();
-                epi_bar();
-                if (ew == 0 && lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.done + s) : "memory");
-            }
-            sc.flush(P.dbg, s, 2, ew == 0 && lane == 0);
-            if (ew == 0 && lane == 0) stamp(s, 2);
-        }
-    } else {
-        // ------------------------------------------------------ activation producers, all stages
-        int stage = 0;
-        uint32_t phase = 0;
-        const int pt = threadIdx.x - 6 * 32;  // 0..127
-        StageClock sc;
-        for (int s = 0; s < n; ++s) {
-            const ChainStage& cs = P.st[s];
-            const FusedGeom& g = cs.g;
-            const long long tb = dclock();
-            if (s == 0) {
-                asm volatile("griddepcontrol.wait;" ::: "memory");  // the input encoder's output
-            } else if (pt == 0) {
-                unsigned seen;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(P.done + s - 1) : "memory");
-                } while (seen < gridDim.x);
-            }
-            prod_bar();  // the previous stage's producers are done with ftab; stage s-1 is complete
-            sc.w1 += dclock() - tb;
-            if (pt == 0) stamp(s, 0);
-            if (cs.in_mode == FIN_BITS) {
-                const int kw_total = (g.K + 31) >> 5;  // a partial last word holds zero pad bits
-                for (int q = pt; q < 4 * g.KB; q += 128) {
-                    int2 e = make_int2(0, -1);
-                    if (q < kw_total) {
-                        const int tap = q / g.Cw, cw = q - tap * g.Cw, ky = tap / g.KW, kx = tap - ky * g.KW;
-                        e = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), cw);
-                    }
-                    ftab[q] = e;
-                }
-            } else {
-                for (int tap = pt; tap < g.KH * g.KW; tap += 128) {
-                    const int ky = tap / g.KW, kx = tap - ky * g.KW;
-                    ftab[tap] = make_int2(((ky - g.PH) << 16) | ((kx - g.PW) & 0xffff), 0);
-                }
-            }
-            prod_bar();
-            if (cs.in_mode == FIN_BITS)
-                chain_produce<FIN_BITS>(g, ftab, full, empty, tmem_base, stage, phase, warp, lane, sc);
-            else
-                chain_produce<FIN_PIX>(g, ftab, full, empty, tmem_base, stage, phase, warp, lane, sc);
-            sc.flush(P.dbg, s, 3, pt == 0);
-        }
-    }
-
-    __syncwarp();  // reconverge role-divergent lanes: bar.sync counts a partial warp as whole
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem_base);
-    if (threadIdx.x == 0) {  // the last CTA out re-arms the stage counters for the next launch
-        __threadfence();
-        if (atomicAdd(P.done + kChainMaxStages, 1u) == gridDim.x - 1) {
-            for (int s = 0; s <= kChainMaxStages; ++s) P.done[s] = 0;
-            __threadfence();
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
 // Swapped-operand fused conv: tiles of 128 output channels (UMMA M, the weights, TMA-loaded
 // into shared memory) x 256 output positions (UMMA N, the activations, expanded by the
 // producer warps into shared memory).
@@ -1697,7 +1173,7 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
 // kernel parameter (PixParams): with the channel loops unrolled, every w_d / P_d is a
 // constant-bank operand of the XOR / compare, so a channel costs XOR, POPC, compare, select.
 template <int DW, bool F32, bool POOL>
-__global__ void __launch_bounds__(256, F32 ? 6 : 8) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
+__global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 3 : 4) : 8) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
     // PDL: the next layer may start its prologue (it waits for this grid before reading);
     // this grid waits for the pixel packer's words
     asm volatile("griddepcontrol.launch_dependents;");
@@ -2544,16 +2020,16 @@ int launch_fused_bn(int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStrea
     }
 }
 
-int g_atmem = -1;  // A operand in TMEM for CTA-local tiles (bnn_set_fused_tmem_a); -1: env / default on
 
+// CTA-local tiles only. (An int8 CTA-pair variant and a shared-memory A operand for packed-bit
+// inputs were measured no faster (profiles/r01_*) and were removed; the float-input first layer
+// keeps A in shared memory: its producers run the im2col gather.)
 template <int IN, int EPI>
 int launch_fused_cg(int cg, int BN, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
-    if (cg == 2) return launch_fused_bn<IN, EPI, 2, 0>(BN, tm, g, s);
-    if (g_atmem < 0) g_atmem = getenv("BNN_FUSED_TMEM_A") ? atoi(getenv("BNN_FUSED_TMEM_A")) : 1;
+    if (cg != 1) return fail(BNN_E_CONFIG, "fused layer: cta_group " + std::to_string(cg) + " is not supported");
     if constexpr (IN == FIN_PIX)  // 3x3 first layer: the 9-tap pixel gather
-        if (g_atmem && g.KH * g.KW == 9) return launch_fused_bn<IN, EPI, 1, 1, 9>(BN, tm, g, s);
-    if constexpr (IN != FIN_F32)
-        if (g_atmem) return launch_fused_bn<IN, EPI, 1, 1>(BN, tm, g, s);
+        if (g.KH * g.KW == 9) return launch_fused_bn<IN, EPI, 1, 1, 9>(BN, tm, g, s);
+    if constexpr (IN != FIN_F32) return launch_fused_bn<IN, EPI, 1, 1>(BN, tm, g, s);
     return launch_fused_bn<IN, EPI, 1, 0>(BN, tm, g, s);
 }
 
@@ -2626,15 +2102,6 @@ int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out
     return launch_check("pack_pixels_kernel");
 }
 
-int fused_set_tmem_a(int enabled) {
-    g_atmem = enabled ? 1 : 0;
-    return BNN_OK;
-}
-
-int fused_tmem_a() {
-    if (g_atmem < 0) g_atmem = getenv("BNN_FUSED_TMEM_A") ? atoi(getenv("BNN_FUSED_TMEM_A")) : 1;
-    return g_atmem != 0;
-}
 
 unsigned long long* fused_timeline_slot(int slots) {
     if (g_tl_used < 0 || g_tl_used + slots > kTlSlots) return nullptr;
@@ -2678,8 +2145,6 @@ int fused_timeline(int op) {
     g_tl_used = -1;
     return BNN_OK;
 }
-
-static int launch_chain_impl(const ChainParams& p, cudaStream_t s);
 
 int prep_logit_bits(const int8_t* w8, int Kpad, int K, int D, int Kw, uint32_t* wbits, cudaStream_t s) {
     const int n = D * Kw;
@@ -2763,8 +2228,29 @@ int launch_pix_popc(const FusedGeom& g, const PixParams& pp, bool f32_in, cudaSt
         const size_t smem = size_t((rows_max - 1) * g.SH + g.KH) * g.W * sizeof(uint32_t);
         if (smem <= 48 * 1024) {
             const int ntiles = int(np / 256);
+            // resident CTAs per SM for this DW and tile size (cached per DW): the grid strides
+            // the tiles over exactly the CTAs that fit, so no partial second wave
+            static int occ[9] = {};
+            auto kern_of = [](int dw) -> const void* {
+                switch (dw) {
+                    case 1: return (const void*)pix_tile_kernel<1>;
+                    case 2: return (const void*)pix_tile_kernel<2>;
+                    case 3: return (const void*)pix_tile_kernel<3>;
+                    case 4: return (const void*)pix_tile_kernel<4>;
+                    case 5: return (const void*)pix_tile_kernel<5>;
+                    case 6: return (const void*)pix_tile_kernel<6>;
+                    case 7: return (const void*)pix_tile_kernel<7>;
+                    default: return (const void*)pix_tile_kernel<8>;
+                }
+            };
+            const int dwi = std::min(std::max(g.Dw, 1), 8);
+            if (!occ[dwi]) {
+                int n = 0;
+                BNN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern_of(dwi), 256, smem));
+                occ[dwi] = std::max(1, n);
+            }
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(unsigned(std::min(ntiles, num_sms() * 8)));  // 32 registers: 8 CTAs per SM
+            cfg.gridDim = dim3(unsigned(std::min(ntiles, num_sms() * occ[dwi])));
             cfg.blockDim = dim3(256);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
@@ -2813,8 +2299,9 @@ int fused_set_fp4_pair(int mode) {
 int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
     set_last_gemm("fused_swap_mxf4");
-    // tile positions (BNN_FP4_NP): 192 measured fastest (conv 128->128 at B=4096, cycles per CTA:
-    // 192 -> 0.94 M, 224 -> 1.14 M, 240 -> 1.18 M: epilogue-bound with 4 epilogue warps)
+    // tile positions (BNN_FP4_NP, 192 or 224): 192 measured fastest (conv 128->128 at B=4096,
+    // cycles per CTA: 192 -> 0.94 M, 224 -> 1.14 M; a 240-position variant measured 1.18 M and was
+    // removed)
     static const int np = getenv("BNN_FP4_NP") ? atoi(getenv("BNN_FP4_NP")) : 192;
     if (in_mode == FIN_PIX) {
         if (g.KH * g.KW == 9) return launch_swap4_t<FIN_PIX, 9, 224>(tm4, g, s);
@@ -2842,8 +2329,7 @@ int launch_swap4(int in_mode, const CUtensorMap& tm4, const FusedGeom& g, cudaSt
                 return launch_swap4_t<FIN_BITS, 0, 224, 1, 1>(tm4, g, s);
             return launch_swap4_t<FIN_BITS, 0, 192, 1, 1>(tm4, g, s);
         }
-        if (np == 192) return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
-        return launch_swap4_t<FIN_BITS, 0, 240>(tm4, g, s);
+        return launch_swap4_t<FIN_BITS, 0, 192>(tm4, g, s);
     }
     return fail(BNN_E_CONFIG, "FP4 swapped fused layer: packed-bit or pixel input only");
 }
@@ -2859,62 +2345,9 @@ int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStre
     return fail(BNN_E_CONFIG, "swapped fused layer: packed-bit or pixel input only");
 }
 
-int launch_chain(const ChainParams& p0, cudaStream_t s) {
-    ChainParams p = p0;
-    p.tl = fused_timeline_slot(p.n);
-    for (int i = 0; p.tl && i < p.n; ++i) g_tl_names.push_back("chain stage " + std::to_string(i));
-    return launch_chain_impl(p, s);
-}
-
-static int launch_chain_impl(const ChainParams& p, cudaStream_t s) {
-    static_assert(sizeof(ChainParams) <= 4096, "kernel parameter space");
-    static bool attr_set = false;
-    if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(fused_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kChainSmem)));
-        attr_set = true;
-    }
-    set_last_gemm("fused_chain_umma_i8");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(num_sms()));  // one CTA per SM, all co-resident (stage hand-off spins)
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kChainSmem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
-    if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, fused_chain_kernel, p));
-        return launch_check("fused_chain_kernel");
-    }
-    ChainParams q = p;
-    const size_t nd = size_t(kChainMaxStages) * 16;
-    BNN_CUDA(cudaMalloc(&q.dbg, nd * sizeof(unsigned long long)));
-    BNN_CUDA(cudaMemset(q.dbg, 0, nd * sizeof(unsigned long long)));
-    BNN_CUDA(cudaLaunchKernelEx(&cfg, fused_chain_kernel, q));
-    BNN_TRY(launch_check("fused_chain_kernel"));
-    std::vector<unsigned long long> h(nd);
-    BNN_CUDA(cudaMemcpy(h.data(), q.dbg, nd * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    cudaFree(q.dbg);
-    const double g = double(num_sms());
-    for (int s = 0; s < p.n; ++s) {
-        const unsigned long long* d = h.data() + s * 16;
-        fprintf(stderr,
-                "[chain stage %d BN=%d in=%d epi=%d rows=%d D=%d KB=%d S=%d] per-CTA kcycles: tma %.1f (wait %.1f) | "
-                "mma %.1f (wait-acc %.1f wait-full %.1f) | epi %.1f (wait-acc %.1f tables %.1f) | prod %.1f (wait-slot %.1f "
-                "wait-dep %.1f)\n",
-                s, p.st[s].bn, p.st[s].in_mode, p.st[s].epi, p.st[s].g.rows, p.st[s].g.D, p.st[s].g.KB, p.st[s].g.ksplit,
-                d[3] / g / 1e3, d[0] / g / 1e3, d[7] / g / 1e3, d[4] / g / 1e3, d[5] / g / 1e3, d[11] / g / 1e3,
-                d[8] / g / 1e3, d[9] / g / 1e3, d[15] / g / 1e3, d[12] / g / 1e3, d[13] / g / 1e3);
-    }
-    return BNN_OK;
-}
-
 int launch_fused(int cg, int BN, int in_mode, int epi, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
     if (g.rows <= 0) return BNN_OK;
-    set_last_gemm(cg == 2 ? "fused_umma_i8_cg2" : (in_mode != FIN_F32 && g_atmem != 0) ? "fused_umma_i8_tmem_a" : "fused_umma_i8");
+    set_last_gemm(in_mode != FIN_F32 ? "fused_umma_i8_tmem_a" : "fused_umma_i8");
     if (in_mode == FIN_PIX) {
         if (epi == FEPI_BITS) return launch_fused_cg<FIN_PIX, FEPI_BITS>(cg, BN, tm, g, s);
         return launch_fused_cg<FIN_PIX, FEPI_NCHW>(cg, BN, tm, g, s);

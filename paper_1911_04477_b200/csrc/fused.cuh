@@ -107,24 +107,9 @@ size_t lin4_ws_bytes(const LinGeom& l);
 size_t lin4_sem_count(const LinGeom& l);
 int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s);
 
-// Chained engine (fused_chain_kernel): every stage of a network in one persistent launch.
-constexpr int kChainMaxStages = 10;
-struct ChainStage {
-    CUtensorMap tm;  // weight map with box rows = bn
-    FusedGeom g;
-    int bn, in_mode, epi, pad;
-};
-struct ChainParams {
-    ChainStage st[kChainMaxStages];
-    int n;
-    unsigned* done;  // [kChainMaxStages + 1] stage-completion counters, zero between launches
-    unsigned long long* dbg;  // per-stage role clocks (BNN_FUSED_PROFILE=1), else null
-    unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [n][grid][4], else null
-};
 // Debug timeline (globaltimer stamps per CTA and launch): op 1 enable + reset, 2 print + disable.
 int fused_timeline(int op);
 unsigned long long* fused_timeline_slot(int slots);
-int launch_chain(const ChainParams& p, cudaStream_t s);
 // Swapped-operand conv (fused_swap_kernel): 128 channels x 256 positions per tile, bits
 // epilogue, CTA-local; tm must be the weight map with box rows 128.
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);
@@ -154,8 +139,6 @@ int fused_prep_weights(const uint32_t* packed, size_t ldw, int D, int K, int C, 
 int fused_prep_params(const int8_t* w8, int Kpad, int D, int Dp, int K, const float* bias, const float* scale,
                       const float* shift, int4* prm, int* bad_dev, cudaStream_t s);
 int fused_make_tmap(CUtensorMap* map, const int8_t* w, int Dpad, int Kpad, int BN);
-int fused_set_tmem_a(int enabled);
-int fused_tmem_a();
 int fused_set_fp4_pair(int mode);
 int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out, cudaStream_t s);
 // cg = 1: CTA-local M=128 tiles; cg = 2: CTA pairs with cta_group::2 M=256 tiles. tm must be

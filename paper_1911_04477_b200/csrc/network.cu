@@ -159,8 +159,7 @@ struct bnn_net {
     bnnk::DevBuf bits[2], pix, ws, sem;
     bnnk::DevBuf lin_ws;   // split-K partial sums of the FP4 linear kernel (lin4)
     bnnk::DevBuf lin_sem;  // its per-tile counters (zeroed once; the kernel leaves them at 0)
-    bnnk::DevBuf chain_done;
-    bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)  // stage counters of the chained kernel (zeroed once; kernels re-arm them)
+    bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)
 };
 
 namespace bnnk {
@@ -672,12 +671,6 @@ int forward_layerwise(bnn_net* net, const float* x, size_t B, float* logits, cud
 }
 
 
-// bnn_set_fused_chain / BNN_FUSED_CHAIN: 1 one chained launch, 0 (default) one launch per
-// weighted layer. The chained kernel removes the ~3-4 us launch boundaries but its stages run
-// slower (one register allocation for all roles and stage shapes, 128 per thread), so at
-// the measured batches the per-layer launches win (profiles/r01_chain_*).
-int g_chain = -1;
-int g_chain_tail = -1;  // BNN_FUSED_CHAIN_TAIL: chain the trailing linear stages (default 0: measured slower)
 
 // Swapped-operand conv kernel (fused_swap_kernel: channels on the MMA's M, positions on N)
 // for conv layers with a packed-bit epilogue. BNN_FUSED_SWAP / bnn_set_fused_swap: 1 (default)
@@ -741,8 +734,6 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         net->bits_batch = B;
         ++net->arena_epoch;
     }
-    if (g_chain < 0) g_chain = getenv("BNN_FUSED_CHAIN") ? atoi(getenv("BNN_FUSED_CHAIN")) : 0;
-    if (g_chain_tail < 0) g_chain_tail = getenv("BNN_FUSED_CHAIN_TAIL") ? atoi(getenv("BNN_FUSED_CHAIN_TAIL")) : 0;
     static const bool prof = getenv("BNN_FUSED_PROFILE") != nullptr;
     // per-stage launch geometry (batch-dependent fields, tiling, buffers)
     struct Plan {
@@ -757,7 +748,6 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
     const void* in = x;
     int which = 0;
     (void)prof;
-    const bool chain_ok = !net->timing && fused_tmem_a();
     for (auto& stp : net->stages) {
         FusedStage& st = *stp;
         FusedGeom g = st.g;
@@ -794,21 +784,6 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         plans.push_back(pl);
         in = g.out_bits;
     }
-    // Chained tail: stages [first_chained, n) run in ONE persistent launch (fused_chain_kernel),
-    // the ones before it one launch each. g_chain = 1 chains every stage; g_chain_tail = 1 only
-    // the trailing run of linear stages (short, launch-latency-bound at inference batches).
-    // Both are off by default: measured slower than one launch per layer.
-    auto chain_stage_ok = [&](size_t i) {
-        const FusedStage& st = *net->stages[i];
-        return chain_ok && plans[i].cg == 1 && st.in_mode != FIN_F32 && st.epi != FEPI_NCHW;
-    };
-    size_t first_chained = plans.size();
-    while (first_chained > 0 && chain_stage_ok(first_chained - 1) &&
-           (g_chain != 0 || net->layers[net->stages[first_chained - 1]->layer]->spec.kind == BNN_LAYER_LINEAR) &&
-           plans.size() - first_chained < size_t(kChainMaxStages))
-        --first_chained;
-    if (g_chain_tail == 0 && g_chain == 0) first_chained = plans.size();
-    if (plans.size() - first_chained < 2 && g_chain == 0) first_chained = plans.size();  // nothing to save
     // one split-K workspace shared by the stages (they run one after another), sized for the
     // largest before any pointer is handed out: growing it between stages would leave the
     // earlier stages' plans pointing at freed memory
@@ -835,11 +810,14 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>(), pl.lg.sem = net->lin_sem.as<unsigned>();
     }
     size_t launches = 0;
-    for (size_t i = 0; i < first_chained; ++i) {
+    for (size_t i = 0; i < plans.size(); ++i) {
         FusedStage& st = *net->stages[i];
         const FusedGeom& g = plans[i].g;
         EventPair layer_ev(net, st.layer, 0, s);
-        if (g_pix_popc < 0) g_pix_popc = getenv("BNN_PIX_POPC") ? atoi(getenv("BNN_PIX_POPC")) : 3;
+        if (g_pix_popc < 0) {
+            g_pix_popc = getenv("BNN_PIX_POPC") ? atoi(getenv("BNN_PIX_POPC")) : 3;
+            if (g_pix_popc < 0 || g_pix_popc > 3) g_pix_popc = 3;  // the range bnn_set_fused_pix_popc accepts
+        }
         // pix_popc 1: the CUDA-core first conv reads the float input itself (no pack_pixels;
         // pix_tile_kernel stages packed input rows in shared memory when the layer allows);
         // 2: after pack_pixels; 3 (default): 1 up to batch 512 (B=256: 1.754 vs 1.731 M img/s),
@@ -876,37 +854,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         layer_ev.close();
         ++launches;
     }
-    if (first_chained < plans.size()) {
-        if (!net->chain_done.p) {
-            BNN_TRY(net->chain_done.alloc((kChainMaxStages + 1) * sizeof(unsigned)));
-            BNN_CUDA(cudaMemsetAsync(net->chain_done.p, 0, (kChainMaxStages + 1) * sizeof(unsigned), s));
-        }
-        const FusedStage& first = *net->stages[first_chained];
-        if (first.in_mode == FIN_PIX) {
-            BNN_TRY(launch_pack_pixels(x, B, first.g.C, size_t(first.g.H) * first.g.W, net->pix.as<uint32_t>(), s));
-            ++launches;
-        }
-        if (first.pre_encode) {
-            BNN_TRY(launch_pack_rows(x, B, size_t(first.g.C), net->pix.as<uint32_t>(), size_t(first.g.Cw), nullptr, s));
-            ++launches;
-        }
-        ChainParams cp;
-        memset(&cp, 0, sizeof cp);
-        cp.n = int(plans.size() - first_chained);
-        cp.done = net->chain_done.as<unsigned>();
-        for (size_t i = first_chained; i < plans.size(); ++i) {
-            const FusedStage& st = *net->stages[i];
-            ChainStage& c = cp.st[i - first_chained];
-            c.tm = st.tm[box_index(plans[i].bn)];
-            c.g = plans[i].g;
-            c.bn = plans[i].bn;
-            c.in_mode = st.in_mode;
-            c.epi = st.epi;
-        }
-        BNN_TRY(launch_chain(cp, s));
-        for (size_t i = first_chained; i < plans.size(); ++i) net->stages[i]->kname = bnn_last_gemm_kernel();
-        ++launches;
-    }
+
     net->last_launches = launches;
     return BNN_OK;
 }
@@ -1071,9 +1019,8 @@ int bnn_net_set_engine(bnn_net* net, int policy) {
 }
 
 int bnn_set_fused_tiling(int cta_group, int bn) {
-    if ((cta_group != 0 && cta_group != 1 && cta_group != 2) ||
-        (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256))
-        return fail(BNN_E_CONFIG, "fused tiling: cta_group in {0,1,2}, bn in {0,32,64,128,256}");
+    if ((cta_group != 0 && cta_group != 1) || (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 256))
+        return fail(BNN_E_CONFIG, "fused tiling: cta_group in {0,1}, bn in {0,32,64,128,256}");
     g_forced_cg = cta_group, g_forced_bn = bn;
     ++g_tiling_epoch;
     return BNN_OK;
@@ -1144,21 +1091,12 @@ int bnn_set_fused_swap(int enabled) {
     return BNN_OK;
 }
 
-int bnn_set_fused_chain(int enabled) {
-    g_chain = enabled ? 1 : 0;
-    ++g_tiling_epoch;  // captured graphs hold the other launch sequence
-    return BNN_OK;
-}
 
 int bnn_set_fused_fp4_pair(int mode) {
     ++g_tiling_epoch;  // captured graphs hold the old kernels
     return fused_set_fp4_pair(mode);
 }
 
-int bnn_set_fused_tmem_a(int enabled) {
-    ++g_tiling_epoch;  // captured graphs hold the old kernels
-    return fused_set_tmem_a(enabled);
-}
 
 int bnn_net_engine(const bnn_net* net) {
     if (use_fused(net)) return BNN_ENGINE_FUSED;

@@ -63,28 +63,21 @@ FUSABLE = {
 }
 
 
-# tilings that run all stages in one chained launch (the others: one launch per weighted layer)
-CHAINED = {"chain", "chain_nosplit", "chain_split16"}
-
-
-@pytest.fixture(params=["auto", "nohalo", "halostream", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall", "nofp4", "fp4all", "nopair", "pair224", "nosmall", "chain", "smem_a", "cg1", "cg2", "nosplit", "split16", "chain_nosplit",
-                        "chain_split16"])
+@pytest.fixture(params=["auto", "nohalo", "halostream", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall",
+                        "nofp4", "fp4all", "nopair", "pair224", "nosmall", "cg1", "nosplit", "split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
     swapped-operand conv kernels, A operand in TMEM and split-K for the small-batch linear
-    layers), with the position-major conv kernel (noswap), with all stages chained in
-    one persistent launch, with the A operand staged in shared memory, with each cta_group
-    forced, and with split-K off / forced to 16 (per-layer and chained). The CUDA-core first conv
+    layers), with the position-major conv kernel (noswap), with the halo-tile conv off or also
+    streaming its weights, with the int8 linear kernel instead of lin4, with cta_group 1 forced,
+    and with split-K off / forced to 16. The CUDA-core first conv
     (pix_popc) runs under "auto" (float input up to batch 512, else after the packer), "pixf32"
     (reading the float input itself, no packer launch) and "pixpacked"; the other settings put the
     pixel-input layer on the tensor-core kernels they select."""
     lib = bnn.load()
     p = request.param
-    bnn._lib.check(lib.bnn_set_fused_tiling({"cg1": 1, "cg2": 2}.get(p, 0), 0))
-    bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if p == "smem_a" else 1))
-    bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16, "chain_nosplit": 1,
-                                            "chain_split16": 16}.get(p, 0)))
-    bnn._lib.check(lib.bnn_set_fused_chain(1 if p in CHAINED else 0))
+    bnn._lib.check(lib.bnn_set_fused_tiling({"cg1": 1}.get(p, 0), 0))
+    bnn._lib.check(lib.bnn_set_fused_split({"nosplit": 1, "split16": 16}.get(p, 0)))
     bnn._lib.check(lib.bnn_set_fused_swap({"noswap": 0, "swapall": 2}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_small_logits(0 if p == "nosmall" else 1))
     bnn._lib.check(lib.bnn_set_fused_pix_popc({"auto": 3, "pixf32": 1, "pixpacked": 2}.get(p, 0)))
@@ -94,9 +87,7 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_lin4(0 if p == "nolin4" else 1))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
-    lib.bnn_set_fused_tmem_a(1)
     lib.bnn_set_fused_split(0)
-    lib.bnn_set_fused_chain(0)
     lib.bnn_set_fused_swap(1)
     lib.bnn_set_fused_small_logits(1)
     lib.bnn_set_fused_pix_popc(3)
@@ -121,29 +112,23 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     net = fused()
     x = orc.fill_random((batch, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     got = net.forward(x)
-    # first-layer pixel encoder + one launch per weighted layer (10), or + one chained launch (2)
     # pack_pixels + 9 weighted layers, or 9 when the CUDA-core first conv reads the floats itself
-    assert net.last_launches() == (2 if tiling in CHAINED else 9 if tiling in ("auto", "pixf32") else 10)
+    assert net.last_launches() == (9 if tiling in ("auto", "pixf32") else 10)
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 
-@pytest.mark.parametrize("mode", ["chain", "cg1_tmem", "cg1_smem", "cg2"])
 @pytest.mark.parametrize("bn", [32, 64, 128, 256])
-def test_forced_tile_shapes_vs_oracle(bnn, orc, mode, bn):
+def test_forced_tile_shapes_vs_oracle(bnn, orc, bn):
     lib = bnn.load()
     net = bnn.Network(seed=1)
     net.set_engine("fused")
     x = orc.fill_random((9, 3, 32, 32), orc.mix64(2, INPUT_STREAM))
     try:
-        bnn._lib.check(lib.bnn_set_fused_tiling(2 if mode == "cg2" else 1, bn))
-        bnn._lib.check(lib.bnn_set_fused_tmem_a(0 if mode == "cg1_smem" else 1))
-        bnn._lib.check(lib.bnn_set_fused_chain(1 if mode == "chain" else 0))
+        bnn._lib.check(lib.bnn_set_fused_tiling(1, bn))
         got = net.forward(x)
     finally:
         lib.bnn_set_fused_tiling(0, 0)
-        lib.bnn_set_fused_tmem_a(1)
-        lib.bnn_set_fused_chain(0)
-    assert np.array_equal(got, orc.net(seed=1).forward(x)), (mode, bn)
+    assert np.array_equal(got, orc.net(seed=1).forward(x)), bn
 
 
 def test_default_network_fused_equals_generic_large_batch(bnn, orc, fused):

@@ -1,9 +1,8 @@
-"""Launch timeline of the fused engine (bnn_debug_timeline): per launch / chain stage, the
-min/median/max over CTAs of four globaltimer stamps, in us from the first stamp.
+"""Launch timeline of the fused engine (bnn_debug_timeline): per launch, the min/median/max over
+CTAs of four globaltimer stamps, in us from the first stamp.
 
-    python tools/timeline.py [B] [chain 0|1]
-Per-layer launches: k0 entry, k1 after the TMEM dealloc (last), k2 griddepcontrol.wait returned, k3 roles done.
-Chain stages: k0 producers passed the hand-off, k1 kernel entry, k2 epilogue done, k3 TMA done.
+    python tools/timeline.py [B]
+k0 entry, k1 after the TMEM dealloc (last), k2 griddepcontrol.wait returned, k3 roles done.
 """
 import os
 import sys
@@ -15,8 +14,6 @@ import paper_1911_04477_b200 as bnn  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 lib = bnn.load()
-if len(sys.argv) > 2:
-    lib.bnn_set_fused_chain(int(sys.argv[2]))
 net = bnn.Network(seed=1)
 s = torch.cuda.current_stream().cuda_stream  # legacy stream: eager launches (no graph)
 x = torch.empty((B, 3, 32, 32), dtype=torch.float32, device="cuda")
