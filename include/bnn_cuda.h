@@ -52,11 +52,12 @@ typedef enum {
 const char* bnn_last_error(void);
 int bnn_version(void);
 /* Name of the kernel variant the last GEMM call on this thread dispatched to
- * ("popc", "umma_i8", ...); for tests and the benchmark. */
+ * ("popc", "xnor4_kernel", ...); for tests and the benchmark. */
 const char* bnn_last_gemm_kernel(void);
-/* K3 kernel selection (process-wide). AUTO picks the integer-pipe kernel below ~2^27
- * bit-MACs and the tcgen05 int8 tensor-core kernel above ("K3 candidates");
- * POPC / UMMA force one of them (used by the parity tests to cover both). */
+/* K3 kernel selection (process-wide). AUTO picks the integer-pipe kernel below ~2^26
+ * bit-MACs and the tcgen05 FP4 tensor-core kernel (operands expanded from the packed bits in
+ * shared memory) above ("K3 candidates"); POPC / UMMA force one of them (used by the
+ * parity tests to cover both). */
 enum { BNN_GEMM_AUTO = 0, BNN_GEMM_POPC = 1, BNN_GEMM_UMMA = 2 };
 int bnn_set_gemm_policy(int policy);
 

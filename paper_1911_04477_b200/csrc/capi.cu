@@ -88,34 +88,22 @@ int launch_pack_rows(const float*, size_t, size_t, uint32_t*, size_t, unsigned l
 int launch_im2col_sign_pack(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*,
                             uint32_t*, size_t, cudaStream_t);
 
-int launch_unpack_s8(const uint32_t*, size_t, size_t, size_t, int8_t*, size_t, cudaStream_t);
-int umma_gemm_s32(const int8_t*, size_t, const int8_t*, size_t, size_t, size_t, size_t, int32_t*,
-                  size_t, cudaStream_t);
-int umma_gemm_f32(const int8_t*, size_t, const int8_t*, size_t, size_t, size_t, size_t, const float*,
-                  size_t, float*, cudaStream_t);
+int xnor4_gemm_s32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, int32_t*, size_t,
+                   cudaStream_t);
+int xnor4_gemm_f32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, const float*, size_t,
+                   float*, cudaStream_t);
 
 namespace {
 int g_policy = BNN_GEMM_AUTO;
 
-// Size rule: the tensor-core path pays an unpack pass
-// (1 bit -> 1 byte per operand element, two launches) and a ~18 us floor; below ~2^31
-// bit-MACs the single-launch integer-pipe kernel finishes first (profiles/r01_gemm_crossover:
-// 1024^3 popc 14.9 us vs 20.7; 1000x1024x4096 popc 41 us vs 29).
+// Size rule: both paths are one launch straight from the packed
+// bits (gemm4.cu expands the operands to e2m1 in shared memory); the integer-pipe kernel is
+// faster only for the smallest products (below ~2^26 bit-MACs, measured in
+// profiles/r02_gemm_crossover.jsonl).
 bool use_umma(size_t M, size_t N, size_t L) {
     if (g_policy == BNN_GEMM_POPC) return false;
     if (g_policy == BNN_GEMM_UMMA) return true;
-    return double(M) * double(N) * double(L) >= 2147483648.0;
-}
-
-// Unpack both packed operands to int8 rows (stride round_up(L, 32)) in stream-ordered scratch.
-int unpack_operands(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N,
-                    size_t L, Scratch& sw, Scratch& sx, size_t& ldk, cudaStream_t s) {
-    ldk = (L + 31) / 32 * 32;
-    BNN_TRY(sw.alloc(M * ldk, s));
-    BNN_TRY(sx.alloc(N * ldk, s));
-    BNN_TRY(launch_unpack_s8(w, ldw, M, L, sw.as<int8_t>(), ldk, s));
-    BNN_TRY(launch_unpack_s8(x, ldx, N, L, sx.as<int8_t>(), ldk, s));
-    return BNN_OK;
+    return double(M) * double(N) * double(L) >= 67108864.0;
 }
 }  // namespace
 
@@ -124,12 +112,7 @@ int unpack_operands(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx
 int gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N,
              size_t L, int32_t* out, size_t ldo, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
-    if (use_umma(M, N, L)) {
-        Scratch sw, sx;
-        size_t ldk;
-        BNN_TRY(unpack_operands(w, ldw, x, ldx, M, N, L, sw, sx, ldk, s));
-        return umma_gemm_s32(sw.as<int8_t>(), ldk, sx.as<int8_t>(), ldk, M, N, ldk, out, ldo, s);
-    }
+    if (use_umma(M, N, L)) return xnor4_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
     return popc_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
 }
 
@@ -137,12 +120,7 @@ int gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_
              size_t L, const float* bias, size_t P, float* out, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
     if (P == 0 || N % P != 0) return fail(BNN_E_SHAPE, "xnor_gemm: N must be a multiple of P");
-    if (use_umma(M, N, L)) {
-        Scratch sw, sx;
-        size_t ldk;
-        BNN_TRY(unpack_operands(w, ldw, x, ldx, M, N, L, sw, sx, ldk, s));
-        return umma_gemm_f32(sw.as<int8_t>(), ldk, sx.as<int8_t>(), ldk, M, N, ldk, bias, P, out, s);
-    }
+    if (use_umma(M, N, L)) return xnor4_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
     return popc_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
 }
 

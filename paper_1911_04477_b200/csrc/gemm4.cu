@@ -1,0 +1,297 @@
+// K3 on the FP4 tensor cores for the standalone operator API: xnor_gemm (kernels.cpp:53-88),
+// its float epilogue (to_float + bias_add, kernels.cpp:90-107) and the conv_forward_binary
+// scatter (reshape_output, lowering.cpp:87-95), in ONE launch straight from the packed bits.
+//
+// Both operands are the reference's packed lines (W row-packed [M x ldw], X col-packed
+// [N x ldx], bit j of word q = element 32q + j, 1 = +1) expanded in shared memory to e2m1
+// {+1.0, -1.0} (codes 0x2 / 0xA) and 0.0 (0x0) for the pad bits past L. The f32 accumulator of
+// kind::mxf4 (block scales 2^0) then holds sum_k w_k x_k = L - 2 popc(w ^ x) exactly (|sum| <= L
+// < 2^24): the reference's xnor_gemm value, with no correction term. (The previous tensor-core
+// path unpacked both operands to int8 in HBM first: two extra launches and 8x the bytes.)
+//
+// CTA anatomy (448 threads): warp 1 TMEM allocator + MMA issuer (converged warp, elected
+// lane), warps 2-5 epilogue (lane = output row m), warps 6-13 producers (thread t expands W line
+// t and X line t of the tile for each 256-element K block). One 128 x NB tile per CTA (NB <= 256
+// columns chosen so the tiles fill the SMs), persistent over tiles when there are more.
+#include <algorithm>
+#include <cstdio>
+
+#include "bnn_common.cuh"
+#include "umma.cuh"
+
+namespace bnnk {
+
+using namespace umma;
+
+namespace {
+
+constexpr int kGThreads = 448;
+constexpr int kGMaxStages = 8;
+constexpr int kGSfCol = 496;
+constexpr size_t kGSmemMax = 232448;
+
+struct G4 {
+    const uint32_t* w;
+    size_t ldw;
+    const uint32_t* x;
+    size_t ldx;
+    int M, N, L, Lw;     // Lw = ceil(L / 32) words per line
+    int KB;              // 256-element K blocks
+    int NB, m_tiles, n_tiles, nst;
+    int32_t* out_s32;    // [M, ldo] (s32 epilogue) or null
+    size_t ldo;
+    float* out_f32;      // [N / P][M][P] (f32 epilogue: float(acc) + bias[m])
+    const float* bias;
+    int P;
+};
+
+__host__ __device__ constexpr uint32_t idesc_mxf4_m128(int N) {
+    return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_mxf4_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf)
+        : "memory");
+}
+
+// 32 elements (bits b, valid mask m) -> 16 bytes of e2m1 at 16-byte chunk `chunk` of SW128 row r:
+// element 8s + n holds element 4n + s of the word (the same permutation for both operands), code
+// 0x2 (+1) for a set bit, 0xA (-1) for a clear one, 0x0 past L.
+__device__ __forceinline__ void put_pm1(uint32_t tile, int r, int chunk, uint32_t b, uint32_t m) {
+    uint32_t o[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const uint32_t xs = (b >> s) & 0x11111111u, ms = (m >> s) & 0x11111111u;
+        o[s] = (ms << 1) | ((ms & ~xs) << 3);
+    }
+    st_shared_v4(tile + uint32_t(r) * 128u + (uint32_t(chunk ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+}
+
+// Words [8kb, 8kb + 8) of line `line` (8 words, zero past the line) and their valid-bit masks.
+__device__ __forceinline__ void load_block(const uint32_t* base, size_t ld, int line, bool live, int kb, int Lw, int L,
+                                           uint32_t (&w)[8], uint32_t (&m)[8]) {
+    const uint32_t* src = base + size_t(live ? line : 0) * ld;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int q = 8 * kb + k;
+        w[k] = (live && q < Lw) ? __ldg(src + q) : 0u;
+        const int nv = L - 32 * q;  // valid elements in word q
+        m[k] = !live || nv <= 0 ? 0u : nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+    }
+}
+
+__global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_constant__ G4 g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const int nst = g.nst;
+    uint8_t* sA = smem_raw + (base - raw);            // [nst][128 x 128 B]
+    uint8_t* sB = sA + size_t(nst) * 16384;           // [nst][NB x 128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(nst) * g.NB * 128);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kGMaxStages;
+    uint64_t* tfull = bars + 2 * kGMaxStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = g.m_tiles * g.n_tiles;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 8);  // the 8 producer warps
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 4);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (warp >= 2 && warp < 6) {  // block scales: every byte of columns [496, 512) = 2^0
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+        const uint32_t lb = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
+        tmem_st8(lb + kGSfCol, v);
+        tmem_st8(lb + kGSfCol + 8, v);
+        tmem_st_wait();
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 1) {
+        const uint32_t idesc = idesc_mxf4_m128(g.NB);
+        int stage = 0, i = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            mbar_wait(tempty, (i & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < g.KB; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sA + size_t(stage) * 16384);
+                const uint32_t b0 = smem_u32(sB + size_t(stage) * g.NB * 128);
+                const int nk = min(4, (g.L - 256 * kb + 63) / 64);  // 64-element steps with data
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= nk) break;
+                    mma_mxf4_w(tmem_base, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                               tmem_base + kGSfCol, (kb != 0 || k != 0));
+                }
+                mma_commit_w(&empty[stage]);
+                if (kb == g.KB - 1) mma_commit_w(tfull);
+                __syncwarp();
+                if (++stage == nst) stage = 0, phase ^= 1;
+            }
+        }
+        mbar_wait(tempty, (i & 1) ^ 1);
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    } else if (warp >= 2 && warp < 6) {
+        // epilogue: lane = output row m, TMEM columns = output columns n
+        const int q = warp & 3;
+        int i = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+            const int m = mt * 128 + q * 32 + lane, n0 = nt * g.NB;
+            mbar_wait(tfull, i & 1);
+            tc_fence_after();
+            const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16);
+            const float bv = (g.out_f32 && g.bias && m < g.M) ? __ldg(g.bias + m) : 0.0f;
+            for (int c = 0; c < (g.NB + 31) / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tb + uint32_t(32 * c), v);
+                tmem_ld_wait();
+                if (m >= g.M) continue;
+                const int nb = n0 + 32 * c;
+                if (g.out_s32) {
+                    int32_t* orow = g.out_s32 + size_t(m) * g.ldo + nb;
+                    const bool vec = nb + 32 <= g.N && 32 * c + 32 <= g.NB && (g.ldo & 3) == 0 &&
+                                     ((reinterpret_cast<uintptr_t>(g.out_s32) & 15) == 0);
+                    if (vec) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<int4*>(orow + j) =
+                                make_int4(int(__uint_as_float(v[j])), int(__uint_as_float(v[j + 1])),
+                                          int(__uint_as_float(v[j + 2])), int(__uint_as_float(v[j + 3])));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (nb + j < g.N && 32 * c + j < g.NB) orow[j] = int(__uint_as_float(v[j]));
+                    }
+                } else {
+                    // to_float (exact: |acc| < 2^24) + bias_add, scattered to [img][m][p]
+#pragma unroll 4
+                    for (int j = 0; j < 32; ++j) {
+                        const int n = nb + j;
+                        if (n >= g.N || 32 * c + j >= g.NB) break;
+                        const int img = n / g.P, p = n - img * g.P;
+                        g.out_f32[(size_t(img) * g.M + m) * g.P + p] = __fadd_rn(__uint_as_float(v[j]), bv);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+        }
+    } else if (warp >= 6) {
+        // producers: thread t expands W line mt*128 + t (t < 128) and X line nt*NB + t (t < NB)
+        const int t = int(threadIdx.x) - 6 * 32;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+            const int am = mt * 128 + t, bn = nt * g.NB + t;
+            const bool has_a = t < 128, has_b = t < g.NB;
+            for (int kb = 0; kb < g.KB; ++kb) {
+                uint32_t aw[8], am8[8], bw[8], bm8[8];
+                load_block(g.w, g.ldw, am, has_a && am < g.M, kb, g.Lw, g.L, aw, am8);
+                load_block(g.x, g.ldx, bn, has_b && bn < g.N, kb, g.Lw, g.L, bw, bm8);
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t ta = smem_u32(sA + size_t(stage) * 16384);
+                const uint32_t tbb = smem_u32(sB + size_t(stage) * g.NB * 128);
+                if (has_a) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) put_pm1(ta, t, k, aw[k], am8[k]);
+                }
+                if (has_b) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) put_pm1(tbb, t, k, bw[k], bm8[k]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[stage]);
+                if (++stage == nst) stage = 0, phase ^= 1;
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+}
+
+int launch_xnor4(G4 g, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(xnor4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGSmemMax)));
+        attr_set = true;
+    }
+    g.Lw = (g.L + 31) / 32;
+    g.KB = (g.L + 255) / 256;
+    g.m_tiles = (g.M + 127) / 128;
+    // image columns per tile: the widest NB (<= 256, multiple of 16) that still gives every SM a
+    // tile, and never wider than N needs
+    const int sms = num_sms();
+    int nb = 256;
+    const int n16 = (g.N + 15) / 16 * 16;
+    while (nb > 16 && (long(g.m_tiles) * ((g.N + nb - 1) / nb) < sms || nb / 2 >= n16)) nb /= 2;
+    g.NB = std::min(nb, n16);
+    g.n_tiles = (g.N + g.NB - 1) / g.NB;
+    g.nst = int(std::min<size_t>(kGMaxStages, (kGSmemMax - 1024 - 256) / (16384 + size_t(g.NB) * 128)));
+    const int units = g.m_tiles * g.n_tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min(units, sms)));
+    cfg.blockDim = dim3(unsigned(kGThreads));
+    cfg.dynamicSmemBytes = 1024 + size_t(g.nst) * (16384 + size_t(g.NB) * 128) + 256;
+    cfg.stream = s;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, xnor4_kernel, g));
+    set_last_gemm("xnor4_kernel");
+    return launch_check("xnor4_kernel");
+}
+
+}  // namespace
+
+// xnor_gemm on the FP4 tensor cores, s32 output [M, ldo] (kernels.cpp:53-88).
+int xnor4_gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N, size_t L,
+                   int32_t* out, size_t ldo, cudaStream_t s) {
+    if (M == 0 || N == 0) return BNN_OK;
+    G4 g{};
+    g.w = w, g.ldw = ldw, g.x = x, g.ldx = ldx, g.M = int(M), g.N = int(N), g.L = int(L);
+    g.out_s32 = out, g.ldo = ldo, g.P = 1;
+    return launch_xnor4(g, s);
+}
+
+// xnor_gemm -> to_float -> bias_add, written as [N / P][M][P] (P = N for a linear layer,
+// oh*ow for a conv: reshape_output, lowering.cpp:87-95).
+int xnor4_gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N, size_t L,
+                   const float* bias, size_t P, float* out, cudaStream_t s) {
+    if (M == 0 || N == 0) return BNN_OK;
+    G4 g{};
+    g.w = w, g.ldw = ldw, g.x = x, g.ldx = ldx, g.M = int(M), g.N = int(N), g.L = int(L);
+    g.out_f32 = out, g.bias = bias, g.P = int(P ? P : N);
+    return launch_xnor4(g, s);
+}
+
+}  // namespace bnnk

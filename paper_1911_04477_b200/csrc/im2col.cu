@@ -68,58 +68,69 @@ __global__ void __launch_bounds__(256)
     if (j0 + line < lines && k0 + kq < wpl) words[(j0 + line) * ld + k0 + kq] = tile[line][kq];
 }
 
-// Row-bits kernel (W <= 32, the CIFAR-class shapes): one block per (image, output row).
-//  1. Sign-pack every input row the block needs — rows iy = oy*sH - pH + kh of all C
-//     channels — into one word each (warp load of the row + __ballot_sync), in smem.
-//  2. Warp w builds output word q (w, w+8, ...) for all ow positions of the row at once:
-//     lane b owns patch row r = 32q + b = (c*kH + kh)*kW + kw, i.e. input row (c, kh) and
-//     tap kw; for position ox its bit is bit ox*sW - pW + kw of that row word (padding
-//     columns are 1 bits of a 64-bit window), and one __ballot_sync over the lanes yields
-//     the whole word for that position (the lane = r bit order is the word's bit order).
-//     With stride 1 the 32 ballots are one 32 x 32 bit transpose across the warp (five
-//     shuffle-xor butterfly rounds), about one instruction per output word.
-//  3. The block's [ow lines x wpl words] output is staged in smem and stored line-contiguous.
+// Row-bits kernel (W <= 32, the CIFAR-class shapes): one block per (image, group of R output
+// rows).
+//  1. Sign-pack every input row the group needs — rows (oy0*sH - pH) .. of all C channels, each
+//     read ONCE per group (R rows share their kH - sH halo rows) — into one word each, in smem.
+//     W % 4 == 0: float4 loads, 8 lanes per input row (4 rows per warp instruction), the row
+//     word assembled with 3 shuffle-xor ORs; otherwise a warp-wide load and a ballot per row.
+//  2. Warp w builds output word q (w, w+8, ...) for all ow positions of each row of the group:
+//     lane b owns patch row r = 32q + b = (c*kH + kh)*kW + kw, i.e. input row (c, kh) and tap
+//     kw; for position ox its bit is bit ox*sW - pW + kw of that row word (padding columns are
+//     1 bits of a 64-bit window). With stride 1 the 32 positions' words are one 32 x 32 bit
+//     transpose across the warp (five shuffle-xor butterfly rounds), else one ballot each.
+//  3. The group's [R*ow lines x wpl words] output is staged in smem and stored line-contiguous.
 __global__ void __launch_bounds__(256)
     im2col_rowbits_kernel(const float* __restrict__ x, int C, int H, int W, int kH, int kW, int sH, int sW,
-                          int pH, int pW, int oh, int ow, int K, int wpl, uint32_t* __restrict__ words,
+                          int pH, int pW, int oh, int ow, int K, int wpl, int R, uint32_t* __restrict__ words,
                           size_t ld) {
     extern __shared__ uint32_t sm[];
-    const int nrows = C * kH;
-    uint32_t* rows = sm;                // [C * kH] row words
-    uint32_t* tile = rows + nrows;      // [ow][wpl]
-    const int oy = blockIdx.x, img = blockIdx.y;
+    const int oy0 = blockIdx.x * R, img = blockIdx.y;
+    const int ry = min(R, oh - oy0);                  // output rows of this group
+    const int nrow = (ry - 1) * sH + kH;              // input rows per channel
+    uint32_t* rows = sm;                              // [C][nrow] row words
+    uint32_t* tile = rows + C * nrow;                 // [ry * ow][wpl]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    // 1. input rows -> sign words (bit ix = x[img, c, iy, ix] >= 0; columns >= W are 1 = padding).
-    // Warp w takes channels [4w, 4w + 4), [4w + 32, ...): kH rows each.
-    const float* xb = x + size_t(img) * C * H * W + (lane < W ? lane : 0);
-    const int iy0 = oy * sH - pH;
-    constexpr int kU = 4;  // measured: 4 beats 16 (0.164 vs 0.207 ms at [256,128,32,32])
-    for (int c0 = warp * kU; c0 < C; c0 += nwarps * kU) {
-        for (int kh = 0; kh < kH; ++kh) {
-            const int iy = iy0 + kh;
-            const bool rin = unsigned(iy) < unsigned(H);
-            float v[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-                v[u] = rin && c0 + u < C && lane < W ? __ldg(xb + (size_t(c0 + u) * H + iy) * W) : 0.0f;
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                // a padding row (iy outside): every tap reads 0.0 -> +1
-                const uint32_t bits = __ballot_sync(0xffffffffu, v[u] >= 0.0f);
-                if (lane == 0 && c0 + u < C) rows[(c0 + u) * kH + kh] = bits;
-            }
+    const int iyb = oy0 * sH - pH;                    // input row of local row 0
+    const float* xb = x + size_t(img) * C * H * W;
+    // 1. input rows -> sign words (bit ix = x[img, c, iy, ix] >= 0; an out-of-image row reads
+    // 0.0 everywhere -> all +1; bits >= W are don't-care: the window below masks them to 1)
+    const int total = C * nrow;
+    if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const int sub = lane >> 3, col = 4 * (lane & 7);
+        for (int t0 = warp * 4; t0 < total; t0 += nwarps * 4) {
+            const int t = t0 + sub;
+            const int c = t / nrow, lr = t - c * nrow, iy = iyb + lr;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (t < total && unsigned(iy) < unsigned(H) && col < W)
+                v = __ldg(reinterpret_cast<const float4*>(xb + (size_t(c) * H + iy) * W + col));
+            uint32_t b = (uint32_t(v.x >= 0.0f) | (uint32_t(v.y >= 0.0f) << 1) | (uint32_t(v.z >= 0.0f) << 2) |
+                          (uint32_t(v.w >= 0.0f) << 3))
+                         << col;
+            b |= __shfl_xor_sync(0xffffffffu, b, 1);
+            b |= __shfl_xor_sync(0xffffffffu, b, 2);
+            b |= __shfl_xor_sync(0xffffffffu, b, 4);
+            if ((lane & 7) == 0 && t < total) rows[t] = b;
+        }
+    } else {
+        for (int t = warp; t < total; t += nwarps) {
+            const int c = t / nrow, lr = t - c * nrow, iy = iyb + lr;
+            const float v = unsigned(iy) < unsigned(H) && lane < W ? __ldg(xb + (size_t(c) * H + iy) * W + lane) : 0.0f;
+            const uint32_t bits = __ballot_sync(0xffffffffu, v >= 0.0f);
+            if (lane == 0) rows[t] = bits;
         }
     }
     __syncthreads();
-    // 2. word q of every position: lane = patch row r
+    // 2. word q of every position of every row of the group: lane = patch row r
     const int kk = kH * kW;
     const uint64_t pad = ~(((1ull << W) - 1ull) << 16);  // row at bits [16, 16 + W), the rest 1
-    for (int q = warp; q < wpl; q += nwarps) {
+    for (int yq = warp; yq < ry * wpl; yq += nwarps) {
+        const int yy = yq / wpl, q = yq - yy * wpl;
         const int r = q * 32 + lane;
         const bool rv = r < K;  // bits past K are 0
         const int c = r / kk, t = r - c * kk, kh = t / kW, kw = t - kh * kW;
-        const uint64_t win = rv ? ((uint64_t(rows[c * kH + kh]) << 16) | pad) : 0ull;
+        const uint64_t win = rv ? ((uint64_t(rows[c * nrow + yy * sH + kh]) << 16) | pad) : 0ull;
         const int sh0 = 16 - pW + kw;  // window bit of position ox: sh0 + ox * sW
         for (int ox0 = 0; ox0 < ow; ox0 += 32) {
             uint32_t mine = 0;
@@ -143,16 +154,20 @@ __global__ void __launch_bounds__(256)
                     if (lane == j) mine = wbits;
                 }
             }
-            if (ox0 + lane < ow) tile[(ox0 + lane) * wpl + q] = mine;
+            if (ox0 + lane < ow) tile[(yy * ow + ox0 + lane) * wpl + q] = mine;
         }
     }
     __syncthreads();
-    // 3. store the [ow x wpl] tile: lines img*oh*ow + oy*ow + ox
-    const int total = ow * wpl;
-    uint32_t* dst = words + (size_t(img) * oh * ow + size_t(oy) * ow) * ld;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-        const int ox = t / wpl, q = t - ox * wpl;
-        dst[size_t(ox) * ld + q] = tile[t];
+    // 3. store the [ry*ow x wpl] tile: lines img*oh*ow + oy0*ow + (yy*ow + ox)
+    const int tot = ry * ow * wpl;
+    uint32_t* dst = words + (size_t(img) * oh * ow + size_t(oy0) * ow) * ld;
+    if (ld == size_t(wpl)) {
+        for (int t = threadIdx.x; t < tot; t += blockDim.x) dst[t] = tile[t];
+    } else {
+        for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+            const int l = t / wpl, q = t - l * wpl;
+            dst[size_t(l) * ld + q] = tile[t];
+        }
     }
 }
 
@@ -170,17 +185,23 @@ int launch_im2col_sign_pack(const float* x, size_t B, size_t C, size_t H, size_t
     if (ld < wpl) return fail(BNN_E_SHAPE, "im2col: leading dimension smaller than ceil(K/32)");
     const size_t lines = B * oh * ow;
     if (lines == 0) return BNN_OK;
-    const size_t kW = g->kernel_w, pW = g->pad_w;
-    const size_t smem = (C * g->kernel_h + ow * wpl) * sizeof(uint32_t);
+    const size_t kW = g->kernel_w, pW = g->pad_w, kH = g->kernel_h, sH = g->stride_h;
     // row-bits kernel: rows fit one word, padding windows stay inside the 64-bit shift (input
-    // column of a tap in [-16, 48)), and enough (image, row) blocks to fill the GPU (a batch-1
-    // layer takes the general kernel)
-    if (W <= 32 && pW <= 16 && smem <= 48 * 1024 && oh < 65536 && B < 65536 &&
-        (ow - 1) * g->stride_w + kW <= 48 + pW && B * oh >= size_t(num_sms())) {
-        im2col_rowbits_kernel<<<dim3(unsigned(oh), unsigned(B)), 256, smem, s>>>(
-            x, int(C), int(H), int(W), int(g->kernel_h), int(kW), int(g->stride_h), int(g->stride_w),
-            int(g->pad_h), int(pW), int(oh), int(ow), int(K), int(wpl), words, ld);
-        return launch_check("im2col_rowbits_kernel");
+    // column of a tap in [-16, 48)). Output rows per block R: the most that keep the block's
+    // smem <= 48 KB and still give every SM two blocks (a batch-1 layer: R = 1, or the general
+    // kernel when even that leaves SMs idle).
+    if (W <= 32 && pW <= 16 && oh < 65536 && B < 65536 && (ow - 1) * g->stride_w + kW <= 48 + pW) {
+        auto smem_of = [&](size_t R) { return (C * ((R - 1) * sH + kH) + R * ow * wpl) * sizeof(uint32_t); };
+        size_t R = 1;
+        while (R < 16 && R * 2 <= oh && smem_of(R * 2) <= 48 * 1024 &&
+               B * ceil_div(oh, R * 2) >= 2 * size_t(num_sms()))
+            R *= 2;
+        if (smem_of(R) <= 48 * 1024 && B * ceil_div(oh, R) >= size_t(num_sms())) {
+            im2col_rowbits_kernel<<<dim3(unsigned(ceil_div(oh, R)), unsigned(B)), 256, smem_of(R), s>>>(
+                x, int(C), int(H), int(W), int(kH), int(kW), int(sH), int(g->stride_w), int(g->pad_h), int(pW),
+                int(oh), int(ow), int(K), int(wpl), int(R), words, ld);
+            return launch_check("im2col_rowbits_kernel");
+        }
     }
     dim3 grid(unsigned(ceil_div(lines, 32)), unsigned(ceil_div(wpl, kWordsPerBlock)));
     im2col_sign_pack_kernel<<<grid, dim3(32, kWordsPerBlock), 0, s>>>(

@@ -359,7 +359,7 @@ def test_gemm_kernels_vs_oracle(bnn, orc, policy, kernel, m, n, L):
     w = orc.pack(orc.fill_random((m, L), m + 7), "rows", True)
     x = orc.pack(orc.fill_random((L, n), n + 9), "cols", True)
     got = bnn.xnor_gemm(bnn.PackedBitMatrix(m, L, "rows", w), bnn.PackedBitMatrix(L, n, "cols", x), L)
-    assert bnn.load().bnn_last_gemm_kernel().decode() == ("popc" if kernel == "popc" else "umma_i8")
+    assert bnn.load().bnn_last_gemm_kernel().decode() == ("popc" if kernel == "popc" else "xnor4_kernel")
     assert np.array_equal(got, orc.xnor_gemm(w, x, L))
 
 
