@@ -249,6 +249,38 @@ def _dev_time(fn, st, flush, iters):
     return tot / iters
 
 
+def _graph_time(fn, st, flush, reps=20):
+    """Device ms per call of fn() (a stream-ordered C-ABI call on st): `reps` calls captured into
+    one CUDA graph and replayed between CUDA events, so host-side call overhead (ctypes, argument
+    checks, launch) is not in the number; L2 is flushed before the replay (outside the events),
+    the calls inside run back to back (operands L2-warm after the first). None if the call
+    sequence cannot be captured."""
+    import torch
+
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            fn()
+            st.synchronize()
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(reps):
+                    fn()
+            g.replay()
+            st.synchronize()
+            tot = 0.0
+            for i in range(3):
+                flush.fill_(float(i))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                g.replay()
+                e1.record(st)
+                st.synchronize()
+                tot += e0.elapsed_time(e1)
+        return tot / 3 / reps
+    except Exception:  # not capturable: report the host-visible timing only
+        return None
+
+
 def _max_over_ranks(v: float, world: int, dev) -> float:
     if world == 1:
         return v
@@ -331,12 +363,16 @@ def measure_configs(lib, dev, st, flush, seed, peaks, cpu, world, rank):
     gemm_kernel = lib.bnn_last_gemm_kernel().decode()
     ms_enc = _max_over_ranks(_dev_time(f_enc, st, flush, 20), world, dev)
     ms_gemm = _max_over_ranks(_dev_time(f_gemm, st, flush, 20), world, dev)
+    dev_lin, dev_enc, dev_gemm = (_graph_time(f, st, flush) for f in (f_lin, f_enc, f_gemm))
     bops = 2.0 * M * N * K
     c1 = {"shape": "linear_forward_packed x[1024,1024] f32, W 1024x1024 packed (BASELINE configs[0])",
           "sharding": f"{world} rank(s) x {nc} columns", "ms": ms, "binary_tops": bops / (ms * 1e-3) / 1e12,
           "gemm_kernel": gemm_kernel, "encode_ms": ms_enc, "xnor_gemm_ms": ms_gemm,
           "xnor_gemm_tops": bops / (ms_gemm * 1e-3) / 1e12,
-          "xnor_gemm_frac_of_int8_peak": (bops / (ms_gemm * 1e-3) / 1e12) / int8_peak}
+          "xnor_gemm_frac_of_int8_peak": (bops / (ms_gemm * 1e-3) / 1e12) / int8_peak,
+          "device_ms": {"linear_forward_packed": dev_lin, "encode": dev_enc, "xnor_gemm": dev_gemm,
+                        "timer": "graph of 20 back-to-back C-ABI calls, per call (host call overhead excluded)"},
+          "xnor_gemm_device_tops": bops / (dev_gemm * 1e-3) / 1e12 if dev_gemm else None}
     if ref is not None:
         xh = x.cpu().numpy()
         ph = pw.cpu().numpy().view(np.uint32)
@@ -361,7 +397,8 @@ def measure_configs(lib, dev, st, flush, seed, peaks, cpu, world, rank):
           "sharding": "replicas (one image per request)" if world > 1 else "single GPU",
           "requests_per_s": world / (ms * 1e-3),
           "binary_tops": world * 2.0 * 64 * 576 * 1024 / (ms * 1e-3) / 1e12,
-          "gemm_kernel": lib.bnn_last_gemm_kernel().decode(), "note": "75.5 M bops per request: latency bound"}
+          "gemm_kernel": lib.bnn_last_gemm_kernel().decode(), "note": "75.5 M bops per request: latency bound",
+          "device_ms": _graph_time(f_conv, st, flush)}
     if ref is not None:
         xh, ph, bh = xc.cpu().numpy(), pwc.cpu().numpy().view(np.uint32), bc.cpu().numpy()
         geo = [3, 3, 1, 1, 1, 1, 64, 64]

@@ -87,6 +87,8 @@ int launch_pack_rows(const float*, size_t, size_t, uint32_t*, size_t, unsigned l
                      cudaStream_t);
 int launch_im2col_sign_pack(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*,
                             uint32_t*, size_t, cudaStream_t);
+int conv_rowbits_fused(const float*, size_t, size_t, size_t, size_t, const uint32_t*, size_t, const float*,
+                       const bnn_conv_geom*, float*, cudaStream_t, int*);
 
 int xnor4_gemm_s32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, int32_t*, size_t,
                    cudaStream_t);
@@ -135,6 +137,12 @@ int conv_forward(const float* x, size_t B, size_t C, size_t H, size_t W, const u
                                      " channels, geometry expects " + std::to_string(g->in_channels));
     const size_t K = g->kernel_h * g->kernel_w * C, wpl = wpl_of(K);
     const size_t lines = B * oh * ow;
+    if (!use_umma(g->out_channels, lines, K)) {
+        // small layers: im2col and the xnor-popcount GEMM in one launch (no scratch)
+        int handled = 0;
+        BNN_TRY(conv_rowbits_fused(x, B, C, H, W, pw, ldw, bias, g, out, s, &handled));
+        if (handled) return BNN_OK;
+    }
     Scratch col;
     BNN_TRY(col.alloc(lines * wpl * sizeof(uint32_t), s));
     BNN_TRY(launch_im2col_sign_pack(x, B, C, H, W, g, col.as<uint32_t>(), wpl, s));

@@ -215,10 +215,17 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
             const int mt = u % g.m_tiles, nt = u / g.m_tiles;
             const int am = mt * 128 + t, bn = nt * g.NB + t;
             const bool has_a = t < 128, has_b = t < g.NB;
+            uint32_t naw[8], nam[8], nbw[8], nbm[8];  // the next block's words, loaded ahead
+            load_block(g.w, g.ldw, am, has_a && am < g.M, 0, g.Lw, g.L, naw, nam);
+            load_block(g.x, g.ldx, bn, has_b && bn < g.N, 0, g.Lw, g.L, nbw, nbm);
             for (int kb = 0; kb < g.KB; ++kb) {
                 uint32_t aw[8], am8[8], bw[8], bm8[8];
-                load_block(g.w, g.ldw, am, has_a && am < g.M, kb, g.Lw, g.L, aw, am8);
-                load_block(g.x, g.ldx, bn, has_b && bn < g.N, kb, g.Lw, g.L, bw, bm8);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) aw[k] = naw[k], am8[k] = nam[k], bw[k] = nbw[k], bm8[k] = nbm[k];
+                if (kb + 1 < g.KB) {
+                    load_block(g.w, g.ldw, am, has_a && am < g.M, kb + 1, g.Lw, g.L, naw, nam);
+                    load_block(g.x, g.ldx, bn, has_b && bn < g.N, kb + 1, g.Lw, g.L, nbw, nbm);
+                }
                 mbar_wait(&empty[stage], phase ^ 1);
                 const uint32_t ta = smem_u32(sA + size_t(stage) * 16384);
                 const uint32_t tbb = smem_u32(sB + size_t(stage) * g.NB * 128);
@@ -254,9 +261,13 @@ int launch_xnor4(G4 g, cudaStream_t s) {
     // image columns per tile: the widest NB (<= 256, multiple of 16) that still gives every SM a
     // tile, and never wider than N needs
     const int sms = num_sms();
-    int nb = 256;
+    // the widest NB whose tiles still fit one wave, unless even NB = 16 needs more (then the
+    // widest NB: fewest rounds)
     const int n16 = (g.N + 15) / 16 * 16;
-    while (nb > 16 && (long(g.m_tiles) * ((g.N + nb - 1) / nb) < sms || nb / 2 >= n16)) nb /= 2;
+    int nb = 256;
+    while (nb > 16 && nb / 2 >= n16) nb /= 2;  // never wider than the batch needs
+    auto tiles_of = [&](int b) { return long(g.m_tiles) * ((g.N + b - 1) / b); };
+    while (nb > 16 && tiles_of(nb) * 2 <= sms) nb /= 2;  // narrower while it still fits one wave
     g.NB = std::min(nb, n16);
     g.n_tiles = (g.N + g.NB - 1) / g.NB;
     g.nst = int(std::min<size_t>(kGMaxStages, (kGSmemMax - 1024 - 256) / (16384 + size_t(g.NB) * 128)));

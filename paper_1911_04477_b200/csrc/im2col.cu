@@ -80,10 +80,11 @@ __global__ void __launch_bounds__(256)
 //     1 bits of a 64-bit window). With stride 1 the 32 positions' words are one 32 x 32 bit
 //     transpose across the warp (five shuffle-xor butterfly rounds), else one ballot each.
 //  3. The group's [R*ow lines x wpl words] output is staged in smem and stored line-contiguous.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
     im2col_rowbits_kernel(const float* __restrict__ x, int C, int H, int W, int kH, int kW, int sH, int sW,
                           int pH, int pW, int oh, int ow, int K, int wpl, int R, uint32_t* __restrict__ words,
-                          size_t ld) {
+                          size_t ld, const uint32_t* __restrict__ cw, size_t ldw, int D, const float* __restrict__ bias,
+                          float* __restrict__ y) {
     extern __shared__ uint32_t sm[];
     const int oy0 = blockIdx.x * R, img = blockIdx.y;
     const int ry = min(R, oh - oy0);                  // output rows of this group
@@ -98,20 +99,31 @@ __global__ void __launch_bounds__(256)
     // 0.0 everywhere -> all +1; bits >= W are don't-care: the window below masks them to 1)
     const int total = C * nrow;
     if ((W & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        // kU float4 loads in flight per lane (kU * 4 rows per warp per round): one memory round
+        // trip per round instead of one per 4 rows
+        constexpr int kU = 4;
         const int sub = lane >> 3, col = 4 * (lane & 7);
-        for (int t0 = warp * 4; t0 < total; t0 += nwarps * 4) {
-            const int t = t0 + sub;
-            const int c = t / nrow, lr = t - c * nrow, iy = iyb + lr;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (t < total && unsigned(iy) < unsigned(H) && col < W)
-                v = __ldg(reinterpret_cast<const float4*>(xb + (size_t(c) * H + iy) * W + col));
-            uint32_t b = (uint32_t(v.x >= 0.0f) | (uint32_t(v.y >= 0.0f) << 1) | (uint32_t(v.z >= 0.0f) << 2) |
-                          (uint32_t(v.w >= 0.0f) << 3))
-                         << col;
-            b |= __shfl_xor_sync(0xffffffffu, b, 1);
-            b |= __shfl_xor_sync(0xffffffffu, b, 2);
-            b |= __shfl_xor_sync(0xffffffffu, b, 4);
-            if ((lane & 7) == 0 && t < total) rows[t] = b;
+        for (int t0 = warp * 4 * kU; t0 < total; t0 += nwarps * 4 * kU) {
+            float4 v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int t = t0 + 4 * u + sub;
+                const int c = t / nrow, lr = t - c * nrow, iy = iyb + lr;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (t < total && unsigned(iy) < unsigned(H) && col < W)
+                    v[u] = __ldg(reinterpret_cast<const float4*>(xb + (size_t(c) * H + iy) * W + col));
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int t = t0 + 4 * u + sub;
+                uint32_t b = (uint32_t(v[u].x >= 0.0f) | (uint32_t(v[u].y >= 0.0f) << 1) |
+                              (uint32_t(v[u].z >= 0.0f) << 2) | (uint32_t(v[u].w >= 0.0f) << 3))
+                             << col;
+                b |= __shfl_xor_sync(0xffffffffu, b, 1);
+                b |= __shfl_xor_sync(0xffffffffu, b, 2);
+                b |= __shfl_xor_sync(0xffffffffu, b, 4);
+                if ((lane & 7) == 0 && t < total) rows[t] = b;
+            }
         }
     } else {
         for (int t = warp; t < total; t += nwarps) {
@@ -125,39 +137,65 @@ __global__ void __launch_bounds__(256)
     // 2. word q of every position of every row of the group: lane = patch row r
     const int kk = kH * kW;
     const uint64_t pad = ~(((1ull << W) - 1ull) << 16);  // row at bits [16, 16 + W), the rest 1
-    for (int yq = warp; yq < ry * wpl; yq += nwarps) {
-        const int yy = yq / wpl, q = yq - yy * wpl;
+    // word q outer (the lane's patch row decode once), the group's rows inner
+    for (int q = warp; q < wpl; q += nwarps) {
         const int r = q * 32 + lane;
         const bool rv = r < K;  // bits past K are 0
         const int c = r / kk, t = r - c * kk, kh = t / kW, kw = t - kh * kW;
-        const uint64_t win = rv ? ((uint64_t(rows[c * nrow + yy * sH + kh]) << 16) | pad) : 0ull;
         const int sh0 = 16 - pW + kw;  // window bit of position ox: sh0 + ox * sW
-        for (int ox0 = 0; ox0 < ow; ox0 += 32) {
-            uint32_t mine = 0;
-            if (sW == 1) {
-                // lane r holds its bits for 32 consecutive positions; a 32 x 32 bit transpose
-                // across the warp (5 shuffle-xor butterfly rounds) gives lane ox its word
-                uint32_t v = uint32_t(win >> (sh0 + ox0));
+        const uint32_t* rowp = rows + c * nrow + kh;
+        for (int yy = 0; yy < ry; ++yy) {
+            const uint64_t win = rv ? ((uint64_t(rowp[yy * sH]) << 16) | pad) : 0ull;
+            for (int ox0 = 0; ox0 < ow; ox0 += 32) {
+                uint32_t mine = 0;
+                if (sW == 1) {
+                    // lane r holds its bits for 32 consecutive positions; a 32 x 32 bit transpose
+                    // across the warp (5 shuffle-xor butterfly rounds) gives lane ox its word
+                    uint32_t v = uint32_t(win >> (sh0 + ox0));
 #pragma unroll
-                for (int j = 16; j >= 1; j >>= 1) {
-                    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                                     : j == 2 ? 0x33333333u : 0x55555555u;
-                    const uint32_t p = __shfl_xor_sync(0xffffffffu, v, j);
-                    v = (lane & j) ? ((v & ~m) | ((p >> j) & m)) : ((v & m) | ((p & m) << j));
-                }
-                mine = v;
-            } else {
+                    for (int j = 16; j >= 1; j >>= 1) {
+                        const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                         : j == 2 ? 0x33333333u : 0x55555555u;
+                        const uint32_t p = __shfl_xor_sync(0xffffffffu, v, j);
+                        v = (lane & j) ? ((v & ~m) | ((p >> j) & m)) : ((v & m) | ((p & m) << j));
+                    }
+                    mine = v;
+                } else {
 #pragma unroll 8
-                for (int j = 0; j < 32; ++j) {
-                    const int ox = ox0 + j;
-                    const uint32_t wbits = __ballot_sync(0xffffffffu, (win >> (sh0 + ox * sW)) & 1ull);
-                    if (lane == j) mine = wbits;
+                    for (int j = 0; j < 32; ++j) {
+                        const int ox = ox0 + j;
+                        const uint32_t wbits = __ballot_sync(0xffffffffu, (win >> (sh0 + ox * sW)) & 1ull);
+                        if (lane == j) mine = wbits;
+                    }
                 }
+                if (ox0 + lane < ow) tile[(yy * ow + ox0 + lane) * wpl + q] = mine;
             }
-            if (ox0 + lane < ow) tile[(yy * ow + ox0 + lane) * wpl + q] = mine;
         }
     }
     __syncthreads();
+    if (y) {
+        // Fused conv_forward_binary (network.cpp:65-79) for small layers: the xnor-popcount GEMM
+        // of the group's patch words against the D packed weight rows (CUDA cores), then
+        // to_float + bias_add (kernels.cpp:90-107) into the NCHW output (reshape_output,
+        // lowering.cpp:87-95). a = L - 2 * sum popc(w ^ x) (pad bits are 0 in both operands).
+        uint32_t* wsm = tile + ry * ow * wpl;  // [D][wpl]
+        for (int t = threadIdx.x; t < D * wpl; t += blockDim.x) {
+            const int d = t / wpl, q = t - d * wpl;
+            wsm[t] = __ldg(cw + size_t(d) * ldw + q);
+        }
+        __syncthreads();
+        const int nl = ry * ow;
+        for (int t = threadIdx.x; t < D * nl; t += blockDim.x) {
+            const int d = t / nl, l = t - d * nl;
+            const uint32_t* xr = tile + l * wpl;
+            const uint32_t* wr = wsm + d * wpl;
+            int pc = 0;
+            for (int q = 0; q < wpl; ++q) pc += __popc(xr[q] ^ wr[q]);
+            y[(size_t(img) * D + d) * oh * ow + size_t(oy0) * ow + l] =
+                __fadd_rn(__int2float_rn(K - 2 * pc), bias ? __ldg(bias + d) : 0.0f);
+        }
+        return;
+    }
     // 3. store the [ry*ow x wpl] tile: lines img*oh*ow + oy0*ow + (yy*ow + ox)
     const int tot = ry * ow * wpl;
     uint32_t* dst = words + (size_t(img) * oh * ow + size_t(oy0) * ow) * ld;
@@ -196,10 +234,10 @@ int launch_im2col_sign_pack(const float* x, size_t B, size_t C, size_t H, size_t
         while (R < 16 && R * 2 <= oh && smem_of(R * 2) <= 48 * 1024 &&
                B * ceil_div(oh, R * 2) >= 2 * size_t(num_sms()))
             R *= 2;
-        if (smem_of(R) <= 48 * 1024 && B * ceil_div(oh, R) >= size_t(num_sms())) {
+        if (smem_of(R) <= 48 * 1024) {
             im2col_rowbits_kernel<<<dim3(unsigned(ceil_div(oh, R)), unsigned(B)), 256, smem_of(R), s>>>(
                 x, int(C), int(H), int(W), int(kH), int(kW), int(sH), int(g->stride_w), int(g->pad_h), int(pW),
-                int(oh), int(ow), int(K), int(wpl), int(R), words, ld);
+                int(oh), int(ow), int(K), int(wpl), int(R), words, ld, nullptr, 0, 0, nullptr, nullptr);
             return launch_check("im2col_rowbits_kernel");
         }
     }
@@ -209,6 +247,28 @@ int launch_im2col_sign_pack(const float* x, size_t B, size_t C, size_t H, size_t
         int(g->stride_w), int(g->pad_h), int(g->pad_w), int(oh), int(ow), lines, int(K), int(wpl),
         words, ld);
     return launch_check("im2col_sign_pack_kernel");
+}
+
+// conv_forward_binary in ONE launch for small layers (the row-bits im2col + a CUDA-core xnor
+// GEMM per block, weights in shared memory): returns 1 when it handled the call, 0 when the
+// shape needs the im2col + GEMM path.
+int conv_rowbits_fused(const float* x, size_t B, size_t C, size_t H, size_t W, const uint32_t* pw, size_t ldw,
+                       const float* bias, const bnn_conv_geom* g, float* out, cudaStream_t s, int* handled) {
+    *handled = 0;
+    size_t oh, ow;
+    BNN_TRY(bnn_output_dims(g, H, W, &oh, &ow));
+    const size_t K = g->kernel_h * g->kernel_w * C, wpl = wpl_of(K), D = g->out_channels;
+    const size_t kW = g->kernel_w, pW = g->pad_w, kH = g->kernel_h, sH = g->stride_h;
+    if (!(W <= 32 && pW <= 16 && oh < 65536 && B < 65536 && (ow - 1) * g->stride_w + kW <= 48 + pW)) return BNN_OK;
+    const size_t smem = (C * kH + ow * wpl + D * wpl) * sizeof(uint32_t);  // one output row per block
+    if (smem > 48 * 1024 || D * ow * wpl > 4096 * 36) return BNN_OK;
+    im2col_rowbits_kernel<<<dim3(unsigned(oh), unsigned(B)), 256, smem, s>>>(
+        x, int(C), int(H), int(W), int(kH), int(kW), int(sH), int(g->stride_w), int(g->pad_h), int(pW), int(oh),
+        int(ow), int(K), int(wpl), 1, nullptr, 0, pw, ldw, int(D), bias, out);
+    BNN_TRY(launch_check("im2col_rowbits_kernel (fused conv)"));
+    set_last_gemm("conv_rowbits_popc");
+    *handled = 1;
+    return BNN_OK;
 }
 
 }  // namespace bnnk

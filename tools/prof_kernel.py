@@ -1,6 +1,6 @@
-"""Run one K1/K2 launch at the bench shapes (for ncu captures).
+"""Run one K1/K2/K3 launch at the bench shapes (for ncu captures).
 
-    python tools/prof_kernel.py im2col|pack_cols|pack_rows
+    python tools/prof_kernel.py im2col|pack_cols|pack_rows|gemm_popc|gemm_xnor4|conv_b1
 """
 import ctypes as C
 import os
@@ -22,6 +22,24 @@ if what == "im2col":
     out = torch.empty((256 * 1024, 36), dtype=torch.int32, device="cuda")
     for _ in range(2):
         _lib.check(lib.bnn_im2col_sign_pack_f32(x.data_ptr(), 256, 128, 32, 32, C.byref(g), out.data_ptr(), 36, S))
+elif what.startswith("gemm"):
+    M = N = L = 1024
+    w = torch.randint(-2**31, 2**31 - 1, (M, L // 32), dtype=torch.int32, device="cuda")
+    x = torch.randint(-2**31, 2**31 - 1, (N, L // 32), dtype=torch.int32, device="cuda")
+    out = torch.empty((M, N), dtype=torch.int32, device="cuda")
+    lib.bnn_set_gemm_policy(1 if what == "gemm_popc" else 2)
+    for _ in range(2):
+        _lib.check(lib.bnn_xnor_gemm_s32(w.data_ptr(), L // 32, x.data_ptr(), L // 32, M, N, L, out.data_ptr(), N, S))
+elif what == "conv_b1":
+    g = _lib.ConvGeom(3, 3, 1, 1, 1, 1, 64, 64)
+    x = torch.empty((1, 64, 32, 32), dtype=torch.float32, device="cuda")
+    _lib.check(lib.bnn_fill_random_f32(7, 0, x.numel(), x.data_ptr(), S))
+    w = torch.randint(-2**31, 2**31 - 1, (64, 18), dtype=torch.int32, device="cuda")
+    b = torch.zeros(64, dtype=torch.float32, device="cuda")
+    y = torch.empty((1, 64, 32, 32), dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        _lib.check(lib.bnn_conv_forward_binary_f32(x.data_ptr(), 1, 64, 32, 32, w.data_ptr(), 18, b.data_ptr(),
+                                                   C.byref(g), y.data_ptr(), S))
 else:
     L = N = 16384
     x = torch.empty((L, N), dtype=torch.float32, device="cuda")
