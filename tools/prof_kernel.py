@@ -1,6 +1,6 @@
 """Run one K1/K2/K3 launch at the bench shapes (for ncu captures).
 
-    python tools/prof_kernel.py im2col|pack_cols|pack_rows|gemm_popc|gemm_xnor4|conv_b1
+    python tools/prof_kernel.py im2col|pack_cols|pack_rows|gemm_popc|gemm_xnor4|conv_b1|probes
 """
 import ctypes as C
 import os
@@ -30,6 +30,13 @@ elif what.startswith("gemm"):
     lib.bnn_set_gemm_policy(1 if what == "gemm_popc" else 2)
     for _ in range(2):
         _lib.check(lib.bnn_xnor_gemm_s32(w.data_ptr(), L // 32, x.data_ptr(), L // 32, M, N, L, out.data_ptr(), N, S))
+elif what == "probes":
+    # the K3 pipe candidates: LOP3+POPC loop, emulated b1 mma.sync, tcgen05 i8 / mxf4
+    a, b = C.c_double(), C.c_double()
+    _lib.check(lib.bnn_probe_popc_peak(C.byref(a), C.byref(b), S))
+    _lib.check(lib.bnn_probe_bmma_peak(C.byref(a), C.byref(b), S))
+    _lib.check(lib.bnn_probe_umma_peak(0, 256, C.byref(a), C.byref(b), S))
+    _lib.check(lib.bnn_probe_umma_peak(1, 256, C.byref(a), C.byref(b), S))
 elif what == "conv_b1":
     g = _lib.ConvGeom(3, 3, 1, 1, 1, 1, 64, 64)
     x = torch.empty((1, 64, 32, 32), dtype=torch.float32, device="cuda")
