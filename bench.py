@@ -505,8 +505,11 @@ def measure_configs(lib, dev, st, flush, seed, peaks, cpu, world, rank):
     out["k3_pipes_tbops"] = {"popc_lop3": popc, "b1_mma_sync_emulated": bmma,
                              "tcgen05_i8": peaks.get("probe", {}).get("tcgen05_i8_tops"),
                              "tcgen05_mxf4": peaks.get("probe", {}).get("tcgen05_mxf4_tops"),
-                             "chosen": "tcgen05: kind::mxf4 for the packed-input convs, kind::i8 for the "
-                                       "linear layers and the large standalone xnor_gemm"}
+                             "chosen": "tcgen05 kind::mxf4 (e2m1 operands, exact) for the packed-input convs "
+                                       "(halo4 / swap4), the linear layers (lin4) and the standalone xnor_gemm "
+                                       "above 2^26 bit-MACs (xnor4); LOP3+POPC below it and for the pixel-input "
+                                       "first conv and the logits",
+                             "ncu_pipe_counters": "profiles/r02_k3_pipes_ncu.json"}
     return out
 
 

@@ -460,13 +460,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     uint32_t v[32];
                     tmem_ld32(tb + uint32_t(32 * cc), v);
                     tmem_ld_wait();
-                    uint32_t mk[4] = {0u, 0u, 0u, 0u};  // four independent select chains
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t w = __ballot_sync(0xffffffffu, (__uint_as_float(v[j]) >= Tf) != flip);
-                        if (lane == j) mk[j & 3] = w;
-                    }
-                    const uint32_t mine = (mk[0] | mk[1]) | (mk[2] | mk[3]);
+                    const uint32_t mine = decisions_transposed(v, Tf, flip, lane);
                     const int col = 32 * cc + lane;
                     if (col < ncol && wvalid) {
                         const int ir = g.dP.div(col), x = col - ir * g.P;

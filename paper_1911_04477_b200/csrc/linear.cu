@@ -222,13 +222,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                             if (bc + j < g.B && bc + j < b0 + g.NB) dst[size_t(j) * g.Dpad] = int(__uint_as_float(v[j]));
                     }
                 } else if (g.epi == FEPI_BITS) {
-                    uint32_t mk[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const uint32_t w = __ballot_sync(0xffffffffu, (__uint_as_float(v[j]) >= Tf) != flip);
-                        if (lane == j) mk[j & 3] = w;
-                    }
-                    const uint32_t mine = (mk[0] | mk[1]) | (mk[2] | mk[3]);
+                    const uint32_t mine = decisions_transposed(v, Tf, flip, lane);
                     if (d0 < g.D && bc + lane < g.B && lane < g.NB - 32 * c)
                         g.out_bits[size_t(bc + lane) * g.Dw + (d0 >> 5)] = mine;
                 } else {

@@ -206,6 +206,27 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | (uint32_t(M >> 4) << 24);     // m_dim
 }
 
+// ------------------------------------------------------- epilogue: 32 x 32 decision transpose
+// Lane c holds 32 accumulator columns of output channel c (a tcgen05.ld 32x32b.x32). Returns
+// lane j's packed word for column j: bit c = (acc[c][j] >= T_c) ^ flip_c. Each lane builds its
+// 32 decision bits (compare + select per column), then a 32 x 32 bit transpose across the warp
+// in five shuffle-xor butterfly rounds: ~95 instructions per 32 columns instead of 32 ballots
+// (~130 instructions and a VOTE dependency chain per ballot).
+__device__ __forceinline__ uint32_t decisions_transposed(const uint32_t (&v)[32], float T, bool flip, int lane) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m |= uint32_t(__uint_as_float(v[j]) >= T) << j;
+    if (flip) m = ~m;
+#pragma unroll
+    for (int j = 16; j >= 1; j >>= 1) {
+        const uint32_t k = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
+                                                                                                   : 0x55555555u;
+        const uint32_t p = __shfl_xor_sync(0xffffffffu, m, j);
+        m = (lane & j) ? ((m & ~k) | ((p >> j) & k)) : ((m & k) | ((p & k) << j));
+    }
+    return m;
+}
+
 // ---------------------------------------------------- warp-issued forms (one elected lane)
 // Called by the whole converged warp with warp-uniform operands: the descriptors stay in uniform
 // registers and one lane (elect.sync) issues. From inside `if (lane == 0)` every MMA went
