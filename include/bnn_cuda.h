@@ -316,6 +316,11 @@ int bnn_set_fused_fp4(int mode);
  * (default) on, 2 also for convs whose weights do not fit (streamed through a ring of shared-
  * memory slots; slower than fused_swap4_kernel for VGG-small). Bit-exact in every mode. */
 int bnn_set_fused_halo(int enabled);
+/* Fused engine: the pixel-input first conv ("same" geometry, C <= 32) on the halo-tile FP4 kernel
+ * with the float input signed by its producers and the channels padded to 64 (zero weights): 1
+ * on, 0 (default: measured faster) the CUDA-core pix_tile / pix_popc kernels. Bit-exact either
+ * way. */
+int bnn_set_fused_halo0(int enabled);
 /* Fused engine: linear layers on the FP4 tensor-core kernel (lin4_kernel: e2m1 weights by TMA,
  * packed input bits expanded in shared memory, K split over CTAs with an exact integer
  * reduction in lin_finish_kernel) instead of the int8 fused_layer_kernel. 0 off, 1 (default)

@@ -121,6 +121,7 @@ _SIGS = {
     "bnn_set_fused_pix_popc": (_I, [_I]),
     "bnn_set_fused_fp4": (_I, [_I]),
     "bnn_set_fused_halo": (_I, [_I]),
+    "bnn_set_fused_halo0": (_I, [_I]),
     "bnn_set_fused_lin4": (_I, [_I]),
     "bnn_set_fused_fp4_pair": (_I, [_I]),
     "bnn_float_gemm_f32": (_I, [_P, _SZ, _SZ, _P, _SZ, _P, _SZ, _P, _P]),

@@ -75,12 +75,19 @@ struct HaloGeom {
     int wst;             // 0: weights resident in shared memory; else ring slots of streamed blocks
     size_t smem;
     FastDiv dP, dS, dQ, dWh, dG;
+    const float* in_f32;      // first layer (halo0): float NCHW input, creal channels -> bit words
+    int creal;
     unsigned long long* dbg;  // BNN_HALO_PROFILE counters, else null
     int dbg_mode;             // profiling experiments (results invalid): 1 no epilogue, 2 no halo fill, 4 no MMA
     int taps, cpt;            // taps (<= 9), K64 steps per tap (C / 64)
     int toff[9];              // canvas shift of tap t, in pixels (= 16-byte halo rows)
 };
 bool halo4_plan(const FusedGeom& g, HaloGeom& h);
+// First conv through halo4 (halo0): the float input signed per pixel by the producers, C <= 32
+// channels padded to 64 per tap (zero weights). prep_w4_pix builds its e2m1 weights from the
+// reference's packed rows: [Dpad, Kpad4/2], K' = KH*KW*64 tap-major.
+int prep_w4_pix(const uint32_t* packed, size_t wpl, int D, int C, int KH, int KW, int Dpad, int Kpad4, uint8_t* w4,
+                cudaStream_t s);
 int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s);
 
 // FP4 linear layer with split-K (linear.cu): weights [Dpad, Kpad4/2] e2m1 via tm4, input bits

@@ -514,6 +514,54 @@ __global__ void __launch_bounds__(kHThreads, 1)
             const uint32_t hb = sH + uint32_t(hs) * hbytes;
             const int q0 = nt * g.TR * g.P;
             const int nh = (g.dbg_mode & 2) ? 0 : g.NH;
+            if (g.in_f32) {
+                // first layer: sign bits of the pixel's creal float channels -> word 0; channels
+                // 32..63 (zero weights) word 1; frame pixels all ones (sign(0.0) = +1)
+                // two pixels per thread per pass, all their channel loads issued before use
+                // (consecutive threads read consecutive pixels of a row: coalesced per channel)
+                for (int j0 = pt; j0 < nh; j0 += 2 * kHProdThreads) {
+                    long long pix[2];
+                    const float* src[2];
+                    const long long hw = (long long)g.H * g.W;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int j = j0 + u * kHProdThreads;
+                        pix[u] = j < nh ? halo_src(g, q0 + j) : -1;
+                        const long long pp = pix[u] < 0 ? 0 : pix[u];
+                        const long long b = pp / hw;
+                        src[u] = g.in_f32 + (b * g.creal) * hw + (pp - b * hw);
+                    }
+                    uint32_t w0[2] = {0u, 0u};
+                    int c = 0;
+                    for (; c + 4 <= g.creal; c += 4) {
+                        float v[2][4];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) v[u][k] = pix[u] >= 0 ? __ldg(src[u] + (c + k) * hw) : 0.0f;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) w0[u] |= uint32_t(v[u][k] >= 0.0f) << (c + k);
+                    }
+                    for (; c < g.creal; ++c) {
+                        float v[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) v[u] = pix[u] >= 0 ? __ldg(src[u] + c * hw) : 0.0f;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) w0[u] |= uint32_t(v[u] >= 0.0f) << c;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int j = j0 + u * kHProdThreads;
+                        if (j >= nh) break;
+                        const uint32_t dst = hb + uint32_t(j) * 16u;
+                        // frame pixels all ones (sign(0.0) = +1); channels 32..63 carry zero weights
+                        st_expand4(dst, pix[u] < 0 ? ~0u : w0[u]);
+                        st_expand4(dst + lbo, pix[u] < 0 ? ~0u : 0u);
+                    }
+                }
+            } else
             for (int j = pt; j < nh; j += 2 * kHProdThreads) {
                 if ((g.Cw & 3) == 0)
                     fill_rows<4>(g, hb, lbo, q0, j, nh);
@@ -628,7 +676,44 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
     h.dG = FastDiv::make(uint32_t(h.G));
     h.dbg = nullptr;
     h.dbg_mode = 0;
+    h.in_f32 = nullptr;
+    h.creal = 0;
     return true;
+}
+
+namespace {
+
+// First-layer e2m1 weights for halo0: K' = T*64 positions, tap-major / channel-minor with the
+// channels padded to 64 (zero weights past C); element e of a 32-group holds position
+// 4 (e % 8) + e / 8 (put_word4's order); reference row bit r = (c*KH + kh)*KW + kw.
+__global__ void prep_w4_pix_kernel(const uint32_t* __restrict__ packed, size_t wpl, int D, int C, int KH, int KW,
+                                   int Dpad, int Kpad4, uint8_t* __restrict__ w4) {
+    const size_t total = size_t(Dpad) * (Kpad4 / 2);
+    const int T = KH * KW;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const int d = int(i / (Kpad4 / 2)), e0 = int(i % (Kpad4 / 2)) * 2;
+        uint8_t v = 0;
+        for (int hh = 0; hh < 2; ++hh) {
+            const int e = e0 + hh, q = e >> 5, el = e & 31;
+            const int k = 32 * q + 4 * (el % 8) + el / 8;
+            const int tap = k >> 6, c = k & 63;
+            if (d >= D || tap >= T || c >= C) continue;
+            const int kh = tap / KW, kw = tap - kh * KW, r = (c * KH + kh) * KW + kw;
+            const uint32_t bit = (packed[size_t(d) * wpl + (r >> 5)] >> (r & 31)) & 1u;
+            v |= uint8_t((bit ? 0x2 : 0xA) << (4 * hh));
+        }
+        w4[i] = v;
+    }
+}
+
+}  // namespace
+
+int prep_w4_pix(const uint32_t* packed, size_t wpl, int D, int C, int KH, int KW, int Dpad, int Kpad4, uint8_t* w4,
+                cudaStream_t s) {
+    const size_t total = size_t(Dpad) * (Kpad4 / 2);
+    prep_w4_pix_kernel<<<unsigned(std::min<size_t>(ceil_div(total, 256), size_t(num_sms()) * 8)), 256, 0, s>>>(
+        packed, wpl, D, C, KH, KW, Dpad, Kpad4, w4);
+    return launch_check("prep_w4_pix_kernel");
 }
 
 int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {

@@ -99,6 +99,9 @@ struct FusedStage {
     bool pre_encode = false;     // first layer is linear: K1 sign-packs each image's features first
     bool small_logits = false;   // tiny final layer: CUDA-core popcount kernel (wbits)
     bool pix_popc = false;       // pixel-input first conv with K <= 32: CUDA-core kernel
+    bool halo0 = false;          // pixel-input first conv through halo4 (float input, C padded to 64)
+    DevBuf w4h;                  // its e2m1 weights [Dpad, K'/2], K' = KH*KW*64
+    CUtensorMap tm4h;
     PixParams pix{};             // its per-channel weight words, thresholds and flips
     const char* kname = "";      // kernel the last forward ran for this stage
     DevBuf w8, prm, wbits;
@@ -398,6 +401,16 @@ int plan_fused(bnn_net* net, cudaStream_t s) {
             st->small_logits = true;
             BNN_TRY(st->wbits.alloc(size_t(g.D) * g.Cw * sizeof(uint32_t)));
             BNN_TRY(prep_logit_bits(st->w8.as<int8_t>(), st->Kpad, g.K, g.D, g.Cw, st->wbits.as<uint32_t>(), s));
+        }
+        if (st->in_mode == FIN_PIX && st->epi == FEPI_BITS && g.C <= 32 && g.SH == 1 && g.SW == 1 &&
+            g.KH == 2 * g.PH + 1 && g.KW == 2 * g.PW + 1 && g.PH <= 1 && g.PW <= 1 && g.OH == g.H && g.OW == g.W &&
+            g.D % 32 == 0) {  // halo0: the first conv on the FP4 tensor cores, channels padded to 64
+            const int Kp4 = int(round_up(size_t(g.KH * g.KW * 64), 256));
+            BNN_TRY(st->w4h.alloc(size_t(st->Dpad) * (Kp4 / 2)));
+            BNN_TRY(prep_w4_pix(L.packed.as<uint32_t>(), L.wpl, g.D, g.C, g.KH, g.KW, st->Dpad, Kp4,
+                                st->w4h.as<uint8_t>(), s));
+            BNN_TRY(make_tmap_2d_s8(&st->tm4h, st->w4h.p, size_t(st->Dpad), size_t(Kp4 / 2), size_t(Kp4 / 2), 128));
+            st->halo0 = true;
         }
         if (st->in_mode == FIN_PIX && st->epi == FEPI_BITS && pix_popc_ok(g)) {
             st->pix_popc = true;
@@ -724,6 +737,25 @@ bool use_lin4(const bnn_net* net, const FusedStage& st) {
            net->layers[st.layer]->spec.kind == BNN_LAYER_LINEAR && st.in_mode == FIN_BITS;
 }
 
+// First conv through halo4 (halo0): BNN_FUSED_HALO0 / bnn_set_fused_halo0: 1 on, 0 (default) the
+// CUDA-core pix_tile / pix_popc kernels (or the int8 tensor-core path). Measured slower for
+// VGG-small's conv 3 -> 128 (41 vs 24 us per layer at batch 256): with K = 9 x 64 a tile is only 9
+// MMAs, so its epilogue (128 channels x 240 positions) bounds the kernel.
+int g_halo0 = -1;
+
+// The halo0 plan for a pixel-input stage: the first conv seen as a 64-channel conv (2 packed
+// words per pixel, K' = taps * 64) whose producers sign the float input themselves.
+bool halo0_plan(const FusedStage& st, const FusedGeom& g, const float* x, HaloGeom& hg) {
+    FusedGeom g0 = g;
+    g0.C = 64, g0.Cw = 2, g0.K = g.KH * g.KW * 64;
+    g0.kb4 = (g0.K + 255) / 256;
+    g0.kq4 = (g0.K - 256 * (g0.kb4 - 1) + 63) / 64;
+    if (!halo4_plan(g0, hg) || hg.wst) return false;
+    hg.in_f32 = x;
+    hg.creal = g.C;
+    return true;
+}
+
 int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStream_t s) {
     if (net->bits_batch < B) {
         const size_t bytes = std::max<size_t>(net->bits_words_per_image, 1) * B * 4;
@@ -822,8 +854,11 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         // pix_tile_kernel stages packed input rows in shared memory when the layer allows);
         // 2: after pack_pixels; 3 (default): 1 up to batch 512 (B=256: 1.754 vs 1.731 M img/s),
         // 2 above (B=4096: 2.70 vs 2.66 M, the packer's one pass beats the per-tile halo rows)
+        if (g_halo0 < 0) g_halo0 = getenv("BNN_FUSED_HALO0") ? atoi(getenv("BNN_FUSED_HALO0")) : 0;
+        HaloGeom hg0;
+        const bool use_h0 = st.halo0 && g_halo0 && g_halo != 0 && halo0_plan(st, g, x, hg0);
         const bool pix_f32 = st.pix_popc && (g_pix_popc == 1 || (g_pix_popc == 3 && B <= 512));
-        if (st.in_mode == FIN_PIX && !pix_f32) {  // first-layer sign bits, one word per pixel
+        if (st.in_mode == FIN_PIX && !pix_f32 && !use_h0) {  // first-layer sign bits, one word per pixel
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
             ++launches;
         }
@@ -834,6 +869,10 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         EventPair gemm_ev(net, st.layer, 1, s);
         if (st.small_logits && g_small_logits) {
             BNN_TRY(launch_logits_popc(g, st.wbits.as<uint32_t>(), s));
+        } else if (use_h0) {
+            HaloGeom h = hg0;
+            h.out = g.out_bits;
+            BNN_TRY(launch_halo4(st.tm4h, h, s));
         } else if (st.pix_popc && g_pix_popc) {
             FusedGeom gp = g;
             if (pix_f32) gp.in = x;
@@ -1072,6 +1111,13 @@ int bnn_set_fused_fp4(int mode) {
 int bnn_set_fused_lin4(int enabled) {
     if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused lin4: 0 (off) or 1 (on)");
     g_lin4 = enabled;
+    ++g_tiling_epoch;  // captured graphs hold the other kernels
+    return BNN_OK;
+}
+
+int bnn_set_fused_halo0(int enabled) {
+    if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused halo0: 0 (off) or 1 (on)");
+    g_halo0 = enabled;
     ++g_tiling_epoch;  // captured graphs hold the other kernels
     return BNN_OK;
 }

@@ -63,7 +63,7 @@ FUSABLE = {
 }
 
 
-@pytest.fixture(params=["auto", "nohalo", "halostream", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall",
+@pytest.fixture(params=["auto", "nohalo", "halostream", "halo0", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall",
                         "nofp4", "fp4all", "nopair", "pair224", "nosmall", "cg1", "nosplit", "split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -84,6 +84,8 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_fp4({"fp4": 1, "fp4all": 2, "nofp4": 0}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_fp4_pair({"nopair": 0, "pair224": 3}.get(p, 1)))
     bnn._lib.check(lib.bnn_set_fused_halo({"nohalo": 0, "halostream": 2}.get(p, 1)))
+    # the pixel-input first conv on the halo FP4 kernel (opt-in: measured slower than pix_tile)
+    bnn._lib.check(lib.bnn_set_fused_halo0(1 if p == "halo0" else 0))
     bnn._lib.check(lib.bnn_set_fused_lin4(0 if p == "nolin4" else 1))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
@@ -94,6 +96,7 @@ def tiling(bnn, request):
     lib.bnn_set_fused_fp4(1)
     lib.bnn_set_fused_fp4_pair(1)
     lib.bnn_set_fused_halo(1)
+    lib.bnn_set_fused_halo0(0)
     lib.bnn_set_fused_lin4(1)
 
 
@@ -112,8 +115,9 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     net = fused()
     x = orc.fill_random((batch, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     got = net.forward(x)
-    # pack_pixels + 9 weighted layers, or 9 when the CUDA-core first conv reads the floats itself
-    assert net.last_launches() == (9 if tiling in ("auto", "pixf32") else 10)
+    # 9 weighted layers, + pack_pixels when the first conv reads packed pixel words (the int8
+    # tensor-core path and pix_popc after the packer); halo0 and pix_tile read the floats
+    assert net.last_launches() == (9 if tiling in ("auto", "pixf32", "halo0") else 10)
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 

@@ -16,7 +16,7 @@ lib = bnn.load()
 SETTINGS = {"default": {}, "split16": {"split": 16, "lin4": 0}, "nosplit": {"split": 1, "lin4": 0},
             "nohalo": {"halo": 0}, "halostream": {"halo": 2}, "nolin4": {"lin4": 0},
             "swapall": {"swap": 2, "halo": 0}, "noswap": {"swap": 0, "halo": 0}, "nosmall": {"small": 0},
-            "nopixpopc": {"pix": 0}, "pixf32": {"pix": 1}, "pixpacked": {"pix": 2},
+            "nopixpopc": {"pix": 0}, "pixf32": {"pix": 1}, "pixpacked": {"pix": 2}, "halo0": {"halo0": 1},
             "nopair": {"pair": 0, "halo": 0}, "pair224": {"pair": 3, "halo": 0}, "fp4all": {"fp4": 2}, "nofp4": {"fp4": 0}}
 QUICK = len(sys.argv) > 1 and sys.argv[1] == "quick"
 if QUICK:
@@ -25,6 +25,7 @@ bad = 0
 for name, st in SETTINGS.items():
     lib.bnn_set_fused_split(st.get("split", 0))
     lib.bnn_set_fused_halo(st.get("halo", 1))
+    lib.bnn_set_fused_halo0(st.get("halo0", 0))
     lib.bnn_set_fused_lin4(st.get("lin4", 1))
     lib.bnn_set_fused_swap(st.get("swap", 1))
     lib.bnn_set_fused_small_logits(st.get("small", 1))
