@@ -2103,6 +2103,8 @@ int launch_pack_pixels(const float* x, size_t B, int C, size_t HW, uint32_t* out
 }
 
 
+void fused_timeline_name(const char* name) { g_tl_names.push_back(name); }
+
 unsigned long long* fused_timeline_slot(int slots) {
     if (g_tl_used < 0 || g_tl_used + slots > kTlSlots) return nullptr;
     unsigned long long* p = g_tl + size_t(g_tl_used) * kTlCtas * 4;

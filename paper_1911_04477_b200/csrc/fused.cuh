@@ -75,6 +75,7 @@ struct HaloGeom {
     int wst;             // 0: weights resident in shared memory; else ring slots of streamed blocks
     size_t smem;
     FastDiv dP, dS, dQ, dWh, dG;
+    unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
     const float* in_f32;      // first layer (halo0): float NCHW input, creal channels -> bit words
     int creal;
     unsigned long long* dbg;  // BNN_HALO_PROFILE counters, else null
@@ -108,6 +109,7 @@ struct LinGeom {
     int* ws;
     unsigned* sem;
     unsigned long long* dbg;  // BNN_LIN4_PROFILE phase stamps, else null
+    unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
 };
 bool lin4_plan(const FusedGeom& g, int epi, LinGeom& l);
 size_t lin4_ws_bytes(const LinGeom& l);
@@ -117,6 +119,7 @@ int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s);
 // Debug timeline (globaltimer stamps per CTA and launch): op 1 enable + reset, 2 print + disable.
 int fused_timeline(int op);
 unsigned long long* fused_timeline_slot(int slots);
+void fused_timeline_name(const char* name);
 // Swapped-operand conv (fused_swap_kernel): 128 channels x 256 positions per tile, bits
 // epilogue, CTA-local; tm must be the weight map with box rows 128.
 int launch_swap(int in_mode, const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s);

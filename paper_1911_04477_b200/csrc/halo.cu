@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "bnn_common.cuh"
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     asm volatile("griddepcontrol.launch_dependents;");
     const bool prof = g.dbg != nullptr;
     const long long k_start = prof ? hclock() : 0;
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = hgtimer();
     if (prof && threadIdx.x == 0) atomicMin(g.dbg + 14, hgtimer());
     const int mt = int(blockIdx.x) % g.m_tiles;
     const int nstride = int(gridDim.x) / g.m_tiles;
@@ -356,6 +358,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     __syncthreads();
     tc_fence_after();
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 2] = hgtimer();
     const long long k_main = prof ? hclock() : 0;
     if (prof && threadIdx.x == 0) atomicAdd(g.dbg + 12, (unsigned long long)(k_main - k_start));
 
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
+        if (g.tl && lane == 0) g.tl[blockIdx.x * 4 + 1] = hgtimer();
     } else if (warp >= 4 && warp < 4 + kHEpiWarps) {
         // epilogue: lane = output channel. Pass 1: aligned 32-column chunks of the accumulator
         // (the two warps of a lane quarter alternate chunks) -> per column, the 32-channel word of
@@ -582,6 +586,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = hgtimer();
     if (prof && threadIdx.x == 0) {
         atomicAdd(g.dbg + 13, (unsigned long long)(hclock() - k_start));
         atomicMax(g.dbg + 15, hgtimer());
@@ -616,9 +621,9 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
     long best = -1;
     // weights resident (wst = 0) when the CTA's slice fits next to two halo stages, else a ring of
     // kHMaxWst streamed blocks (K chunks per tap a power of two)
+    if (cpt & (cpt - 1)) return false;  // the unrolled issue loops take 1, 2, 4 or 8 K steps per tap
     for (int wst : {0, kHMaxWst}) {
         if (best >= 0) break;  // a resident plan exists
-        if (wst && (cpt & (cpt - 1))) break;
         const size_t wbytes = size_t(wst ? wst : KB4) * 16384;
         for (int G = 1; G <= 16; G *= 2) {
             if (G > 1 && G > fg.B) break;
@@ -678,6 +683,7 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
     h.dbg_mode = 0;
     h.in_f32 = nullptr;
     h.creal = 0;
+    h.tl = nullptr;
     return true;
 }
 
@@ -734,8 +740,12 @@ int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static const bool prof = getenv("BNN_HALO_PROFILE") != nullptr;
+    HaloGeom ht = h;
+    ht.tl = fused_timeline_slot(1);
+    if (ht.tl) fused_timeline_name((std::string("halo4 D=") + std::to_string(h.D) + " C=" + std::to_string(h.Cw * 32) +
+                                    " W=" + std::to_string(h.W) + (h.pool ? " pool" : "")).c_str());
     if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, h.wst ? halo4_kernel<true> : halo4_kernel<false>, tm4, h));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, h.wst ? halo4_kernel<true> : halo4_kernel<false>, tm4, ht));
         BNN_TRY(launch_check("halo4_kernel"));
     } else {  // synchronous, not capturable: tools only
         HaloGeom hp = h;

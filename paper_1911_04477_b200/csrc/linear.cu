@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "bnn_common.cuh"
 #include "fused.cuh"
@@ -94,7 +95,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     const int units = g.m_tiles * g.n_tiles * g.ksplit;
-    const unsigned long long t_start = g.dbg ? lgtimer() : 0;
+    const unsigned long long t_start = (g.dbg || g.tl) ? lgtimer() : 0;
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = t_start;
     // BNN_LIN4_PROFILE: per-phase times (ns since the CTA started, summed over CTAs)
     auto stamp = [&](int k) {
         if (g.dbg) atomicAdd(g.dbg + k, lgtimer() - t_start);
@@ -189,9 +191,11 @@ __global__ void __launch_bounds__(kLThreads, 1)
         mbar_wait(tempty, (i & 1) ^ 1);  // the epilogue has read the last accumulator
         tc_fence_after();
         tmem_dealloc<512>(tmem_base);
+        if (g.tl && lane == 0) g.tl[blockIdx.x * 4 + 1] = lgtimer();
     } else if (warp < 6) {
         // epilogue: lane = output feature d, TMEM columns = images
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (g.tl && warp == 2 && lane == 0) g.tl[blockIdx.x * 4 + 2] = lgtimer();
         const int q = warp & 3;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
@@ -362,6 +366,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         }
     }
     if (threadIdx.x == 0) stamp(6);
+    if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = lgtimer();
 }
 
 // Host plan: images per tile (NB, <= 256, a multiple of 16), feature tiles of 128 and the K
@@ -406,6 +411,14 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
             }
         }
     }
+    if (const char* f = getenv("BNN_LIN4_FORCE")) {  // experiments: "NB,split" for every lin4 layer
+        int nb = 0, ks = 0;
+        if (sscanf(f, "%d,%d", &nb, &ks) == 2 && nb >= 16 && nb <= 256 && nb % 16 == 0 && ks >= 1) {
+            l.NB = nb, l.n_tiles = (fg.B + nb - 1) / nb;
+            l.kbs = (l.KB4 + ks - 1) / ks, l.ksplit = (l.KB4 + l.kbs - 1) / l.kbs;
+            if (l.ksplit > 1 && l.m_tiles * l.n_tiles * l.ksplit > sms) return false;
+        }
+    }
     l.nst = int(std::min<size_t>(kLStages, (kLSmem - 1024 - 256) / (16384 + size_t(l.NB) * 128)));
     l.Dpad = (fg.D + 31) / 32 * 32;
     l.prm = fg.prm;
@@ -416,6 +429,7 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     l.ws = nullptr;
     l.sem = nullptr;
     l.dbg = nullptr;
+    l.tl = nullptr;
     return true;
 }
 
@@ -441,8 +455,12 @@ int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static const bool prof = getenv("BNN_LIN4_PROFILE") != nullptr;
+    LinGeom lt = l;
+    lt.tl = fused_timeline_slot(1);
+    if (lt.tl) fused_timeline_name(("lin4 D=" + std::to_string(l.D) + " K=" + std::to_string(l.K) + " split=" +
+                                    std::to_string(l.ksplit)).c_str());
     if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, l));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, lt));
         BNN_TRY(launch_check("lin4_kernel"));
     } else {  // synchronous, not capturable: tools only
         LinGeom lp = l;
