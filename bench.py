@@ -965,10 +965,11 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "binary (+-1 bits; exact FP4 e2m1 / int8 tensor-core MMA, integer-valued accumulate), f32 logits",
             "data": "synthetic: reference fill_random input stream (seed 1), seed-derived weights",
-            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
-                       "parallelism": f"dp{world}: batch shards, replicated packed weights, NCCL logits gather",
-                       "engine": engine, "l2": "flushed before every step (256 MiB write outside the events)",
-                       "binary_tops": net_ops * world * args.steps / (total_ms * 1e-3) / 1e12},
+            # config: the workload only, identical in both arms (the driver compares them)
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world},
+            "arm": {"parallelism": f"dp{world}: batch shards, replicated packed weights, NCCL logits gather",
+                    "engine": engine, "l2": "flushed before every step (256 MiB write outside the events)",
+                    "binary_tops": net_ops * world * args.steps / (total_ms * 1e-3) / 1e12},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {
                 "bound": "tensor", "achieved": achieved, "peak": kpeak, "unit": "TOPS",
@@ -1037,8 +1038,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "binary (+-1 bits, popcount), f32 epilogue",
         "data": "synthetic: reference fill_random input stream (seed 1), seed-derived weights",
-        "config": {"workload": WORKLOAD, "batch_per_gpu": args.batch, "global_batch": args.batch,
-                   "parallelism": f"CPU: the batch sharded over {cores} host threads"},
+        # config: the workload only, identical in both arms (the driver compares them)
+        "config": {"workload": WORKLOAD, "batch_per_gpu": args.batch, "global_batch": args.batch * world},
+        "arm": {"parallelism": f"CPU: the batch sharded over {cores} host threads (rank 0 of {world})"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "reference",
                          "sample": f"the full {args.batch}-image batch per step, oracle/_ref/libbnnref_{ref.isa}.so",
                          "threads_1_images_per_s": one, "cpu": cpu_info()},
