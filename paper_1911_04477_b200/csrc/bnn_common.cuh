@@ -66,6 +66,14 @@ __host__ __device__ __forceinline__ float unit_random(uint64_t seed, uint64_t in
     return static_cast<float>(top) * 0x1.0p-23f - 1.0f;
 }
 
+#ifdef __CUDACC__
+// A value every lane of the (converged) warp holds, through a lane-0 shuffle: ptxas then treats it
+// as warp-uniform, so role branches on the warp index are uniform branches and what is computed
+// under them (UMMA descriptors, TMEM addresses) stays in uniform registers.
+__device__ __forceinline__ int warp_uniform(int x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+#endif
+
 }  // namespace bnnk
 
 #define BNN_TRY(expr)                 \

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int* tu_s = reinterpret_cast<int*>(ftab + kMaxQ);                 // [kMaxD] thresholds Tu
     uint32_t* flip_s = reinterpret_cast<uint32_t*>(tu_s + kMaxD);     // [kMaxD / 32] flip words
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     if (!g.pdl_late) asm volatile("griddepcontrol.launch_dependents;");  // the next layer may start its prologue
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     // (stamp 1 is written at the very end, after the TMEM dealloc)
     // Programmatic dependent launch: everything above touches only this launch's constants
     // (weights' tensor map, thresholds, tables, TMEM, barriers), so it overlaps the previous
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int2* ftab = reinterpret_cast<int2*>(bars + 32);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const int units = gridDim.x, unit = blockIdx.x;
@@ -907,7 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 2] = gtimer();
 
@@ -1458,7 +1458,7 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int2* ftab = reinterpret_cast<int2*>(bars + 32);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = gtimer();
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -1508,7 +1508,7 @@ __global__ void __launch_bounds__(sw4_threads<NP, SP, CG>(), 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     if (warp >= 2 && warp < 6) {  // scale factors: every byte of columns [448, 512) = 2^0
         uint32_t v[32];
 #pragma unroll

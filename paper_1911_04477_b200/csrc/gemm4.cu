@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     const int units = g.m_tiles * g.n_tiles;
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; ++s) {
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     if (warp >= 2 && warp < 6) {  // block scales: every byte of columns [496, 512) = 2^0
         uint32_t v[8];
 #pragma unroll

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     uint64_t* wempty = wfull + kHMaxWst;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + kHMaxWst);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     const bool prof = g.dbg != nullptr;
     const long long k_start = prof ? hclock() : 0;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     if (warp == 0 && lane == 0 && !STREAM) {
         // the resident weights are build-time constants: load them before the grid dependency
         mbar_arrive_expect_tx(wbar, wbytes);
@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         HClock cw, ct, cf;
         if (!STREAM) cw.wait(prof, wbar, 0);
         tc_fence_after();
+        long long t_first = 0;
         int hs = 0, i = 0, ws = 0;
         uint32_t hph = 0, wph = 0;
         for (int nt = n0; nt < g.n_tiles; nt += nstride, ++i) {
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             ct.wait(prof, &tempty[acc], ((i >> 1) & 1) ^ 1);
             cf.wait(prof, &full[hs], hph);
             tc_fence_after();
+            if (prof && i == 0) t_first = hclock() - k_main;
             {
                 const uint32_t d = tmem_base + uint32_t(acc * g.N);
                 // descriptors by 32-bit adds on the start-address field (every address < 256 KB)
@@ -426,6 +428,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             atomicAdd(g.dbg + 1, (unsigned long long)ct.acc);
             atomicAdd(g.dbg + 2, (unsigned long long)cf.acc);
             atomicAdd(g.dbg + 3, (unsigned long long)(hclock() - k_main));
+            atomicAdd(g.dbg + 8, (unsigned long long)t_first);
         }
         // the epilogue has read the last accumulators
         for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
@@ -444,6 +447,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const bool wvalid = m0 < g.D;
         const int4 pc = wvalid ? __ldg(g.prm + m0 + lane) : make_int4(0x7fffffff, 0, 0, 0);
         const float Tf = float(pc.x);  // exact: |Tu| <= K < 2^24
+        const float Tm1 = Tf - 1.0f;    // ge_bits form of the same threshold
         const bool flip = pc.y != 0;
         const int oword = m0 >> 5;
         const int nch = (g.dbg_mode & 1) ? 0 : (g.N + 31) >> 5;
@@ -453,31 +457,48 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const int npu = (g.dbg_mode & 1) ? 0 : (g.TR >> 1) * g.G * nwch;
         int i = 0;
         HClock ce;
+        long long t_ld = 0, t_cmp = 0;  // profile: unpooled chunk time in TMEM loads / in total
         for (int nt = n0; nt < g.n_tiles; nt += nstride, ++i) {
             const int acc = i & 1;
             ce.wait(prof, &tfull[acc], (i >> 1) & 1);
             tc_fence_after();
+            if (prof && i == 0 && warp == 4 && lane == 0) atomicAdd(g.dbg + 9, (unsigned long long)(hclock() - k_main));
             const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g.N);
             const int r0 = nt * g.TR;
             if (!g.pool) {
-                for (int cc = half; cc < nch; cc += 2) {
-                    uint32_t v[32];
-                    tmem_ld32(tb + uint32_t(32 * cc), v);
+                // this warp's chunks are cc0, cc0 + 2, ... (the pair's first chunk alternates per
+                // tile so odd chunk counts balance); two chunks per pass, both loads in flight
+                const int cc0 = half ^ (i & 1);
+                for (int cc = cc0; cc < nch; cc += 4) {
+                    const bool two = cc + 2 < nch;  // warp-uniform
+                    uint32_t v0[32], v1[32];
+                    const long long c0 = prof ? hclock() : 0;
+                    tmem_ld32(tb + uint32_t(32 * cc), v0);
+                    if (two) tmem_ld32(tb + uint32_t(32 * (cc + 2)), v1);
                     tmem_ld_wait();
-                    const uint32_t mine = decisions_transposed(v, Tf, flip, lane);
-                    const int col = 32 * cc + lane;
-                    if (col < ncol && wvalid) {
-                        const int ir = g.dP.div(col), x = col - ir * g.P;
-                        const int slot = g.dQ.div(x), w = x - slot * g.Q;
-                        const int r = r0 + ir, grp = g.dS.div(r), h = r - grp * g.S;
-                        const int b = grp * g.G + slot;
-                        if (w < g.W && h < g.H && slot < g.G && b < g.B)
-                            g.out[(size_t(b * g.H + h) * g.W + w) * g.Dw + oword] = mine;
+                    if (prof) t_ld += hclock() - c0;
+                    const uint32_t fm = flip ? 0xFFFFFFFFu : 0u;
+                    uint32_t m0 = ge_bits(v0, Tm1) ^ fm, m1 = two ? ge_bits(v1, Tm1) ^ fm : 0u;
+                    m0 = transpose32(m0, lane);
+                    if (two) m1 = transpose32(m1, lane);
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        if (k == 1 && !two) break;
+                        const int col = 32 * (cc + 2 * k) + lane;
+                        if (col < ncol && wvalid) {
+                            const int ir = g.dP.div(col), x = col - ir * g.P;
+                            const int slot = g.dQ.div(x), w = x - slot * g.Q;
+                            const int r = r0 + ir, grp = g.dS.div(r), h = r - grp * g.S;
+                            const int b = grp * g.G + slot;
+                            if (w < g.W && h < g.H && slot < g.G && b < g.B)
+                                g.out[(size_t(b * g.H + h) * g.W + w) * g.Dw + oword] = k ? m1 : m0;
+                        }
                     }
+                    if (prof) t_cmp += hclock() - c0;
                 }
             } else {
                 // units: (row pair, image slot, <= 32 columns), alternating between the two warps
-                for (int u = half; u < npu; u += 2) {
+                for (int u = half ^ (i & 1); u < npu; u += 2) {  // first unit alternates per tile
                     const int ch = u % nwch, t2 = u / nwch;
                     const int slot = t2 % g.G, ir = 2 * (t2 / g.G);
                     const int r = r0 + ir, grp = g.dS.div(r), h = r - grp * g.S;
@@ -503,6 +524,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
         if (prof && warp == 4 && lane == 0) {
             atomicAdd(g.dbg + 6, (unsigned long long)ce.acc);
             atomicAdd(g.dbg + 7, (unsigned long long)(hclock() - k_main));
+            atomicAdd(g.dbg + 10, (unsigned long long)t_ld);
+            atomicAdd(g.dbg + 11, (unsigned long long)t_cmp);
         }
     } else if (warp == 2 || warp == 3 || warp == 12 || warp >= 14) {
         // halo producers: canvas pixel j of the tile -> its Cw words (or the all-ones frame word)
@@ -763,10 +786,10 @@ int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
         fprintf(stderr,
                 "[halo4 mode=%d B=%d H=%d W=%d C=%d D=%d pool=%d | G=%d P=%d TR=%d N=%d NH=%d nst=%d tiles=%d grid=%d] "
                 "span %.1f us | per-CTA kcyc: setup %.1f, total %.1f | mma: wait-w %.1f wait-acc %.1f wait-halo %.1f "
-                "busy-total %.1f | prod: wait %.1f total %.1f | epi: wait %.1f total %.1f\n",
+                "busy-total %.1f | prod: wait %.1f total %.1f | epi: wait %.1f total %.1f (unpooled chunks: ld %.1f all %.1f) | first halo %.1f first acc %.1f\n",
                 hp.dbg_mode, h.B, h.H, h.W, h.Cw * 32, h.D, h.pool, h.G, h.P, h.TR, h.N, h.NH, h.nst, h.n_tiles, h.grid,
                 (d[15] - d[14]) / 1e3, d[12] / n / k, d[13] / n / k, d[0] / n / k, d[1] / n / k, d[2] / n / k,
-                d[3] / n / k, d[4] / n / k, d[5] / n / k, d[6] / n / k, d[7] / n / k);
+                d[3] / n / k, d[4] / n / k, d[5] / n / k, d[6] / n / k, d[7] / n / k, d[10] / n / k, d[11] / n / k, d[8] / n / k, d[9] / n / k);
     }
     set_last_gemm("halo4_kernel");
     return BNN_OK;

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
     const int units = g.m_tiles * g.n_tiles * g.ksplit;
     const unsigned long long t_start = (g.dbg || g.tl) ? lgtimer() : 0;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
     if (warp >= 2 && warp < 6) {  // block scales: every byte of columns [496, 512) = 2^0
         uint32_t v[8];
 #pragma unroll
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                             if (bc + j < g.B && bc + j < b0 + g.NB) dst[size_t(j) * g.Dpad] = int(__uint_as_float(v[j]));
                     }
                 } else if (g.epi == FEPI_BITS) {
-                    const uint32_t mine = decisions_transposed(v, Tf, flip, lane);
+                    const uint32_t mine = decisions_transposed(v, Tf - 1.0f, flip, lane);
                     if (d0 < g.D && bc + lane < g.B && lane < g.NB - 32 * c)
                         g.out_bits[size_t(bc + lane) * g.Dw + (d0 >> 5)] = mine;
                 } else {

@@ -206,17 +206,24 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | (uint32_t(M >> 4) << 24);     // m_dim
 }
 
-// ------------------------------------------------------- epilogue: 32 x 32 decision transpose
-// Lane c holds 32 accumulator columns of output channel c (a tcgen05.ld 32x32b.x32). Returns
-// lane j's packed word for column j: bit c = (acc[c][j] >= T_c) ^ flip_c. Each lane builds its
-// 32 decision bits (compare + select per column), then a 32 x 32 bit transpose across the warp
-// in five shuffle-xor butterfly rounds: ~95 instructions per 32 columns instead of 32 ballots
-// (~130 instructions and a VOTE dependency chain per ballot).
-__device__ __forceinline__ uint32_t decisions_transposed(const uint32_t (&v)[32], float T, bool flip, int lane) {
-    uint32_t m = 0;
+// Bit j of the result = (v[j] >= T) for exact integer-valued f32 accumulators and an integer
+// threshold passed as Tm1 = T - 1: v >= T <=> v > T - 1 <=> (Tm1 - v) < 0, the sign bit of an
+// exact difference (0 - 0 is +0, so equality reads "not less"). One FADD + one funnel shift per
+// column instead of a compare, a select and an OR.
+// Four independent 8-column chains (one 32-long funnel-shift chain was latency-bound: ncu
+// stall_wait on the dependent SHF), merged at the end.
+__device__ __forceinline__ uint32_t ge_bits(const uint32_t (&v)[32], float Tm1) {
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int j = 0; j < 32; ++j) m |= uint32_t(__uint_as_float(v[j]) >= T) << j;
-    if (flip) m = ~m;
+    for (int j = 7; j >= 0; --j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            m[c] = __funnelshift_l(__float_as_uint(Tm1 - __uint_as_float(v[8 * c + j])), m[c], 1);
+    return m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24);
+}
+
+// 32 x 32 bit transpose across the warp: bit j of lane i -> bit i of lane j (5 shuffle rounds).
+__device__ __forceinline__ uint32_t transpose32(uint32_t m, int lane) {
 #pragma unroll
     for (int j = 16; j >= 1; j >>= 1) {
         const uint32_t k = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
@@ -225,6 +232,12 @@ __device__ __forceinline__ uint32_t decisions_transposed(const uint32_t (&v)[32]
         m = (lane & j) ? ((m & ~k) | ((p >> j) & k)) : ((m & k) | ((p & k) << j));
     }
     return m;
+}
+
+// Lane = output channel, v = its 32 accumulator columns: returns, in lane j, the 32-channel word
+// of column j's decisions (v >= T) ^ flip (T - 1 passed as Tm1, see ge_bits).
+__device__ __forceinline__ uint32_t decisions_transposed(const uint32_t (&v)[32], float Tm1, bool flip, int lane) {
+    return transpose32(ge_bits(v, Tm1) ^ (flip ? 0xFFFFFFFFu : 0u), lane);
 }
 
 // ---------------------------------------------------- warp-issued forms (one elected lane)

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(128, 1) check(const uint8_t* A, const uint8_t*
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sp = smem_raw + (base - raw);
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2;
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // A smem [4 chunks][128 rows][16 B] at base; B smem [4 chunks][kRowsB rows][16 B] at base + 8192
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(128, 1) check(const uint8_t* A, const uint8_t*
     }
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&bar2, 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<512>(&tslot);
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsi
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2;
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsi
         st_shared_v4(base + 16 * i, 0x22222222u * (i & 1), 0x02020202u, 0u, 0x20202020u);
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&bar2, 1);
         fence_mbar_init();
         stop = 0;
     }
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(128, 1) seq(int N, int P, int cpt, int NH, int
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2;
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB4 = (9 * cpt + 3) / 4;
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(128, 1) seq(int N, int P, int cpt, int NH, int
         st_shared_v4(base + 16 * i, 0x22222222u * (i & 1), 0x02020202u, 0u, 0x20202020u);
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&bar2, 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<512>(&tslot);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(128, 1) seq(int N, int P, int cpt, int NH, int
         const uint32_t lbo = NH * 16;
         long long t0 = clock64();
         for (int t = 0; t < tiles; ++t) {
-            const uint32_t d = tm + (t & 1) * N;
+            const uint32_t d = tm + (t & 1) * ((FLAGS & 8) ? 256 : N);
             const uint64_t ad0 = sdesc_k_sw128(base);
             const uint64_t bd0 = sdesc_k_none(hb, lbo, 128);
             uint32_t aoff = 0;
@@ -356,6 +359,12 @@ __global__ void __launch_bounds__(128, 1) seq(int N, int P, int cpt, int NH, int
                     if (!(FLAGS & 2)) aoff += (s & 3) == 3 ? (16384u - 96u) / 16u : 2u;
                     boff += 2u * (lbo >> 4);
                 }
+            }
+            if (FLAGS & 16) {  // a commit per tile (the kernel commits the halo stage and the accumulator)
+                asm volatile(
+                    "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                    "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar2))
+                    : "memory");
             }
         }
         long long t1 = clock64();
@@ -467,6 +476,22 @@ int main() {
     run_tmem<4, 1>(32);
     if (getenv("HALO_PROBE_SKIP_SEQ")) return 0;
     // conv1 / conv3 / conv4 geometries of the halo kernel
+    if (getenv("HALO_PROBE_SWEEP")) {
+        // LBO (halo rows NH) and K steps per tap, N = 208 / 224 / 256
+        for (int N : {208, 256})
+            for (int nh = N + 72; nh <= N + 136; nh += 8) {
+                run_seq<0>("sweep real", N, 34, 2, nh);
+                run_seq<3>("sweep no shift, A fixed", N, 34, 2, nh);
+            }
+        run_seq<0>("cpt4 real", 208, 34, 4, 280);
+        run_seq<3>("cpt4 no shift, A fixed", 208, 34, 4, 280);
+        run_seq<0>("cpt2 real", 224, 37, 2, 304);
+        run_seq<3>("cpt2 no shift, A fixed", 224, 37, 2, 304);
+        run_seq<0>("cpt1 real", 208, 34, 1, 280);
+        run_seq<0>("P mult 8 real", 208, 40, 2, 296);
+        run_seq<0>("P mult 8 real", 208, 48, 2, 304);
+        return 0;
+    }
     run_seq<0>("warp, real", 208, 34, 2, 280);
     run_seq<1>("warp, no tap shift", 208, 34, 2, 280);
     run_seq<2>("warp, A fixed", 208, 34, 2, 280);
@@ -478,6 +503,12 @@ int main() {
     run_seq<1>("warp, no tap shift", 224, 37, 4, 304);
     run_seq<0>("warp, real", 256, 34, 2, 336);
     run_seq<0>("warp, real, NH mult 8 rows", 208, 40, 2, 296);
+    run_seq<8>("warp, real, acc at 256", 208, 34, 2, 280);
+    run_seq<16>("warp, real, commit per tile", 208, 34, 2, 280);
+    run_seq<24>("warp, real, acc 256, commit", 208, 34, 2, 280);
+    run_seq<8>("warp, real, acc at 256", 144, 18, 4, 184);
+    run_seq<0>("warp, real", 160, 10, 4, 184);
+    run_seq<8>("warp, real, acc at 256", 160, 10, 4, 184);
 
     int bad = 0;
     if (getenv("HALO_PROBE_ALL")) {

@@ -17,6 +17,8 @@ if len(sys.argv) > 2:
 s = torch.cuda.current_stream().cuda_stream
 x = torch.empty((B, 3, 32, 32), dtype=torch.float32, device="cuda")
 bnn._lib.check(bnn.load().bnn_fill_random_f32(bnn.mix64(1, 0x696E707574), 0, x.numel(), x.data_ptr(), s))
-out = net.forward_device(x)
+# REPS forwards (profile counters print per launch: the first forward is cold — TLB, L2)
+for _ in range(int(os.environ.get("REPS", "1"))):
+    out = net.forward_device(x)
 torch.cuda.synchronize()
 print("ok", out.shape, net.engine)
