@@ -59,6 +59,9 @@ constexpr int kHMaxN = 240;
 constexpr int kHMaxStages = 4;
 constexpr int kHMaxWst = 8;  // streamed-weight ring slots
 constexpr size_t kHSmemMax = 232448;  // 227 KB opt-in per CTA
+constexpr size_t kHBarBytes = 256;     // mbarriers + the TMEM slot
+constexpr int kHTabs = kHMaxStages + 2;  // column-table ring: producers run <= nst + 2 tiles ahead of the epilogue
+constexpr size_t kHTail = kHBarBytes + size_t(kHTabs) * kHMaxN * 4;  // + the epilogue's column tables
 
 // K-major, no swizzle: core matrix = 8 rows x 16 bytes, 8-row groups 128 B apart (SBO), the two
 // K core matrices of one K=64 e2m1 step LBO apart.
@@ -223,8 +226,16 @@ __device__ __forceinline__ long long halo_src(const HaloGeom& g, int idx) {
 
 // Halo rows j0 and j0 + kHProdThreads of a tile: every vector load of both rows is issued before
 // the first store (one L2 round trip per pair of rows). V words per load (Cw <= 16).
+// Halo row j is the input pixel of tap (1, 1) of tile column j - (P + 1), whose output pixel (a
+// "same" conv on the same canvas) it therefore also is: unpooled layers record it in the tile's
+// column table for the epilogue (tab, else null).
+__device__ __forceinline__ void put_col(const HaloGeom& g, int* tab, int j, long long pix) {
+    const int c = j - g.P - 1;  // columns past the tile's TR canvas rows (N is a multiple of 16): -1
+    if (tab && c >= 0 && c < g.N) tab[c] = c < g.TR * g.P ? int(pix) : -1;
+}
+
 template <int V>
-__device__ __forceinline__ void fill_rows(const HaloGeom& g, uint32_t hb, uint32_t lbo, int q0, int j0, int nh) {
+__device__ __forceinline__ void fill_rows(const HaloGeom& g, uint32_t hb, uint32_t lbo, int q0, int j0, int nh, int* tab) {
     using Vec = typename std::conditional<V == 4, uint4, uint2>::type;
     constexpr int kMaxV = 16 / V;
     const int nv = g.Cw / V;
@@ -235,6 +246,7 @@ __device__ __forceinline__ void fill_rows(const HaloGeom& g, uint32_t hb, uint32
         const int j = j0 + h * kHProdThreads;
         has[h] = j < nh;
         const long long pix = has[h] ? halo_src(g, q0 + j) : -1;
+        if (has[h]) put_col(g, tab, j, pix);
         const Vec* src = reinterpret_cast<const Vec*>(g.in + (pix < 0 ? 0 : pix) * g.Cw);
 #pragma unroll
         for (int v = 0; v < kMaxV; ++v) {
@@ -305,6 +317,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     uint64_t* wfull = wbar + 1;                 // streamed weights: [kHMaxWst] ring slots
     uint64_t* wempty = wfull + kHMaxWst;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wempty + kHMaxWst);
+    int* coltab = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + kHBarBytes);  // [nst + 2][kHMaxN]
 
     const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
@@ -451,11 +464,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const bool flip = pc.y != 0;
         const int oword = m0 >> 5;
         const int nch = (g.dbg_mode & 1) ? 0 : (g.N + 31) >> 5;
-        const int ncol = g.TR * g.P;  // tile columns that are canvas positions of this tile
         const int Hh = g.H >> 1, Wh = g.W >> 1;
         const int nwch = (g.W + 31) >> 5;  // pooled units per row pair and slot
         const int npu = (g.dbg_mode & 1) ? 0 : (g.TR >> 1) * g.G * nwch;
-        int i = 0;
+        int i = 0, ts = 0;
         HClock ce;
         long long t_ld = 0, t_cmp = 0;  // profile: unpooled chunk time in TMEM loads / in total
         for (int nt = n0; nt < g.n_tiles; nt += nstride, ++i) {
@@ -466,6 +478,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
             const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g.N);
             const int r0 = nt * g.TR;
             if (!g.pool) {
+                // the tile's column table (tile column -> NHWC output pixel, or -1 for frame columns
+                // and images past the batch), written by the producers with the halo: slot ts of
+                // the ring, whose next writer (tile i + nst + 2) waits for this tile's accumulator
+                // release (tempty) through the halo and MMA barriers
+                const int* tab = (g.dbg_mode & 2) ? nullptr : coltab + ts * kHMaxN;  // profile: no halo, no table
+                if (++ts == g.nst + 2) ts = 0;
                 // this warp's chunks are cc0, cc0 + 2, ... (the pair's first chunk alternates per
                 // tile so odd chunk counts balance); two chunks per pass, both loads in flight
                 const int cc0 = half ^ (i & 1);
@@ -485,14 +503,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     for (int k = 0; k < 2; ++k) {
                         if (k == 1 && !two) break;
                         const int col = 32 * (cc + 2 * k) + lane;
-                        if (col < ncol && wvalid) {
-                            const int ir = g.dP.div(col), x = col - ir * g.P;
-                            const int slot = g.dQ.div(x), w = x - slot * g.Q;
-                            const int r = r0 + ir, grp = g.dS.div(r), h = r - grp * g.S;
-                            const int b = grp * g.G + slot;
-                            if (w < g.W && h < g.H && slot < g.G && b < g.B)
-                                g.out[(size_t(b * g.H + h) * g.W + w) * g.Dw + oword] = k ? m1 : m0;
-                        }
+                        const int pix = tab && col < g.N ? tab[col] : -1;
+                        if (pix >= 0 && wvalid) g.out[size_t(pix) * g.Dw + oword] = k ? m1 : m0;
                     }
                     if (prof) t_cmp += hclock() - c0;
                 }
@@ -533,12 +545,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
         // (warps 2, 3, 12, 14, 15: none on the MMA warp's sub-partition 1; warp 13 idles)
         const int pw = warp < 4 ? warp - 2 : warp == 12 ? 2 : warp - 11;
         const int pt = pw * 32 + lane;
-        int hs = 0;
+        int hs = 0, ts = 0;
         uint32_t hph = 0;
         HClock cp;
         for (int nt = n0; nt < g.n_tiles; nt += nstride) {
             cp.wait(prof, &empty[hs], hph ^ 1);
             const uint32_t hb = sH + uint32_t(hs) * hbytes;
+            int* tab = g.pool ? nullptr : coltab + ts * kHMaxN;
+            if (++ts == g.nst + 2) ts = 0;
             const int q0 = nt * g.TR * g.P;
             const int nh = (g.dbg_mode & 2) ? 0 : g.NH;
             if (g.in_f32) {
@@ -582,6 +596,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     for (int u = 0; u < 2; ++u) {
                         const int j = j0 + u * kHProdThreads;
                         if (j >= nh) break;
+                        put_col(g, tab, j, pix[u]);
                         const uint32_t dst = hb + uint32_t(j) * 16u;
                         // frame pixels all ones (sign(0.0) = +1); channels 32..63 carry zero weights
                         st_expand4(dst, pix[u] < 0 ? ~0u : w0[u]);
@@ -591,9 +606,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
             } else
             for (int j = pt; j < nh; j += 2 * kHProdThreads) {
                 if ((g.Cw & 3) == 0)
-                    fill_rows<4>(g, hb, lbo, q0, j, nh);
+                    fill_rows<4>(g, hb, lbo, q0, j, nh, tab);
                 else
-                    fill_rows<2>(g, hb, lbo, q0, j, nh);
+                    fill_rows<2>(g, hb, lbo, q0, j, nh, tab);
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -661,7 +676,7 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
                 const int N = round_up_i(TR * P, 16);
                 const int NH = round_up_i(N + 2 * P + 2, 8);
                 const size_t hbytes = size_t(fg.Cw) * NH * 16;
-                const size_t avail = kHSmemMax - 1024 - 256;
+                const size_t avail = kHSmemMax - 1024 - kHTail;
                 if (wbytes + 2 * hbytes > avail) continue;
                 const int n_tiles = (total_rows + TR - 1) / TR;
                 const int ctas = std::min(per_m, n_tiles);
@@ -699,7 +714,7 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
         const int ky = t / fg.KW, kx = t % fg.KW;
         h.toff[t] = t < h.taps ? (ky - fg.PH + 1) * h.P + (kx - fg.PW + 1) : 0;
     }
-    h.smem = 1024 + size_t(h.wst ? h.wst : KB4) * 16384 + size_t(h.nst) * fg.Cw * h.NH * 16 + 256;
+    h.smem = 1024 + size_t(h.wst ? h.wst : KB4) * 16384 + size_t(h.nst) * fg.Cw * h.NH * 16 + kHTail;
     h.dWh = FastDiv::make(uint32_t(std::max(1, fg.W / 2)));
     h.dG = FastDiv::make(uint32_t(h.G));
     h.dbg = nullptr;

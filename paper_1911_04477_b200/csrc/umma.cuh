@@ -223,13 +223,20 @@ __device__ __forceinline__ uint32_t ge_bits(const uint32_t (&v)[32], float Tm1) 
 }
 
 // 32 x 32 bit transpose across the warp: bit j of lane i -> bit i of lane j (5 shuffle rounds).
+// Round j: the lane keeps the half of its word selected by mask (k below, ~k in lanes with bit j
+// set) and takes the other half from its partner rotated by j (left in the lower lane, right in
+// the upper; the bits the rotation wraps around are masked off): shuffle, funnel-shift rotate
+// and one LOP3 per round, no lane-dependent branches.
 __device__ __forceinline__ uint32_t transpose32(uint32_t m, int lane) {
 #pragma unroll
     for (int j = 16; j >= 1; j >>= 1) {
         const uint32_t k = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
                                                                                                    : 0x55555555u;
+        const bool up = (lane & j) != 0;
+        const uint32_t mask = up ? ~k : k;
         const uint32_t p = __shfl_xor_sync(0xffffffffu, m, j);
-        m = (lane & j) ? ((m & ~k) | ((p >> j) & k)) : ((m & k) | ((p & k) << j));
+        const uint32_t q = __funnelshift_l(p, p, up ? 32 - j : j);  // rotate left by j, or right by j
+        m = (m & mask) | (q & ~mask);
     }
     return m;
 }

@@ -406,6 +406,188 @@ void run_seq(const char* name, int N, int P, int cpt, int NH) {
     cudaFree(d);
 }
 
+// ---------------------------------------------------------------- the kernel's issue path
+// halo4_kernel's MMA issue (warp-uniform role, descriptors as 32-bit lo/hi adds, taps x CPT
+// unrolled) and alternatives: V 0 elect.sync inside every MMA asm (the kernel), 1 one asm block
+// per tap (elect once, CPT MMAs), 2 an elected lane issues the whole tile (CUTLASS style).
+__device__ __forceinline__ void mma_lohi(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                         uint32_t sf, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 ad, bd;\n\t"
+        "mov.b64 ad, {%1, %2};\n\t"
+        "mov.b64 bd, {%3, %4};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], ad, bd, %5, [%7], [%7], p;\n\t}" ::"r"(d),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc), "r"(sf)
+        : "memory");
+}
+__device__ __forceinline__ void mma_plain(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                          uint32_t sf, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 ad, bd;\n\t"
+        "mov.b64 ad, {%1, %2};\n\t"
+        "mov.b64 bd, {%3, %4};\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], ad, bd, %5, [%7], [%7], p;\n\t}" ::"r"(d),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc), "r"(sf)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+// one tap, 2 K steps, elect once
+__device__ __forceinline__ void mma_tap2(uint32_t d, uint32_t alo0, uint32_t alo1, uint32_t ahi, uint32_t blo0, uint32_t blo1,
+                                         uint32_t bhi, uint32_t idesc, uint32_t sf, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a0, a1, b0, b1;\n\t"
+        "mov.b64 a0, {%1, %3};\n\tmov.b64 a1, {%2, %3};\n\t"
+        "mov.b64 b0, {%4, %6};\n\tmov.b64 b1, {%5, %6};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %8, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a0, b0, %7, [%9], [%9], p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a1, b1, %7, [%9], [%9], 1;\n\t}" ::"r"(d),
+        "r"(alo0), "r"(alo1), "r"(ahi), "r"(blo0), "r"(blo1), "r"(bhi), "r"(idesc), "r"(acc0), "r"(sf)
+        : "memory");
+}
+
+template <int V, int CPT>
+__global__ void __launch_bounds__(128, 1) seq2(int N, int P, int NH, int tiles, unsigned long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    __shared__ uint64_t bar, bar2, bar3, bar4;
+    __shared__ uint32_t tslot;
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    const int KB4 = (9 * CPT + 3) / 4;
+    const uint32_t hb = base + KB4 * 16384;
+    for (int i = threadIdx.x; i < (KB4 * 16384 + 2 * CPT * NH * 16) / 16; i += blockDim.x)
+        st_shared_v4(base + 16 * i, 0x22222222u * (i & 1), 0x02020202u, 0u, 0x20202020u);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&bar2, 1);
+        mbar_init(&bar3, 1);
+        mbar_init(&bar4, 1);
+        fence_mbar_init();
+        mbar_arrive(&bar3);  // phase 0 complete: waits on parity 0 return at once
+    }
+    if (warp == 0) tmem_alloc<512>(&tslot);
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = __shfl_sync(0xffffffffu, tslot, 0);
+    {
+        uint32_t v[8];
+        for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+        tmem_st8(tm + (uint32_t(32 * warp) << 16) + kSfCol, v);
+        tmem_st8(tm + (uint32_t(32 * warp) << 16) + kSfCol + 8, v);
+        tmem_st_wait();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        const uint32_t idesc = idesc_mxf4(128, N);
+        const uint32_t lbo = NH * 16;
+        uint32_t toff[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) toff[t] = uint32_t((t / 3) * P + t % 3);
+        const uint64_t ad0 = sdesc_k_sw128(base);
+        const uint64_t bd0 = sdesc_k_none(hb, lbo, 128);
+        const uint32_t alo = uint32_t(ad0), ahi = uint32_t(ad0 >> 32), blo = uint32_t(bd0), bhi = uint32_t(bd0 >> 32);
+        const uint32_t sf = tm + kSfCol, step16 = 2u * (lbo >> 4);
+        long long t0 = clock64();
+        for (int t = 0; t < tiles; ++t) {
+            const uint32_t d = tm + (t & 1) * N;
+            if constexpr (V >= 3) {  // the kernel's per-tile waits (already-completed phases) and fence
+                mbar_wait(&bar3, 0);
+                mbar_wait(&bar3, 0);
+                tc_fence_after();
+            }
+            if constexpr (V == 0 || V >= 3) {
+#pragma unroll
+                for (int tp = 0; tp < 9; ++tp)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        const int st = tp * CPT + c;
+                        mma_lohi(d, alo + uint32_t((st >> 2) * 1024 + (st & 3) * 2), ahi, blo + toff[tp] + uint32_t(c) * step16, bhi,
+                                 idesc, sf, st != 0);
+                    }
+            } else if constexpr (V == 1) {
+                static_assert(CPT == 2, "tap2");
+#pragma unroll
+                for (int tp = 0; tp < 9; ++tp) {
+                    const int st = tp * 2;
+                    mma_tap2(d, alo + uint32_t((st >> 2) * 1024 + (st & 3) * 2), alo + uint32_t(((st + 1) >> 2) * 1024 + ((st + 1) & 3) * 2),
+                             ahi, blo + toff[tp], blo + toff[tp] + step16, bhi, idesc, sf, st != 0);
+                }
+            } else {
+                if (elect_one()) {
+#pragma unroll
+                    for (int tp = 0; tp < 9; ++tp)
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) {
+                            const int st = tp * CPT + c;
+                            mma_plain(d, alo + uint32_t((st >> 2) * 1024 + (st & 3) * 2), ahi, blo + toff[tp] + uint32_t(c) * step16,
+                                      bhi, idesc, sf, st != 0);
+                        }
+                }
+                __syncwarp();
+            }
+            asm volatile(
+                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar2))
+                : "memory");
+            if constexpr (V >= 4)
+                asm volatile(
+                    "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                    "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar4))
+                    : "memory");
+            if constexpr (V >= 5) __syncwarp();
+        }
+        long long t1 = clock64();
+        if (lane == 0) {
+            mma_commit(&bar);
+            mbar_wait(&bar, 0);
+        }
+        __syncwarp();
+        long long t2 = clock64();
+        if (blockIdx.x == 0 && lane == 0) {
+            out[0] = t1 - t0;
+            out[1] = t2 - t0;
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+template <int V, int CPT>
+void run_seq2(const char* name, int N, int P, int NH) {
+    unsigned long long* d;
+    cudaMalloc(&d, 64);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    auto k = seq2<V, CPT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int tiles = 100;
+    k<<<sms, 128, 200 * 1024>>>(N, P, NH, 2, d);
+    k<<<sms, 128, 200 * 1024>>>(N, P, NH, tiles, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[2];
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    const double n = double(tiles) * 9 * CPT;
+    printf("seq2 V%d %-22s N=%3d P=%2d cpt=%d NH=%3d: %6.1f cyc/mma (ideal %5.1f), issue %6.1f  err=%s\n", V, name, N, P, CPT, NH,
+           double(h[1]) / n, N / 2.0, double(h[0]) / n, cudaGetErrorString(err));
+    cudaFree(d);
+}
+
 // ---------------------------------------------------------------- TMEM load rate (tcgen05.ld)
 // WPQ warps per lane quarter each load 32x32b.x32 (4 KB) `iters` times at column stride CS
 // (aligned 32 or not), with (WAIT=1) or without a wait per load (WAIT=0: 4 loads per wait).
@@ -476,6 +658,23 @@ int main() {
     run_tmem<4, 1>(32);
     if (getenv("HALO_PROBE_SKIP_SEQ")) return 0;
     // conv1 / conv3 / conv4 geometries of the halo kernel
+    if (getenv("HALO_PROBE_SEQ2")) {
+        run_seq2<0, 2>("kernel form", 208, 34, 280);
+        run_seq2<3, 2>("+ 2 waits per tile", 208, 34, 280);
+        run_seq2<4, 2>("+ 2 commits", 208, 34, 280);
+        run_seq2<5, 2>("+ syncwarp", 208, 34, 280);
+        run_seq2<5, 4>("+ syncwarp", 144, 18, 184);
+        run_seq2<1, 2>("asm per tap", 208, 34, 280);
+        run_seq2<2, 2>("elected lane", 208, 34, 280);
+        run_seq2<0, 4>("kernel form", 144, 18, 184);
+        run_seq2<2, 4>("elected lane", 144, 18, 184);
+        run_seq2<0, 4>("kernel form", 160, 10, 184);
+        run_seq2<2, 4>("elected lane", 160, 10, 184);
+        run_seq2<0, 2>("kernel form", 256, 34, 336);
+        run_seq2<1, 2>("asm per tap", 256, 34, 336);
+        run_seq2<2, 2>("elected lane", 256, 34, 336);
+        return 0;
+    }
     if (getenv("HALO_PROBE_SWEEP")) {
         // LBO (halo rows NH) and K steps per tap, N = 208 / 224 / 256
         for (int N : {208, 256})
