@@ -6,7 +6,7 @@ timeout 1800 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider 
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fused|pack_pixels|logits|pix_|halo|lin4" -c 30 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-sweep --no-configs > /dev/null 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fused|pix_|halo|lin4|logits" -c 9 -o gpurun_out/prof_b256 -f python tools/prof_net.py 256 > gpurun_out/prof.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"fused|pack_pixels|logits|pix_tile|pix_popc|halo4|lin4" -c 30 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-sweep --no-configs > /dev/null 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fused|pix_tile|pix_popc|halo4|lin4|logits" -c 9 -o gpurun_out/prof_b256 -f python tools/prof_net.py 256 > gpurun_out/prof.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/prof.log
 tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/prof.log

@@ -17,7 +17,9 @@ def main(rep, batch):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
     out = {}
-    for i, r in enumerate(rows[2:]):
+    kn = hdr.index("Kernel Name")
+    layer_rows = [r for r in rows[2:] if "prep_" not in r[kn]]  # build-time weight preparation: not a layer
+    for i, r in enumerate(layer_rows[:len(LAYERS)]):
         d = dict(zip(hdr, r))
 
         def num(k):
