@@ -181,7 +181,7 @@ static int run_check(int N, int shift, int ts) {
 // mode 0: TS; mode 1: SS; mode 2: SS while warps 1-3 store 16 B per lane continuously;
 // mode 3: TS with the same store traffic.
 template <int MODE>
-__global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsigned long long* out) {
+__global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsigned long long* out, int M = 128) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsi
     tc_fence_after();
     if (threadIdx.x == 0) {
         const uint32_t b0 = base + 32768 + 16 * shift;
-        const uint32_t idesc = idesc_mxf4(128, N);
+        const uint32_t idesc = idesc_mxf4(M, N);
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             const int k = it & 3;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128, 1) rate(int N, int iters, int shift, unsi
 }
 
 template <int MODE>
-void run_rate(int N, int shift) {
+void run_rate(int N, int shift, int M = 128) {
     unsigned long long* d;
     cudaMalloc(&d, 64);
     cudaMemset(d, 0, 64);
@@ -266,12 +266,12 @@ void run_rate(int N, int shift) {
     auto k = rate<MODE>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 130 * 1024);
     const int iters = 8192;
-    k<<<sms, 128, 130 * 1024>>>(N, 64, shift, d);
+    k<<<sms, 128, 130 * 1024>>>(N, 64, shift, d, M);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k<<<sms, 128, 130 * 1024>>>(N, iters, shift, d);
+    k<<<sms, 128, 130 * 1024>>>(N, iters, shift, d, M);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     float ms;
@@ -281,8 +281,8 @@ void run_rate(int N, int shift) {
     const double cyc = double(h[1]) / iters;
     const double st_bytes = double(h[3] + h[4] + h[5]) * 32 * 16;
     static const char* names[] = {"TS", "SS", "SS+stores", "TS+stores"};
-    printf("rate %-9s N=%3d shift=%d: %6.1f cyc/mma (ideal %5.1f)  %.1f T MAC-ops/s  stores %.1f B/cyc  err=%s\n",
-           names[MODE], N, shift, cyc, N / 2.0, 2.0 * sms * iters * 128.0 * N * 64 / (ms * 1e-3) / 1e12,
+    printf("rate %-9s M=%3d N=%3d shift=%d: %6.1f cyc/mma (ideal at M=128 %5.1f)  %.1f T MAC-ops/s  stores %.1f B/cyc  err=%s\n",
+           names[MODE], M, N, shift, cyc, N / 2.0, 2.0 * sms * iters * double(M) * N * 64 / (ms * 1e-3) / 1e12,
            st_bytes / double(h[1]), cudaGetErrorString(err));
     cudaFree(d);
 }
@@ -649,6 +649,7 @@ void run_tmem(int cs) {
 }
 
 int main() {
+    setvbuf(stdout, nullptr, _IONBF, 0);
     run_tmem<1, 1>(32);
     run_tmem<1, 1>(17);
     run_tmem<2, 1>(32);
@@ -658,6 +659,7 @@ int main() {
     run_tmem<4, 1>(32);
     if (getenv("HALO_PROBE_SKIP_SEQ")) return 0;
     // conv1 / conv3 / conv4 geometries of the halo kernel
+    // (kind::mxf4 with M = 64 is an illegal instruction on sm_100a: run_rate<1>(n, 0, 64) faults)
     if (getenv("HALO_PROBE_SEQ2")) {
         run_seq2<0, 2>("kernel form", 208, 34, 280);
         run_seq2<3, 2>("+ 2 waits per tile", 208, 34, 280);
