@@ -1173,7 +1173,7 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
 // kernel parameter (PixParams): with the channel loops unrolled, every w_d / P_d is a
 // constant-bank operand of the XOR / compare, so a channel costs XOR, POPC, compare, select.
 template <int DW, bool F32, bool POOL>
-__global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 3 : 4) : 8) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
+__global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 2 : 4) : (DW > 6 ? 4 : 6)) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
     // PDL: the next layer may start its prologue (it waits for this grid before reading);
     // this grid waits for the pixel packer's words
     asm volatile("griddepcontrol.launch_dependents;");
@@ -1225,15 +1225,17 @@ __global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 3 : 4) : 8) pix_popc_kern
         uint32_t o[DW];
 #pragma unroll
         for (int w = 0; w < DW; ++w) {
-            uint32_t acc = 0;
+            // bit j of nd = (c > P_d) = the sign of P_d - c (|P_d| <= 33, make_pix_params), shifted
+            // in by a funnel shift: subtract + shift per channel instead of compare + select + or
+            uint32_t nd = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 31; j >= 0; --j) {
                 const int d = 32 * w + j;
                 int c = __popc(xs[0] ^ pp.w[d]);
                 if (POOL) c = min(min(c, __popc(xs[1] ^ pp.w[d])), min(__popc(xs[2] ^ pp.w[d]), __popc(xs[3] ^ pp.w[d])));
-                acc |= c <= pp.p[d] ? (1u << j) : 0u;
+                nd = __funnelshift_l(uint32_t(pp.p[d] - c), nd, 1);
             }
-            o[w] = acc ^ pp.flip[w];
+            o[w] = ~nd ^ pp.flip[w];
         }
         uint32_t* out = g.out_bits + size_t(p) * DW;
         if constexpr (DW % 4 == 0) {
@@ -1296,13 +1298,13 @@ __global__ void __launch_bounds__(256) pix_tile_kernel(const FusedGeom g, const 
         uint32_t o[DW];
 #pragma unroll
         for (int w = 0; w < DW; ++w) {
-            uint32_t acc = 0;
+            uint32_t nd = 0;  // bit j = (popc > P_d), as in pix_popc_kernel
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 31; j >= 0; --j) {
                 const int d = 32 * w + j;
-                acc |= __popc(x ^ pp.w[d]) <= pp.p[d] ? (1u << j) : 0u;
+                nd = __funnelshift_l(uint32_t(pp.p[d] - __popc(x ^ pp.w[d])), nd, 1);
             }
-            o[w] = acc ^ pp.flip[w];
+            o[w] = ~nd ^ pp.flip[w];
         }
         uint32_t* out = g.out_bits + size_t(p0 + int(threadIdx.x)) * DW;
 #pragma unroll
@@ -2214,7 +2216,9 @@ int make_pix_params(const uint32_t* wbits_host, const int4* prm_host, int D, int
     for (int d = 0; d < D; ++d) {
         const int4 e = prm_host[d];  // (Tu, flip, S, bias bits)
         pp->w[d] = wbits_host[d];
-        pp->p[d] = (K + e.z) / 2 - e.x;  // K + S is even
+        // K + S is even; popc is in [0, 32], so clamping to [-1, 33] keeps every decision and
+        // keeps P - popc far from overflow (the kernels take its sign)
+        pp->p[d] = int(std::max<long long>(-1, std::min<long long>(33, (long long)(K + e.z) / 2 - e.x)));
         if (e.y) pp->flip[d / 32] |= 1u << (d % 32);
     }
     return BNN_OK;
