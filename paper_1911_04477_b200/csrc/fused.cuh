@@ -74,7 +74,7 @@ struct HaloGeom {
     int steps, KB4;      // K / 64 MMA steps, 256-element weight blocks
     int wst;             // 0: weights resident in shared memory; else ring slots of streamed blocks
     size_t smem;
-    FastDiv dP, dS, dQ, dWh, dG;
+    FastDiv dP, dS, dQ, dNw, dG;  // dNw: pooled epilogue units (<= 32 columns) per row pair and image
     unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
     const float* in_f32;      // first layer (halo0): float NCHW input, creal channels -> bit words
     int creal;

@@ -469,10 +469,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const int npu = (g.dbg_mode & 1) ? 0 : (g.TR >> 1) * g.G * nwch;
         int i = 0, ts = 0;
         HClock ce;
-        long long t_ld = 0, t_cmp = 0;  // profile: unpooled chunk time in TMEM loads / in total
+        long long t_ld = 0, t_cmp = 0, t_tile = 0, t_tail = 0;  // profile: unpooled chunk time in TMEM loads / in total
         for (int nt = n0; nt < g.n_tiles; nt += nstride, ++i) {
             const int acc = i & 1;
             ce.wait(prof, &tfull[acc], (i >> 1) & 1);
+            const long long th0 = prof ? hclock() : 0;
             tc_fence_after();
             if (prof && i == 0 && warp == 4 && lane == 0) atomicAdd(g.dbg + 9, (unsigned long long)(hclock() - k_main));
             const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g.N);
@@ -511,8 +512,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
             } else {
                 // units: (row pair, image slot, <= 32 columns), alternating between the two warps
                 for (int u = half ^ (i & 1); u < npu; u += 2) {  // first unit alternates per tile
-                    const int ch = u % nwch, t2 = u / nwch;
-                    const int slot = t2 % g.G, ir = 2 * (t2 / g.G);
+                    // (no integer division by runtime values: ~30 instructions each)
+                    const int t2 = g.dNw.div(u), ch = u - t2 * nwch;
+                    const int ti = g.dG.div(t2), slot = t2 - ti * g.G, ir = 2 * ti;
                     const int r = r0 + ir, grp = g.dS.div(r), h = r - grp * g.S;
                     const int b = grp * g.G + slot;
                     if (h >= g.H || b >= g.B) continue;  // frame rows, images past the batch (warp-uniform)
@@ -520,6 +522,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     const uint32_t taddr = tb + uint32_t(ir * g.P + slot * g.Q + w0);
                     uint32_t* dst = g.out + (size_t(b * Hh + (h >> 1)) * Wh + (w0 >> 1)) * g.Dw + oword;
                     const uint32_t pitch = uint32_t(g.P);
+                    const long long c0 = prof ? hclock() : 0;
                     switch (wn) {
                         case 32: pool_unit<32>(taddr, pitch, Tf, flip, lane, dst, size_t(g.Dw), wvalid); break;
                         case 16: pool_unit<16>(taddr, pitch, Tf, flip, lane, dst, size_t(g.Dw), wvalid); break;
@@ -527,17 +530,22 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         case 4: pool_unit<4>(taddr, pitch, Tf, flip, lane, dst, size_t(g.Dw), wvalid); break;
                         default: pool_unit<2>(taddr, pitch, Tf, flip, lane, dst, size_t(g.Dw), wvalid); break;
                     }
+                    if (prof) t_cmp += hclock() - c0, ++t_ld;  // pooled: unit time, unit count
                 }
             }
+            const long long tt0 = prof ? hclock() : 0;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM reads of this tile done
+            if (prof) t_tile += tt0 - th0, t_tail += hclock() - tt0;
         }
         if (prof && warp == 4 && lane == 0) {
             atomicAdd(g.dbg + 6, (unsigned long long)ce.acc);
             atomicAdd(g.dbg + 7, (unsigned long long)(hclock() - k_main));
             atomicAdd(g.dbg + 10, (unsigned long long)t_ld);
             atomicAdd(g.dbg + 11, (unsigned long long)t_cmp);
+            atomicAdd(g.dbg + 16, (unsigned long long)t_tile);
+            atomicAdd(g.dbg + 17, (unsigned long long)t_tail);
         }
     } else if (warp == 2 || warp == 3 || warp == 12 || warp >= 14) {
         // halo producers: canvas pixel j of the tile -> its Cw words (or the all-ones frame word)
@@ -715,7 +723,7 @@ bool halo4_plan(const FusedGeom& fg, HaloGeom& h) {
         h.toff[t] = t < h.taps ? (ky - fg.PH + 1) * h.P + (kx - fg.PW + 1) : 0;
     }
     h.smem = 1024 + size_t(h.wst ? h.wst : KB4) * 16384 + size_t(h.nst) * fg.Cw * h.NH * 16 + kHTail;
-    h.dWh = FastDiv::make(uint32_t(std::max(1, fg.W / 2)));
+    h.dNw = FastDiv::make(uint32_t((fg.W + 31) / 32));
     h.dG = FastDiv::make(uint32_t(h.G));
     h.dbg = nullptr;
     h.dbg_mode = 0;
@@ -788,23 +796,23 @@ int launch_halo4(const CUtensorMap& tm4, const HaloGeom& h, cudaStream_t s) {
     } else {  // synchronous, not capturable: tools only
         HaloGeom hp = h;
         hp.dbg_mode = atoi(getenv("BNN_HALO_PROFILE")) >> 1;
-        BNN_CUDA(cudaMalloc(&hp.dbg, 16 * sizeof(unsigned long long)));
-        unsigned long long init[16] = {};
+        BNN_CUDA(cudaMalloc(&hp.dbg, 24 * sizeof(unsigned long long)));
+        unsigned long long init[24] = {};
         init[14] = ~0ull;
         BNN_CUDA(cudaMemcpy(hp.dbg, init, sizeof init, cudaMemcpyHostToDevice));
         BNN_CUDA(cudaLaunchKernelEx(&cfg, h.wst ? halo4_kernel<true> : halo4_kernel<false>, tm4, hp));
         BNN_TRY(launch_check("halo4_kernel"));
-        unsigned long long d[16];
+        unsigned long long d[24];
         BNN_CUDA(cudaMemcpy(d, hp.dbg, sizeof d, cudaMemcpyDeviceToHost));
         cudaFree(hp.dbg);
         const double n = h.grid, k = 1e3;
         fprintf(stderr,
                 "[halo4 mode=%d B=%d H=%d W=%d C=%d D=%d pool=%d | G=%d P=%d TR=%d N=%d NH=%d nst=%d tiles=%d grid=%d] "
                 "span %.1f us | per-CTA kcyc: setup %.1f, total %.1f | mma: wait-w %.1f wait-acc %.1f wait-halo %.1f "
-                "busy-total %.1f | prod: wait %.1f total %.1f | epi: wait %.1f total %.1f (unpooled chunks: ld %.1f all %.1f) | first halo %.1f first acc %.1f\n",
+                "busy-total %.1f | prod: wait %.1f total %.1f | epi: wait %.1f total %.1f (chunks: ld %.1f all %.1f; pooled: units, all; tile body %.1f tail %.1f) | first halo %.1f first acc %.1f\n",
                 hp.dbg_mode, h.B, h.H, h.W, h.Cw * 32, h.D, h.pool, h.G, h.P, h.TR, h.N, h.NH, h.nst, h.n_tiles, h.grid,
                 (d[15] - d[14]) / 1e3, d[12] / n / k, d[13] / n / k, d[0] / n / k, d[1] / n / k, d[2] / n / k,
-                d[3] / n / k, d[4] / n / k, d[5] / n / k, d[6] / n / k, d[7] / n / k, d[10] / n / k, d[11] / n / k, d[8] / n / k, d[9] / n / k);
+                d[3] / n / k, d[4] / n / k, d[5] / n / k, d[6] / n / k, d[7] / n / k, d[10] / n / k, d[11] / n / k, d[16] / n / k, d[17] / n / k, d[8] / n / k, d[9] / n / k);
     }
     set_last_gemm("halo4_kernel");
     return BNN_OK;
