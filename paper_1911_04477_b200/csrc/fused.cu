@@ -1328,7 +1328,16 @@ __global__ void logits_popc_kernel(const uint32_t* __restrict__ act, int Kw, int
     const uint4* x4 = reinterpret_cast<const uint4*>(act + size_t(b) * Kw);
     const uint4* w4 = reinterpret_cast<const uint4*>(wbits + size_t(d) * Kw);
     int acc = 0;
-    if ((Kw & 3) == 0) {
+    if ((Kw & 3) == 0 && Kw <= 64) {  // every word's load in flight before the first popcount
+        uint4 xv[16], wv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (4 * q < Kw) xv[q] = __ldg(x4 + q), wv[q] = __ldg(w4 + q);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (4 * q < Kw)
+                acc += __popc(xv[q].x ^ wv[q].x) + __popc(xv[q].y ^ wv[q].y) + __popc(xv[q].z ^ wv[q].z) + __popc(xv[q].w ^ wv[q].w);
+    } else if ((Kw & 3) == 0) {
         for (int q = 0; q < Kw / 4; ++q) {
             const uint4 x = __ldg(x4 + q), w = __ldg(w4 + q);
             acc += __popc(x.x ^ w.x) + __popc(x.y ^ w.y) + __popc(x.z ^ w.z) + __popc(x.w ^ w.w);
