@@ -507,9 +507,39 @@ def measure_configs(lib, dev, st, flush, seed, peaks, cpu, world, rank):
                              "tcgen05_mxf4": peaks.get("probe", {}).get("tcgen05_mxf4_tops"),
                              "chosen": "tcgen05 kind::mxf4 (e2m1 operands, exact) for the packed-input convs "
                                        "(halo4 / swap4), the linear layers (lin4) and the standalone xnor_gemm "
-                                       "above 2^26 bit-MACs (xnor4); LOP3+POPC below it and for the pixel-input "
+                                       "above 2^26 bit-MACs (xnor4; xnor4t, TMA-fed, above 2^32); LOP3+POPC below it and for the pixel-input "
                                        "first conv and the logits",
                              "ncu_pipe_counters": "profiles/r02_k3_pipes_ncu.json"}
+
+    # K3 on large GEMMs (the north star's ">= 50 % of the chosen pipe's peak for large GEMMs"):
+    # standalone xnor_gemm (s32 output, the reference's IntMatrix) through the C ABI, AUTO policy
+    # (the TMA-fed FP4 kernel, operands expanded once into HBM scratch inside the call)
+    lg = {}
+    for (Mg, Ng, Lg) in ((8192, 8192, 8192), (4096, 1024, 9216)):
+        wplg = Lg // 32
+        wg = torch.randint(-2**31, 2**31 - 1, (Mg, wplg), dtype=torch.int32, device=dev)
+        xg = torch.randint(-2**31, 2**31 - 1, (Ng, wplg), dtype=torch.int32, device=dev)
+        og = torch.empty((Mg, Ng), dtype=torch.int32, device=dev)
+        fg = lambda: _lib.check(lib.bnn_xnor_gemm_s32(wg.data_ptr(), wplg, xg.data_ptr(), wplg, Mg, Ng, Lg,
+                                                      og.data_ptr(), Ng, S))
+        msg = _dev_time(fg, st, flush, 10)
+        kern = lib.bnn_last_gemm_kernel().decode()
+        tops = 2.0 * Mg * Ng * Lg / (msg * 1e-3) / 1e12
+        e = {"ms": msg, "binary_tops": tops, "frac_of_fp4_peak": tops / fp4_peak, "kernel": kern}
+        got = og.clone()
+        _lib.check(lib.bnn_set_gemm_policy(1))  # the integer-pipe kernel on the same operands
+        fg()
+        _lib.check(lib.bnn_set_gemm_policy(0))
+        st.synchronize()
+        e["equal_to_popc_kernel"] = bool(torch.equal(got, og))
+        if ref is not None:  # a 256 x 256 corner against the unmodified reference
+            wh = wg[:256].cpu().numpy().view(np.uint32)
+            xh = xg[:256].cpu().numpy().view(np.uint32)
+            e["corner_parity_vs_reference"] = bool(np.array_equal(got[:256, :256].cpu().numpy(),
+                                                                  ref.xnor_gemm(wh, xh, Lg, threads=cores)))
+        lg[f"{Mg}x{Ng}x{Lg}"] = e
+        del wg, xg, og, got
+    out["k3_large_gemm"] = lg
     return out
 
 

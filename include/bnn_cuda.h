@@ -55,10 +55,11 @@ int bnn_version(void);
  * ("popc", "xnor4_kernel", ...); for tests and the benchmark. */
 const char* bnn_last_gemm_kernel(void);
 /* K3 kernel selection (process-wide). AUTO picks the integer-pipe kernel below ~2^26
- * bit-MACs and the tcgen05 FP4 tensor-core kernel (operands expanded from the packed bits in
- * shared memory) above ("K3 candidates"); POPC / UMMA force one of them (used by the
- * parity tests to cover both). */
-enum { BNN_GEMM_AUTO = 0, BNN_GEMM_POPC = 1, BNN_GEMM_UMMA = 2 };
+ * bit-MACs, the tcgen05 FP4 tensor-core kernel with operands expanded from the packed bits in
+ * shared memory up to ~2^32, and above that the FP4 kernel fed by TMA from operands expanded
+ * once to e2m1 in HBM scratch ("K3 candidates"); POPC / UMMA / UMMA_TMA force one of
+ * them (used by the parity tests to cover all three). */
+enum { BNN_GEMM_AUTO = 0, BNN_GEMM_POPC = 1, BNN_GEMM_UMMA = 2, BNN_GEMM_UMMA_TMA = 3 };
 int bnn_set_gemm_policy(int policy);
 
 /* ConvGeometry (tensor.hpp:101-111), same field order. */
@@ -324,7 +325,9 @@ int bnn_set_fused_halo0(int enabled);
 /* Fused engine: linear layers on the FP4 tensor-core kernel (lin4_kernel: e2m1 weights by TMA,
  * packed input bits expanded in shared memory, K split over CTAs with an exact integer
  * reduction in lin_finish_kernel) instead of the int8 fused_layer_kernel. 0 off, 1 (default)
- * on. Bit-exact either way. */
+ * on; the images are TMA-loaded from an e2m1 copy expanded once per layer (expand_act4_kernel)
+ * when many feature tiles share them (>= 4 tiles, batch >= 512), else expanded by the producer
+ * warps of every CTA; 2 / 3 force one of the two. Bit-exact either way. */
 int bnn_set_fused_lin4(int enabled);
 /* Fused engine: FP4 swapped conv on CTA pairs (cta_group::2, 256 channels per pair: each SM
  * expands half the activation rows) for layers with >= 256 channels: 0 off, 1 (default) on.

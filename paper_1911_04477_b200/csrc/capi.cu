@@ -94,6 +94,10 @@ int xnor4_gemm_s32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, siz
                    cudaStream_t);
 int xnor4_gemm_f32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, const float*, size_t,
                    float*, cudaStream_t);
+int xnor4t_gemm_s32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, int32_t*, size_t,
+                    cudaStream_t);
+int xnor4t_gemm_f32(const uint32_t*, size_t, const uint32_t*, size_t, size_t, size_t, size_t, const float*, size_t,
+                    float*, cudaStream_t);
 
 namespace {
 int g_policy = BNN_GEMM_AUTO;
@@ -104,8 +108,17 @@ int g_policy = BNN_GEMM_AUTO;
 // profiles/r02_gemm_crossover.jsonl).
 bool use_umma(size_t M, size_t N, size_t L) {
     if (g_policy == BNN_GEMM_POPC) return false;
-    if (g_policy == BNN_GEMM_UMMA) return true;
+    if (g_policy == BNN_GEMM_UMMA || g_policy == BNN_GEMM_UMMA_TMA) return true;
     return double(M) * double(N) * double(L) >= 67108864.0;
+}
+// Among the tensor-core kernels: the TMA-fed one (operands expanded once into HBM) for the
+// large products, where the in-CTA expansion is the bound (measured crossover in
+// profiles/r02_gemm_crossover_t.jsonl).
+bool use_tma(size_t M, size_t N, size_t L) {
+    if (g_policy == BNN_GEMM_UMMA_TMA) return true;
+    if (g_policy != BNN_GEMM_AUTO) return false;
+    // M = 128 x 262144 positions: one weight tile, every line expanded once anyway
+    return double(M) * double(N) * double(L) >= 4294967296.0 && M >= 512 && N >= 512;
 }
 }  // namespace
 
@@ -114,7 +127,9 @@ bool use_umma(size_t M, size_t N, size_t L) {
 int gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N,
              size_t L, int32_t* out, size_t ldo, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
-    if (use_umma(M, N, L)) return xnor4_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
+    if (use_umma(M, N, L))
+        return use_tma(M, N, L) ? xnor4t_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s)
+                                : xnor4_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
     return popc_gemm_s32(w, ldw, x, ldx, M, N, L, out, ldo, s);
 }
 
@@ -122,7 +137,9 @@ int gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_
              size_t L, const float* bias, size_t P, float* out, cudaStream_t s) {
     BNN_TRY(check_gemm_args(ldw, ldx, M, N, L));
     if (P == 0 || N % P != 0) return fail(BNN_E_SHAPE, "xnor_gemm: N must be a multiple of P");
-    if (use_umma(M, N, L)) return xnor4_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
+    if (use_umma(M, N, L))
+        return use_tma(M, N, L) ? xnor4t_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s)
+                                : xnor4_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
     return popc_gemm_f32(w, ldw, x, ldx, M, N, L, bias, P, out, s);
 }
 
@@ -176,7 +193,7 @@ int bnn_version(void) { return 1; }
 const char* bnn_last_gemm_kernel(void) { return g_last_gemm; }
 
 int bnn_set_gemm_policy(int policy) {
-    if (policy < BNN_GEMM_AUTO || policy > BNN_GEMM_UMMA) return fail(BNN_E_CONFIG, "bad GEMM policy");
+    if (policy < BNN_GEMM_AUTO || policy > BNN_GEMM_UMMA_TMA) return fail(BNN_E_CONFIG, "bad GEMM policy");
     g_policy = policy;
     return BNN_OK;
 }

@@ -22,7 +22,9 @@ constexpr int kColsWordsPerBlock = 8;
 
 // STRICT = false: bit = (v >= 0)        -> pack_rows(sign(x))
 // STRICT = true : bit = (v == +1), any v not in {+1,-1} records its row-major index
-template <bool STRICT>
+// E2M1 = true: each word is written as the 16 bytes of e2m1 {0, 1.0} codes the fused engine's
+// TMA-fed linear kernel reads (expand_act4_kernel's format) to `words` viewed as uint4 [D, wpl].
+template <bool STRICT, bool E2M1 = false>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict__ x, size_t D,
                                                         size_t L, uint32_t* __restrict__ words,
                                                         size_t ld, size_t wpl,
@@ -55,7 +57,13 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict_
         const uint32_t wbits = __ballot_sync(0xffffffffu, bit);
         if (lane == j) mine = wbits;
     }
-    if (k0 + lane < wpl) words[row * ld + k0 + lane] = mine;
+    if (k0 + lane < wpl) {
+        if (E2M1)
+            reinterpret_cast<uint4*>(words)[row * wpl + k0 + lane] =
+                make_uint4((mine << 1) & 0x22222222u, mine & 0x22222222u, (mine >> 1) & 0x22222222u, (mine >> 2) & 0x22222222u);
+        else
+            words[row * ld + k0 + lane] = mine;
+    }
 }
 
 template <bool STRICT>
@@ -195,6 +203,17 @@ int launch_pack_rows(const float* x, size_t D, size_t L, uint32_t* words, size_t
         pack_rows_kernel<true><<<blocks, 256, 0, s>>>(x, D, L, words, ld, wpl, first_bad);
     else
         pack_rows_kernel<false><<<blocks, 256, 0, s>>>(x, D, L, words, ld, wpl, nullptr);
+    return launch_check("pack_rows_kernel");
+}
+
+// pack_rows(sign(x)) written as e2m1 lines [D, wpl * 16 bytes] (the fused engine's first linear
+// layer when its images are TMA-loaded: one pass instead of pack_rows + expand_act4).
+int launch_pack_rows_e2m1(const float* x, size_t D, size_t L, void* out4, cudaStream_t s) {
+    if (D == 0 || L == 0) return fail(BNN_E_SHAPE, "pack_rows: extents must be >= 1");
+    const size_t wpl = wpl_of(L);
+    const size_t warps = D * ceil_div(wpl, 32);
+    const unsigned blocks = unsigned(ceil_div(warps * 32, 256));
+    pack_rows_kernel<false, true><<<blocks, 256, 0, s>>>(x, D, L, static_cast<uint32_t*>(out4), wpl, wpl, nullptr);
     return launch_check("pack_rows_kernel");
 }
 

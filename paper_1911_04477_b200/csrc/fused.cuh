@@ -110,11 +110,17 @@ struct LinGeom {
     unsigned* sem;
     unsigned long long* dbg;  // BNN_LIN4_PROFILE phase stamps, else null
     unsigned long long* tl;   // timeline stamps (bnn_debug_timeline), [grid][4], else null
+    int tmab;                 // 1: images TMA-loaded from in4 (expanded once by expand_act4), no producers
+    uint8_t* in4;             // [B, Kw * 16] e2m1 images when tmab
 };
 bool lin4_plan(const FusedGeom& g, int epi, LinGeom& l);
+// Images [B, Kw] packed bits -> e2m1 {0, 1.0} lines [B, Kw * 16 bytes] in put_word4's order.
+int launch_expand_act4(const LinGeom& l, cudaStream_t s);
+// -1 auto (by size), 0 producer-expanded images, 1 TMA-loaded images (bnn_set_fused_lin4 1 / 3 / 2)
+void set_lin4_tma(int mode);
 size_t lin4_ws_bytes(const LinGeom& l);
 size_t lin4_sem_count(const LinGeom& l);
-int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s);
+int launch_lin4(const CUtensorMap& tm4, const CUtensorMap& tmx, const LinGeom& l, cudaStream_t s);
 
 // Debug timeline (globaltimer stamps per CTA and launch): op 1 enable + reset, 2 print + disable.
 int fused_timeline(int op);

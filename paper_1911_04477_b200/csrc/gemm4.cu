@@ -19,9 +19,13 @@
 #include "bnn_common.cuh"
 #include "umma.cuh"
 
+#include <cuda.h>
+
 namespace bnnk {
 
 using namespace umma;
+
+int make_tmap_2d_s8(CUtensorMap* map, const void* base, size_t rows, size_t K, size_t ld, uint32_t box_rows);
 
 namespace {
 
@@ -43,6 +47,7 @@ struct G4 {
     float* out_f32;      // [N / P][M][P] (f32 epilogue: float(acc) + bias[m])
     const float* bias;
     int P;
+    int accs;  // TMEM accumulators (xnor4t_kernel)
 };
 
 __host__ __device__ constexpr uint32_t idesc_mxf4_m128(int N) {
@@ -83,6 +88,44 @@ __device__ __forceinline__ void load_block(const uint32_t* base, size_t ld, int 
         w[k] = (live && q < Lw) ? __ldg(src + q) : 0u;
         const int nv = L - 32 * q;  // valid elements in word q
         m[k] = !live || nv <= 0 ? 0u : nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+    }
+}
+
+// Epilogue of one 128 x NB tile: lane = output row m, TMEM columns from tb = output columns
+// n0 + c. s32 output [M, ldo], or to_float + bias_add scattered to [N / P][M][P].
+__device__ __forceinline__ void store_tile(const G4& g, uint32_t tb, int m, int n0) {
+    const float bv = (g.out_f32 && g.bias && m < g.M) ? __ldg(g.bias + m) : 0.0f;
+    for (int c = 0; c < (g.NB + 31) / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tb + uint32_t(32 * c), v);
+        tmem_ld_wait();
+        if (m >= g.M) continue;
+        const int nb = n0 + 32 * c;
+        if (g.out_s32) {
+            int32_t* orow = g.out_s32 + size_t(m) * g.ldo + nb;
+            const bool vec = nb + 32 <= g.N && 32 * c + 32 <= g.NB && (g.ldo & 3) == 0 &&
+                             ((reinterpret_cast<uintptr_t>(g.out_s32) & 15) == 0);
+            if (vec) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<int4*>(orow + j) =
+                        make_int4(int(__uint_as_float(v[j])), int(__uint_as_float(v[j + 1])),
+                                  int(__uint_as_float(v[j + 2])), int(__uint_as_float(v[j + 3])));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (nb + j < g.N && 32 * c + j < g.NB) orow[j] = int(__uint_as_float(v[j]));
+            }
+        } else {
+            // to_float (exact: |acc| < 2^24) + bias_add, scattered to [img][m][p]
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const int n = nb + j;
+                if (n >= g.N || 32 * c + j >= g.NB) break;
+                const int img = n / g.P, p = n - img * g.P;
+                g.out_f32[(size_t(img) * g.M + m) * g.P + p] = __fadd_rn(__uint_as_float(v[j]), bv);
+            }
+        }
     }
 }
 
@@ -168,40 +211,7 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
             const int m = mt * 128 + q * 32 + lane, n0 = nt * g.NB;
             mbar_wait(tfull, i & 1);
             tc_fence_after();
-            const uint32_t tb = tmem_base + (uint32_t(q * 32) << 16);
-            const float bv = (g.out_f32 && g.bias && m < g.M) ? __ldg(g.bias + m) : 0.0f;
-            for (int c = 0; c < (g.NB + 31) / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld32(tb + uint32_t(32 * c), v);
-                tmem_ld_wait();
-                if (m >= g.M) continue;
-                const int nb = n0 + 32 * c;
-                if (g.out_s32) {
-                    int32_t* orow = g.out_s32 + size_t(m) * g.ldo + nb;
-                    const bool vec = nb + 32 <= g.N && 32 * c + 32 <= g.NB && (g.ldo & 3) == 0 &&
-                                     ((reinterpret_cast<uintptr_t>(g.out_s32) & 15) == 0);
-                    if (vec) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<int4*>(orow + j) =
-                                make_int4(int(__uint_as_float(v[j])), int(__uint_as_float(v[j + 1])),
-                                          int(__uint_as_float(v[j + 2])), int(__uint_as_float(v[j + 3])));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (nb + j < g.N && 32 * c + j < g.NB) orow[j] = int(__uint_as_float(v[j]));
-                    }
-                } else {
-                    // to_float (exact: |acc| < 2^24) + bias_add, scattered to [img][m][p]
-#pragma unroll 4
-                    for (int j = 0; j < 32; ++j) {
-                        const int n = nb + j;
-                        if (n >= g.N || 32 * c + j >= g.NB) break;
-                        const int img = n / g.P, p = n - img * g.P;
-                        g.out_f32[(size_t(img) * g.M + m) * g.P + p] = __fadd_rn(__uint_as_float(v[j]), bv);
-                    }
-                }
-            }
+            store_tile(g, tmem_base + (uint32_t(q * 32) << 16), m, n0);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
@@ -247,6 +257,214 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+}
+
+// ---------------------------------------------------------------- large GEMMs: TMA-fed operands
+//
+// Above ~2^32 bit-MACs the in-CTA expansion above is the bound: every CTA re-expands its A and B
+// lines for every tile, and the producers' shared-memory stores compete with the MMA's operand
+// reads. For those products both operands are expanded ONCE into HBM scratch (expand4_kernel:
+// 4 B of packed bits -> 16 B of e2m1, the same element order and codes as put_pm1, 0x0 past L),
+// and xnor4t_kernel streams them with TMA (SWIZZLE_128B, the layout put_pm1 writes by hand; rows
+// past M / N and bytes past the line are zero-filled by TMA, i.e. e2m1 0.0, the pad value).
+//
+// CTA anatomy (192 threads): warp 0 TMA producer (one lane), warp 1 TMEM allocator + MMA issuer,
+// warps 2-5 epilogue. Two accumulators in TMEM (columns 0 and 256, NB <= 240; the block scales
+// at 496) so the epilogue of tile i overlaps the MMAs of tile i + 1.
+
+constexpr int kTThreads = 192;
+
+// Packed lines [rows, ld words] (L valid bits each) -> e2m1 lines [rows, Lw * 16 bytes].
+__global__ void __launch_bounds__(256) expand4_kernel(const uint32_t* __restrict__ src, size_t ld, size_t rows, int Lw,
+                                                      int L, uint4* __restrict__ dst) {
+    const size_t total = rows * size_t(Lw);
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = i / size_t(Lw);
+        const int q = int(i - r * size_t(Lw));
+        const uint32_t b = __ldg(src + r * ld + q);
+        const int nv = L - 32 * q;
+        const uint32_t m = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
+        uint32_t o[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const uint32_t xs = (b >> s) & 0x11111111u, ms = (m >> s) & 0x11111111u;
+            o[s] = (ms << 1) | ((ms & ~xs) << 3);
+        }
+        dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__global__ void __launch_bounds__(kTThreads, 1)
+    xnor4t_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                  const __grid_constant__ G4 g) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const int nst = g.nst;
+    uint8_t* sA = smem_raw + (base - raw);   // [nst][128 x 128 B]
+    uint8_t* sB = sA + size_t(nst) * 16384;  // [nst][NB x 128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(nst) * g.NB * 128);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kGMaxStages;
+    uint64_t* tfull = bars + 2 * kGMaxStages;  // [2]
+    uint64_t* tempty = tfull + 2;              // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
+    const int units = g.m_tiles * g.n_tiles;
+    const uint32_t stage_tx = 16384u + uint32_t(g.NB) * 128u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tA);
+        tma_prefetch(&tB);
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = warp_uniform(*tmem_slot);
+    if (warp >= 2) {  // block scales: every byte of columns [496, 512) = 2^0
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+        const uint32_t lb = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
+        tmem_st8(lb + kGSfCol, v);
+        tmem_st8(lb + kGSfCol + 8, v);
+        tmem_st_wait();
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+                for (int kb = 0; kb < g.KB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], stage_tx);
+                    tma_load_2d(&tA, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
+                    tma_load_2d(&tB, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
+                    if (++stage == nst) stage = 0, phase ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        const uint32_t idesc = idesc_mxf4_m128(g.NB);
+        int stage = 0, i = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            const int acc = g.accs == 2 ? (i & 1) : 0, use = g.accs == 2 ? (i >> 1) : i;
+            const uint32_t d = tmem_base + uint32_t(acc * 256);
+            mbar_wait(&tempty[acc], (use & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < g.KB; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sA + size_t(stage) * 16384);
+                const uint32_t b0 = smem_u32(sB + size_t(stage) * g.NB * 128);
+                const int nk = min(4, (g.L - 256 * kb + 63) / 64);  // 64-element steps with data
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (k >= nk) break;
+                    mma_mxf4_w(d, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc, tmem_base + kGSfCol,
+                               (kb != 0 || k != 0));
+                }
+                mma_commit_w(&empty[stage]);
+                if (kb == g.KB - 1) mma_commit_w(&tfull[acc]);
+                __syncwarp();
+                if (++stage == nst) stage = 0, phase ^= 1;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        int i = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+            const int acc = g.accs == 2 ? (i & 1) : 0, use = g.accs == 2 ? (i >> 1) : i;
+            const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+            mbar_wait(&tfull[acc], use & 1);
+            tc_fence_after();
+            store_tile(g, tmem_base + uint32_t(acc * 256) + (uint32_t(q * 32) << 16), mt * 128 + q * 32 + lane,
+                       nt * g.NB);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// Tile width for the TMA kernel: NB in [16, 240] (multiple of 16, two accumulators) minimising
+// waves x (NB + per-tile overhead) over the SMs; never wider than N needs.
+int pick_nb_t(int m_tiles, int N, int sms) {
+    const int n16 = (N + 15) / 16 * 16;
+    int best = std::min(240, n16);
+    double best_cost = 1e300;
+    for (int nb = std::min(240, n16); nb >= 16; nb -= 16) {
+        const long units = long(m_tiles) * ((N + nb - 1) / nb);
+        const long waves = (units + sms - 1) / sms;
+        const double cost = double(waves) * (nb + 40);
+        if (cost < best_cost * 0.999) best_cost = cost, best = nb;
+    }
+    return best;
+}
+
+int launch_xnor4t(G4 g, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        BNN_CUDA(cudaFuncSetAttribute(xnor4t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGSmemMax)));
+        attr_set = true;
+    }
+    g.Lw = (g.L + 31) / 32;
+    g.KB = (g.L + 255) / 256;
+    g.m_tiles = (g.M + 127) / 128;
+    const int sms = num_sms();
+    g.NB = pick_nb_t(g.m_tiles, g.N, sms);
+    g.accs = 2;
+    g.n_tiles = (g.N + g.NB - 1) / g.NB;
+    g.nst = int(std::min<size_t>(kGMaxStages, (kGSmemMax - 1024 - 256) / (16384 + size_t(g.NB) * 128)));
+    // operands expanded once to e2m1 in stream-ordered scratch, 16 B per packed word
+    const size_t lb = size_t(g.Lw) * 16;
+    Scratch ea, eb;
+    BNN_TRY(ea.alloc(size_t(g.M) * lb, s));
+    BNN_TRY(eb.alloc(size_t(g.N) * lb, s));
+    const int eg = sms * 8;
+    expand4_kernel<<<eg, 256, 0, s>>>(g.w, g.ldw, size_t(g.M), g.Lw, g.L, ea.as<uint4>());
+    expand4_kernel<<<eg, 256, 0, s>>>(g.x, g.ldx, size_t(g.N), g.Lw, g.L, eb.as<uint4>());
+    BNN_TRY(launch_check("expand4_kernel"));
+    CUtensorMap ta, tb;
+    BNN_TRY(make_tmap_2d_s8(&ta, ea.p, size_t(g.M), lb, lb, 128));
+    BNN_TRY(make_tmap_2d_s8(&tb, eb.p, size_t(g.N), lb, lb, uint32_t(g.NB)));
+    const int units = g.m_tiles * g.n_tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min(units, sms)));
+    cfg.blockDim = dim3(unsigned(kTThreads));
+    cfg.dynamicSmemBytes = 1024 + size_t(g.nst) * (16384 + size_t(g.NB) * 128) + 256;
+    cfg.stream = s;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, xnor4t_kernel, ta, tb, g));
+    set_last_gemm("xnor4t_kernel");
+    return launch_check("xnor4t_kernel");
 }
 
 int launch_xnor4(G4 g, cudaStream_t s) {
@@ -303,6 +521,25 @@ int xnor4_gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx,
     g.w = w, g.ldw = ldw, g.x = x, g.ldx = ldx, g.M = int(M), g.N = int(N), g.L = int(L);
     g.out_f32 = out, g.bias = bias, g.P = int(P ? P : N);
     return launch_xnor4(g, s);
+}
+
+// The same two products on the TMA-fed kernel (operands expanded once to e2m1 in HBM scratch).
+int xnor4t_gemm_s32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N, size_t L,
+                    int32_t* out, size_t ldo, cudaStream_t s) {
+    if (M == 0 || N == 0) return BNN_OK;
+    G4 g{};
+    g.w = w, g.ldw = ldw, g.x = x, g.ldx = ldx, g.M = int(M), g.N = int(N), g.L = int(L);
+    g.out_s32 = out, g.ldo = ldo, g.P = 1;
+    return launch_xnor4t(g, s);
+}
+
+int xnor4t_gemm_f32(const uint32_t* w, size_t ldw, const uint32_t* x, size_t ldx, size_t M, size_t N, size_t L,
+                    const float* bias, size_t P, float* out, cudaStream_t s) {
+    if (M == 0 || N == 0) return BNN_OK;
+    G4 g{};
+    g.w = w, g.ldw = ldw, g.x = x, g.ldx = ldx, g.M = int(M), g.N = int(N), g.L = int(L);
+    g.out_f32 = out, g.bias = bias, g.P = int(P ? P : N);
+    return launch_xnor4t(g, s);
 }
 
 }  // namespace bnnk

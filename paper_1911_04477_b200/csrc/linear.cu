@@ -78,7 +78,8 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }  // namespace
 
 __global__ void __launch_bounds__(kLThreads, 1)
-    lin4_kernel(const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ LinGeom g) {
+    lin4_kernel(const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ CUtensorMap tmX4,
+                const __grid_constant__ LinGeom g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -103,8 +104,9 @@ __global__ void __launch_bounds__(kLThreads, 1)
     };
     if (threadIdx.x == 0) {
         tma_prefetch(&tmW4);
+        if (g.tmab) tma_prefetch(&tmX4);
         for (int s = 0; s < nst; ++s) {
-            mbar_init(&full[s], 1 + 8);  // TMA arrive (expect_tx) + 8 producer warps
+            mbar_init(&full[s], g.tmab ? 1 : 1 + 8);  // TMA arrive (expect_tx) [+ 8 producer warps]
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
@@ -144,18 +146,24 @@ __global__ void __launch_bounds__(kLThreads, 1)
     };
 
     if (warp == 0) {
-        // weights: build-time constants, loaded ahead of the grid dependency
+        // weights: build-time constants, loaded ahead of the grid dependency (with TMA-loaded
+        // images: the first ring's weights, then the wait, then both operands)
         if (lane == 0) {
-            int stage = 0;
+            int stage = 0, issued = 0;
             uint32_t phase = 0;
+            const uint32_t btx = g.tmab ? uint32_t(g.NB) * 128u : 0u;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int mt, nt, ks, kb0, kb1;
                 decode(u, mt, nt, ks);
                 kb_range(ks, kb0, kb1);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], 16384);
+                    mbar_arrive_expect_tx(&full[stage], 16384 + btx);
                     tma_load_2d(&tmW4, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
+                    if (g.tmab) {
+                        if (issued == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+                        tma_load_2d(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
+                    }
                     if (++stage == nst) stage = 0, phase ^= 1;
                 }
             }
@@ -233,11 +241,18 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     // to_float(a) + bias (kernels.cpp:90-107): one rounding of an exact integer
                     if (dvalid) {
                         const float bias = __int_as_float(pd.w);
+                        float* orow = g.out_f32 + size_t(d) * g.ldo + bc;
+                        auto val = [&](int j) { return __fadd_rn(__int2float_rn(2 * int(__uint_as_float(v[j])) - pd.z), bias); };
+                        if (bc + 32 <= g.B && 32 * c + 32 <= g.NB && (g.ldo & 3) == 0 &&
+                            (reinterpret_cast<uintptr_t>(g.out_f32) & 15) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (bc + j < g.B && 32 * c + j < g.NB)
-                                g.out_f32[size_t(d) * g.ldo + bc + j] =
-                                    __fadd_rn(__int2float_rn(2 * int(__uint_as_float(v[j])) - pd.z), bias);
+                            for (int j = 0; j < 32; j += 4)  // 16-byte stores: a quarter of the store instructions
+                                *reinterpret_cast<float4*>(orow + j) = make_float4(val(j), val(j + 1), val(j + 2), val(j + 3));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (bc + j < g.B && 32 * c + j < g.NB) orow[j] = val(j);
+                        }
                     }
                 }
             }
@@ -247,7 +262,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
             if (warp == 2 && lane == 0) stamp(5);
         }
         if (g.ksplit > 1) __threadfence();  // partial sums visible GPU-wide before the arrival
-    } else {
+    } else if (!g.tmab) {
         // producers: thread = image row r of the tile; per 256-element K block its 8 packed words
         asm volatile("griddepcontrol.wait;" ::: "memory");
         const int r = int(threadIdx.x) - 6 * 32;  // 0..255
@@ -369,6 +384,36 @@ __global__ void __launch_bounds__(kLThreads, 1)
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 3] = lgtimer();
 }
 
+// Images [B, Kw] packed bits -> e2m1 lines [B, Kw * 16 B]: word q of image b becomes the 16
+// bytes put_word4_sw writes for it (codes 0x2 = 1.0 for a set bit, 0x0 for a clear one), so a
+// TMA SW128 box of these lines is the producers' tile byte for byte. Pad bits are 0 -> 0.0.
+__global__ void __launch_bounds__(256) expand_act4_kernel(const uint32_t* __restrict__ in, size_t n, uint4* __restrict__ out) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = __ldg(in + i);
+        out[i] = make_uint4((w << 1) & 0x22222222u, w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
+    }
+}
+
+int launch_expand_act4(const LinGeom& l, cudaStream_t s) {
+    const size_t n = size_t(l.B) * l.Kw;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min<size_t>((n + 255) / 256, size_t(num_sms()) * 8)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BNN_CUDA(cudaLaunchKernelEx(&cfg, expand_act4_kernel, l.in, n, reinterpret_cast<uint4*>(l.in4)));
+    return launch_check("expand_act4_kernel");
+}
+
+int g_lin4_tma = -2;  // -2 unread, -1 auto, 0 / 1 forced (bnn_set_fused_lin4 2 / 3, BNN_LIN4_TMA)
+void set_lin4_tma(int mode) { g_lin4_tma = mode; }
+
 // Host plan: images per tile (NB, <= 256, a multiple of 16), feature tiles of 128 and the K
 // split that gives ~one wave of CTAs (at least 2 K blocks per slice, at most 8 slices).
 bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
@@ -430,6 +475,12 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     l.sem = nullptr;
     l.dbg = nullptr;
     l.tl = nullptr;
+    // Images TMA-loaded from a once-expanded e2m1 copy (expand_act4_kernel, one extra launch)
+    // instead of expanded by the producers in every CTA: pays when each image row would be
+    // expanded by many feature tiles (BNN_LIN4_TMA=0/1 forces it off/on).
+    if (g_lin4_tma == -2) g_lin4_tma = getenv("BNN_LIN4_TMA") ? atoi(getenv("BNN_LIN4_TMA")) : -1;
+    l.tmab = g_lin4_tma >= 0 ? (g_lin4_tma != 0) : (l.m_tiles >= 4 && fg.B >= 512);
+    l.in4 = nullptr;
     return true;
 }
 
@@ -437,7 +488,7 @@ size_t lin4_sem_count(const LinGeom& l) { return l.ksplit > 1 ? size_t(2) * l.m_
 
 size_t lin4_ws_bytes(const LinGeom& l) { return l.ksplit > 1 ? size_t(l.ksplit) * l.B * l.Dpad * sizeof(int) : 0; }
 
-int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
+int launch_lin4(const CUtensorMap& tm4, const CUtensorMap& tmx, const LinGeom& l, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
         BNN_CUDA(cudaFuncSetAttribute(lin4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLSmem)));
@@ -460,7 +511,7 @@ int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
     if (lt.tl) fused_timeline_name(("lin4 D=" + std::to_string(l.D) + " K=" + std::to_string(l.K) + " split=" +
                                     std::to_string(l.ksplit)).c_str());
     if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, lt));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, tmx, lt));
         BNN_TRY(launch_check("lin4_kernel"));
     } else {  // synchronous, not capturable: tools only
         LinGeom lp = l;
@@ -470,7 +521,7 @@ int launch_lin4(const CUtensorMap& tm4, const LinGeom& l, cudaStream_t s) {
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, lp));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, tmx, lp));
         cudaEventRecord(e1, s);
         BNN_TRY(launch_check("lin4_kernel"));
         BNN_CUDA(cudaStreamSynchronize(s));

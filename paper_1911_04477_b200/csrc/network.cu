@@ -28,6 +28,7 @@ namespace bnnk {
 
 int launch_pack_cols(const float*, size_t, size_t, uint32_t*, size_t, unsigned long long*,
                      cudaStream_t);
+int launch_pack_rows_e2m1(const float* x, size_t D, size_t L, void* out4, cudaStream_t s);
 int launch_pack_rows(const float*, size_t, size_t, uint32_t*, size_t, unsigned long long*,
                      cudaStream_t);
 int launch_im2col_sign_pack(const float*, size_t, size_t, size_t, size_t, const bnn_conv_geom*,
@@ -162,6 +163,7 @@ struct bnn_net {
     bnnk::DevBuf bits[2], pix, ws, sem;
     bnnk::DevBuf lin_ws;   // split-K partial sums of the FP4 linear kernel (lin4)
     bnnk::DevBuf lin_sem;  // its per-tile counters (zeroed once; the kernel leaves them at 0)
+    bnnk::DevBuf lin_x4;   // e2m1 images of a TMA-fed lin4 stage (expand_act4_kernel)
     bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)
 };
 
@@ -773,10 +775,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         int cg, bn;
         bool lin4 = false;
         LinGeom lg{};
+        CUtensorMap tmx;  // the e2m1 images of a TMA-fed lin4 stage
     };
     std::vector<Plan> plans;
     size_t ws_need = 0, sem_need = 0;  // the largest split-K workspace of any stage
     size_t lin_ws_need = 0, lin_sem_need = 0;  // the largest lin4 workspace and counter array
+    size_t lin_x4_need = 0;                    // the largest expanded image block of a TMA-fed lin4
     const void* in = x;
     int which = 0;
     (void)prof;
@@ -812,6 +816,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             pl.lin4 = true;
             lin_ws_need = std::max(lin_ws_need, lin4_ws_bytes(pl.lg));
             lin_sem_need = std::max(lin_sem_need, lin4_sem_count(pl.lg) * sizeof(unsigned));
+            if (pl.lg.tmab) lin_x4_need = std::max(lin_x4_need, size_t(pl.lg.B) * pl.lg.Kw * 16);
         }
         plans.push_back(pl);
         in = g.out_bits;
@@ -837,9 +842,18 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         BNN_CUDA(cudaMemsetAsync(net->lin_sem.p, 0, lin_sem_need, s));
         ++net->arena_epoch;
     }
+    if (net->lin_x4.bytes < lin_x4_need) {
+        BNN_TRY(net->lin_x4.alloc(lin_x4_need));
+        ++net->arena_epoch;
+    }
     for (auto& pl : plans) {
         if (pl.g.ksplit > 1) pl.g.ws = net->ws.as<int>(), pl.g.sem = net->sem.as<unsigned>();
         if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>(), pl.lg.sem = net->lin_sem.as<unsigned>();
+        if (pl.lin4 && pl.lg.tmab) {
+            pl.lg.in4 = net->lin_x4.as<uint8_t>();
+            const size_t lb = size_t(pl.lg.Kw) * 16;
+            BNN_TRY(make_tmap_2d_s8(&pl.tmx, pl.lg.in4, size_t(pl.lg.B), lb, lb, uint32_t(pl.lg.NB)));
+        }
     }
     size_t launches = 0;
     for (size_t i = 0; i < plans.size(); ++i) {
@@ -862,7 +876,12 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             BNN_TRY(launch_pack_pixels(x, B, g.C, size_t(g.H) * g.W, net->pix.as<uint32_t>(), s));
             ++launches;
         }
-        if (st.pre_encode) {  // K1: pack_rows(sign(x)) over [B, F]
+        const bool pre4 = st.pre_encode && plans[i].lin4 && plans[i].lg.tmab &&
+                          size_t(g.Cw) == wpl_of(size_t(g.C));  // straight to e2m1 images
+        if (pre4) {
+            BNN_TRY(launch_pack_rows_e2m1(x, B, size_t(g.C), plans[i].lg.in4, s));
+            ++launches;
+        } else if (st.pre_encode) {  // K1: pack_rows(sign(x)) over [B, F]
             BNN_TRY(launch_pack_rows(x, B, size_t(g.C), net->pix.as<uint32_t>(), size_t(g.Cw), nullptr, s));
             ++launches;
         }
@@ -878,8 +897,13 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             if (pix_f32) gp.in = x;
             BNN_TRY(launch_pix_popc(gp, st.pix, pix_f32, s));
         }
-        else if (plans[i].lin4)
-            BNN_TRY(launch_lin4(st.tm4, plans[i].lg, s));
+        else if (plans[i].lin4) {
+            if (plans[i].lg.tmab && !pre4) {
+                BNN_TRY(launch_expand_act4(plans[i].lg, s));
+                ++launches;
+            }
+            BNN_TRY(launch_lin4(st.tm4, plans[i].lg.tmab ? plans[i].tmx : st.tm4, plans[i].lg, s));
+        }
         else if (HaloGeom hg; use_halo(net, st, plans[i].cg) && halo4_plan(g, hg) && (!hg.wst || g_halo == 2))
             BNN_TRY(launch_halo4(st.tm4, hg, s));
         else if (use_fp4(net, st, plans[i].cg))
@@ -1109,8 +1133,10 @@ int bnn_set_fused_fp4(int mode) {
 }
 
 int bnn_set_fused_lin4(int enabled) {
-    if (enabled < 0 || enabled > 1) return fail(BNN_E_CONFIG, "fused lin4: 0 (off) or 1 (on)");
-    g_lin4 = enabled;
+    if (enabled < 0 || enabled > 3)
+        return fail(BNN_E_CONFIG, "fused lin4: 0 (off), 1 (on), 2 (on, TMA-loaded images), 3 (on, producer-expanded images)");
+    g_lin4 = enabled != 0;
+    set_lin4_tma(enabled == 2 ? 1 : enabled == 3 ? 0 : -1);
     ++g_tiling_epoch;  // captured graphs hold the other kernels
     return BNN_OK;
 }

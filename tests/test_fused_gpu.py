@@ -63,7 +63,7 @@ FUSABLE = {
 }
 
 
-@pytest.fixture(params=["auto", "nohalo", "halostream", "halo0", "nolin4", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall",
+@pytest.fixture(params=["auto", "nohalo", "halostream", "halo0", "nolin4", "lin4tma", "lin4prod", "nopixpopc", "pixf32", "pixpacked", "noswap", "swapall",
                         "nofp4", "fp4all", "nopair", "pair224", "nosmall", "cg1", "nosplit", "split16"])
 def tiling(bnn, request):
     """Every fused test runs with the automatic tile choice (one launch per weighted layer,
@@ -86,7 +86,8 @@ def tiling(bnn, request):
     bnn._lib.check(lib.bnn_set_fused_halo({"nohalo": 0, "halostream": 2}.get(p, 1)))
     # the pixel-input first conv on the halo FP4 kernel (opt-in: measured slower than pix_tile)
     bnn._lib.check(lib.bnn_set_fused_halo0(1 if p == "halo0" else 0))
-    bnn._lib.check(lib.bnn_set_fused_lin4(0 if p == "nolin4" else 1))
+    # lin4 images: TMA-loaded from a once-expanded e2m1 copy (forced on / off; auto by size)
+    bnn._lib.check(lib.bnn_set_fused_lin4({"nolin4": 0, "lin4tma": 2, "lin4prod": 3}.get(p, 1)))
     yield p
     lib.bnn_set_fused_tiling(0, 0)
     lib.bnn_set_fused_split(0)
@@ -117,7 +118,8 @@ def test_default_network_fused_vs_oracle(bnn, orc, fused, tiling, batch):
     got = net.forward(x)
     # 9 weighted layers, + pack_pixels when the first conv reads packed pixel words (the int8
     # tensor-core path and pix_popc after the packer); halo0 and pix_tile read the floats
-    assert net.last_launches() == (9 if tiling in ("auto", "pixf32", "halo0") else 10)
+    assert net.last_launches() == ((9 if tiling in ("auto", "pixf32", "halo0") else 10) +
+                                   (2 if tiling == "lin4tma" else 0))  # + expand_act4 for fc1 and fc2
     assert np.array_equal(got, orc.net(seed=1).forward(x))
 
 

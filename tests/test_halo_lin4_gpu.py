@@ -85,3 +85,23 @@ def test_deep_linear_splits_k(bnn):
     x = np.zeros((5, *shape[1:]), dtype=np.float32)
     net.forward(x)
     assert _kernels(bnn, net)[0] == "lin4_kernel"
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])  # auto, TMA-loaded images forced, producer-expanded forced
+@pytest.mark.parametrize("batch", [1, 37, 600])
+def test_lin4_tma_images_vs_oracle(bnn, orc, mode, batch):
+    """lin4 with the images expanded once to e2m1 (expand_act4_kernel) and TMA-loaded, against
+    the producer-expanded path and the oracle: K % 256 != 0, D % 128 != 0, split-K and not."""
+    lib = bnn.load()
+    layers = [lin(992)] + G + [lin(544)] + G + [lin(10)]
+    net = bnn.Network(layers, (2336, 1, 1), 41)
+    net.set_engine("fused")
+    x = orc.fill_random((batch, 2336, 1, 1), orc.mix64(41, INPUT_STREAM))
+    try:
+        bnn._lib.check(lib.bnn_set_fused_lin4(mode))
+        got = net.forward(x)
+        ks = _kernels(bnn, net)
+    finally:
+        lib.bnn_set_fused_lin4(1)
+    assert ks.count("lin4_kernel") >= 2, ks
+    assert np.array_equal(got, orc.net(layers, (2336, 1, 1), 41).forward(x))

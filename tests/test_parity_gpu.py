@@ -346,24 +346,27 @@ def test_network_device_path_and_deterministic(bnn, orc):
 @pytest.fixture
 def policy(bnn):
     lib = bnn.load()
-    yield lambda p: lib.bnn_set_gemm_policy({"auto": 0, "popc": 1, "umma": 2}[p])
+    yield lambda p: lib.bnn_set_gemm_policy({"auto": 0, "popc": 1, "umma": 2, "tma": 3}[p])
     lib.bnn_set_gemm_policy(0)
 
 
-@pytest.mark.parametrize("kernel", ["popc", "umma"])
+GEMM_KERNEL = {"popc": "popc", "umma": "xnor4_kernel", "tma": "xnor4t_kernel"}
+
+
+@pytest.mark.parametrize("kernel", ["popc", "umma", "tma"])
 @pytest.mark.parametrize("m,n,L", [(1, 1, 1), (3, 4, 31), (16, 16, 33), (128, 256, 128), (130, 70, 9216),
                                    (257, 513, 1000), (1024, 1024, 1024), (64, 1024, 576),
-                                   (1000, 300, 4096), (5, 3000, 200)])
+                                   (1000, 300, 4096), (5, 3000, 200), (300, 481, 257), (129, 241, 2050)])
 def test_gemm_kernels_vs_oracle(bnn, orc, policy, kernel, m, n, L):
     policy(kernel)
     w = orc.pack(orc.fill_random((m, L), m + 7), "rows", True)
     x = orc.pack(orc.fill_random((L, n), n + 9), "cols", True)
     got = bnn.xnor_gemm(bnn.PackedBitMatrix(m, L, "rows", w), bnn.PackedBitMatrix(L, n, "cols", x), L)
-    assert bnn.load().bnn_last_gemm_kernel().decode() == ("popc" if kernel == "popc" else "xnor4_kernel")
+    assert bnn.load().bnn_last_gemm_kernel().decode() == GEMM_KERNEL[kernel]
     assert np.array_equal(got, orc.xnor_gemm(w, x, L))
 
 
-@pytest.mark.parametrize("kernel", ["popc", "umma"])
+@pytest.mark.parametrize("kernel", ["popc", "umma", "tma"])
 def test_gemm_kernels_golden_and_layers(bnn, orc, golden, policy, kernel):
     policy(kernel)
     arrays, meta = golden
@@ -392,3 +395,29 @@ def test_network_both_kernels(bnn, orc, policy, kernel):
     net = bnn.Network(seed=1)
     x = orc.fill_random((8, 3, 32, 32), orc.mix64(1, INPUT_STREAM))
     assert np.array_equal(net.forward(x), orc.net(seed=1).forward(x))
+
+
+@pytest.mark.parametrize("m,n,L", [(2048, 2100, 1030), (4096, 1024, 9216)])
+def test_gemm_auto_large_takes_tma_kernel(bnn, orc, policy, m, n, L):
+    """Above 2^32 bit-MACs AUTO runs the TMA-fed FP4 kernel (operands expanded once in HBM)."""
+    policy("auto")
+    w = orc.pack(orc.fill_random((m, L), m + 3), "rows", True)
+    x = orc.pack(orc.fill_random((L, n), n + 5), "cols", True)
+    got = bnn.xnor_gemm(bnn.PackedBitMatrix(m, L, "rows", w), bnn.PackedBitMatrix(L, n, "cols", x), L)
+    assert bnn.load().bnn_last_gemm_kernel().decode() == "xnor4t_kernel"
+    assert np.array_equal(got, orc.xnor_gemm(w, x, L))
+
+
+def test_conv_large_takes_tma_kernel(bnn, orc, policy):
+    """conv_forward_binary whose GEMM is above 2^32 bit-MACs: the TMA kernel's f32 epilogue
+    (to_float + bias_add + reshape_output scatter) against the oracle (forced: with 136 output
+    channels AUTO keeps the in-CTA expansion kernel)."""
+    policy("tma")
+    g = bnn.ConvGeometry(3, 3, 1, 1, 1, 1, 128, 136)
+    x = orc.fill_random((33, 128, 32, 32), 5)
+    w = orc.fill_random((136, 1152), 6)
+    b = orc.fill_random((136,), 7)
+    y = bnn.conv_forward_binary(x, bnn.sign_pack_rows(w), b, g)
+    assert bnn.load().bnn_last_gemm_kernel().decode() == "xnor4t_kernel"
+    want = orc.conv_forward_binary(x, orc.pack(w, "rows", True), b, list(g.__dict__.values()))
+    assert np.array_equal(y, want)

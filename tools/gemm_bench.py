@@ -20,7 +20,7 @@ def main():
                                                     "1000,1024,4096", "4096,4096,4096", "128,262144,1152",
                                                     "8192,8192,8192"])
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--kernels", default="popc,umma")
+    ap.add_argument("--kernels", default="popc,umma,tma")
     a = ap.parse_args()
     lib = bnn.load()
     s = torch.cuda.current_stream().cuda_stream
@@ -36,7 +36,7 @@ def main():
         out = torch.empty((M, N), dtype=torch.int32, device="cuda")
         ref = None
         for k in a.kernels.split(","):
-            lib.bnn_set_gemm_policy({"popc": 1, "umma": 2}[k])
+            lib.bnn_set_gemm_policy({"popc": 1, "umma": 2, "tma": 3}[k])
             run = lambda: bnn._lib.check(lib.bnn_xnor_gemm_s32(w.data_ptr(), wpl, x.data_ptr(), wpl, M, N, L,
                                                                out.data_ptr(), N, s))
             for _ in range(3):
