@@ -274,23 +274,46 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
 
 constexpr int kTThreads = 192;
 
-// Packed lines [rows, ld words] (L valid bits each) -> e2m1 lines [rows, Lw * 16 bytes].
-__global__ void __launch_bounds__(256) expand4_kernel(const uint32_t* __restrict__ src, size_t ld, size_t rows, int Lw,
-                                                      int L, uint4* __restrict__ dst) {
-    const size_t total = rows * size_t(Lw);
-    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+// Packed lines [rows, ld words] (L valid bits each) -> e2m1 lines [rows, Lw * 16 bytes], both
+// operands in one launch (blockIdx.y). Dense lines with no partial last word (ld = Lw, L = 32 Lw,
+// the usual large-GEMM case) stream 4 words per thread (16-byte load, 4 x 16-byte stores).
+struct Expand4Op {
+    const uint32_t* src;
+    size_t ld, rows;
+    uint4* dst;
+};
+
+__device__ __forceinline__ uint4 pm1_word(uint32_t b, uint32_t m) {
+    uint32_t o[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const uint32_t xs = (b >> s) & 0x11111111u, ms = (m >> s) & 0x11111111u;
+        o[s] = (ms << 1) | ((ms & ~xs) << 3);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__global__ void __launch_bounds__(256) expand4_kernel(const Expand4Op a, const Expand4Op b, int Lw, int L) {
+    const Expand4Op& op = blockIdx.y ? b : a;
+    const size_t total = op.rows * size_t(Lw);
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    const size_t t0 = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (op.ld == size_t(Lw) && L == 32 * Lw && (total & 3) == 0 && (reinterpret_cast<uintptr_t>(op.src) & 15) == 0) {
+        const uint4* src4 = reinterpret_cast<const uint4*>(op.src);
+        for (size_t i = t0; i < total / 4; i += stride) {
+            const uint4 w = __ldg(src4 + i);
+            op.dst[4 * i + 0] = pm1_word(w.x, 0xffffffffu);
+            op.dst[4 * i + 1] = pm1_word(w.y, 0xffffffffu);
+            op.dst[4 * i + 2] = pm1_word(w.z, 0xffffffffu);
+            op.dst[4 * i + 3] = pm1_word(w.w, 0xffffffffu);
+        }
+        return;
+    }
+    for (size_t i = t0; i < total; i += stride) {
         const size_t r = i / size_t(Lw);
         const int q = int(i - r * size_t(Lw));
-        const uint32_t b = __ldg(src + r * ld + q);
         const int nv = L - 32 * q;
-        const uint32_t m = nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
-        uint32_t o[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const uint32_t xs = (b >> s) & 0x11111111u, ms = (m >> s) & 0x11111111u;
-            o[s] = (ms << 1) | ((ms & ~xs) << 3);
-        }
-        dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
+        op.dst[i] = pm1_word(__ldg(op.src + r * op.ld + q), nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u));
     }
 }
 
@@ -449,9 +472,8 @@ int launch_xnor4t(G4 g, cudaStream_t s) {
     Scratch ea, eb;
     BNN_TRY(ea.alloc(size_t(g.M) * lb, s));
     BNN_TRY(eb.alloc(size_t(g.N) * lb, s));
-    const int eg = sms * 8;
-    expand4_kernel<<<eg, 256, 0, s>>>(g.w, g.ldw, size_t(g.M), g.Lw, g.L, ea.as<uint4>());
-    expand4_kernel<<<eg, 256, 0, s>>>(g.x, g.ldx, size_t(g.N), g.Lw, g.L, eb.as<uint4>());
+    expand4_kernel<<<dim3(unsigned(sms * 4), 2), 256, 0, s>>>(Expand4Op{g.w, g.ldw, size_t(g.M), ea.as<uint4>()},
+                                                              Expand4Op{g.x, g.ldx, size_t(g.N), eb.as<uint4>()}, g.Lw, g.L);
     BNN_TRY(launch_check("expand4_kernel"));
     CUtensorMap ta, tb;
     BNN_TRY(make_tmap_2d_s8(&ta, ea.p, size_t(g.M), lb, lb, 128));

@@ -12,6 +12,8 @@
 // Two kernels: im2col_rowbits_kernel (W <= 32) sign-packs each input row once and builds
 // every output word from kW-bit fields of those row words; im2col_sign_pack_kernel is the
 // general one (a load and compare per bit).
+#include <algorithm>
+
 #include "bnn_common.cuh"
 
 namespace bnnk {
@@ -137,6 +139,19 @@ __global__ void __launch_bounds__(256, 5)
     // 2. word q of every position of every row of the group: lane = patch row r
     const int kk = kH * kW;
     const uint64_t pad = ~(((1ull << W) - 1ull) << 16);  // row at bits [16, 16 + W), the rest 1
+    // per-lane transpose constants (see transpose32 in umma.cuh): round j keeps the half of the
+    // word selected by k_j (~k_j in lanes with bit j set) and rotates the partner's word by j
+    uint32_t keep[5];
+    int rot[5];
+#pragma unroll
+    for (int jj = 0; jj < 5; ++jj) {
+        const int j = 16 >> jj;
+        const uint32_t k = jj == 0 ? 0x0000FFFFu : jj == 1 ? 0x00FF00FFu : jj == 2 ? 0x0F0F0F0Fu : jj == 3 ? 0x33333333u
+                                                                                                     : 0x55555555u;
+        const bool up = (lane & j) != 0;
+        keep[jj] = up ? ~k : k;
+        rot[jj] = up ? 32 - j : j;
+    }
     // word q outer (the lane's patch row decode once), the group's rows inner
     for (int q = warp; q < wpl; q += nwarps) {
         const int r = q * 32 + lane;
@@ -150,14 +165,15 @@ __global__ void __launch_bounds__(256, 5)
                 uint32_t mine = 0;
                 if (sW == 1) {
                     // lane r holds its bits for 32 consecutive positions; a 32 x 32 bit transpose
-                    // across the warp (5 shuffle-xor butterfly rounds) gives lane ox its word
+                    // across the warp gives lane ox its word: per round a shuffle, a funnel-shift
+                    // rotate and one LOP3 with the lane's loop-invariant keep mask and rotation
                     uint32_t v = uint32_t(win >> (sh0 + ox0));
 #pragma unroll
-                    for (int j = 16; j >= 1; j >>= 1) {
-                        const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                                         : j == 2 ? 0x33333333u : 0x55555555u;
+                    for (int jj = 0; jj < 5; ++jj) {
+                        const int j = 16 >> jj;
                         const uint32_t p = __shfl_xor_sync(0xffffffffu, v, j);
-                        v = (lane & j) ? ((v & ~m) | ((p >> j) & m)) : ((v & m) | ((p & m) << j));
+                        const uint32_t qv = __funnelshift_l(p, p, rot[jj]);
+                        v = (v & keep[jj]) | (qv & ~keep[jj]);
                     }
                     mine = v;
                 } else {
@@ -178,17 +194,21 @@ __global__ void __launch_bounds__(256, 5)
         // of the group's patch words against the D packed weight rows (CUDA cores), then
         // to_float + bias_add (kernels.cpp:90-107) into the NCHW output (reshape_output,
         // lowering.cpp:87-95). a = L - 2 * sum popc(w ^ x) (pad bits are 0 in both operands).
-        uint32_t* wsm = tile + ry * ow * wpl;  // [D][wpl]
-        for (int t = threadIdx.x; t < D * wpl; t += blockDim.x) {
+        // blockIdx.z: this block's slice of output channels [d0, d0 + nd) (more blocks in flight
+        // for batch-1 layers; the patch words are rebuilt per slice, from L2)
+        const int dch = (D + gridDim.z - 1) / gridDim.z;
+        const int d0 = blockIdx.z * dch, nd = min(D, d0 + dch) - d0;
+        uint32_t* wsm = tile + ry * ow * wpl;  // [nd][wpl]
+        for (int t = threadIdx.x; t < nd * wpl; t += blockDim.x) {
             const int d = t / wpl, q = t - d * wpl;
-            wsm[t] = __ldg(cw + size_t(d) * ldw + q);
+            wsm[t] = __ldg(cw + size_t(d0 + d) * ldw + q);
         }
         __syncthreads();
         const int nl = ry * ow;
-        for (int t = threadIdx.x; t < D * nl; t += blockDim.x) {
-            const int d = t / nl, l = t - d * nl;
+        for (int t = threadIdx.x; t < nd * nl; t += blockDim.x) {
+            const int dl = t / nl, l = t - dl * nl, d = d0 + dl;
             const uint32_t* xr = tile + l * wpl;
-            const uint32_t* wr = wsm + d * wpl;
+            const uint32_t* wr = wsm + dl * wpl;
             int pc = 0;
             for (int q = 0; q < wpl; ++q) pc += __popc(xr[q] ^ wr[q]);
             y[(size_t(img) * D + d) * oh * ow + size_t(oy0) * ow + l] =
@@ -262,7 +282,9 @@ int conv_rowbits_fused(const float* x, size_t B, size_t C, size_t H, size_t W, c
     if (!(W <= 32 && pW <= 16 && oh < 65536 && B < 65536 && (ow - 1) * g->stride_w + kW <= 48 + pW)) return BNN_OK;
     const size_t smem = (C * kH + ow * wpl + D * wpl) * sizeof(uint32_t);  // one output row per block
     if (smem > 48 * 1024 || D * ow * wpl > 4096 * 36) return BNN_OK;
-    im2col_rowbits_kernel<<<dim3(unsigned(oh), unsigned(B)), 256, smem, s>>>(
+    // channel slices: enough blocks for two per SM when the batch x rows grid is small
+    const size_t dz = std::max<size_t>(1, std::min<size_t>(ceil_div(2 * size_t(num_sms()), oh * B), D / 4));
+    im2col_rowbits_kernel<<<dim3(unsigned(oh), unsigned(B), unsigned(dz)), 256, smem, s>>>(
         x, int(C), int(H), int(W), int(kH), int(kW), int(sH), int(g->stride_w), int(g->pad_h), int(pW), int(oh),
         int(ow), int(K), int(wpl), 1, nullptr, 0, pw, ldw, int(D), bias, out);
     BNN_TRY(launch_check("im2col_rowbits_kernel (fused conv)"));

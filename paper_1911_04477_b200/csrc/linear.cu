@@ -63,6 +63,16 @@ __device__ __forceinline__ void put_word4_sw(uint32_t tile, int r, int chunk, ui
                  w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
 }
 
+// One 32-feature decision word of the next layer's input: packed bits, or (out4 set: the next
+// layer TMA-loads its images) the 16 bytes of e2m1 {0, 1.0} codes expand_act4_kernel would make.
+__device__ __forceinline__ void store_act(const LinGeom& g, size_t word, uint32_t w) {
+    if (g.out4)
+        reinterpret_cast<uint4*>(g.out4)[word] =
+            make_uint4((w << 1) & 0x22222222u, w & 0x22222222u, (w >> 1) & 0x22222222u, (w >> 2) & 0x22222222u);
+    else
+        g.out_bits[word] = w;
+}
+
 __device__ __forceinline__ unsigned long long lgtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 } else if (g.epi == FEPI_BITS) {
                     const uint32_t mine = decisions_transposed(v, Tf - 1.0f, flip, lane);
                     if (d0 < g.D && bc + lane < g.B && lane < g.NB - 32 * c)
-                        g.out_bits[size_t(bc + lane) * g.Dw + (d0 >> 5)] = mine;
+                        store_act(g, size_t(bc + lane) * g.Dw + (d0 >> 5), mine);
                 } else {
                     // to_float(a) + bias (kernels.cpp:90-107): one rounding of an exact integer
                     if (dvalid) {
@@ -362,7 +372,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                 w |= __shfl_xor_sync(0xffffffffu, w, 1);
                 w |= __shfl_xor_sync(0xffffffffu, w, 2);
                 w |= __shfl_xor_sync(0xffffffffu, w, 4);
-                if ((lane & 7) == 0 && d < g.D) g.out_bits[size_t(b) * g.Dw + (d >> 5)] = w;
+                if ((lane & 7) == 0 && d < g.D) store_act(g, size_t(b) * g.Dw + (d >> 5), w);
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -481,6 +491,7 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     if (g_lin4_tma == -2) g_lin4_tma = getenv("BNN_LIN4_TMA") ? atoi(getenv("BNN_LIN4_TMA")) : -1;
     l.tmab = g_lin4_tma >= 0 ? (g_lin4_tma != 0) : (l.m_tiles >= 4 && fg.B >= 512);
     l.in4 = nullptr;
+    l.out4 = nullptr;
     return true;
 }
 

@@ -163,7 +163,7 @@ struct bnn_net {
     bnnk::DevBuf bits[2], pix, ws, sem;
     bnnk::DevBuf lin_ws;   // split-K partial sums of the FP4 linear kernel (lin4)
     bnnk::DevBuf lin_sem;  // its per-tile counters (zeroed once; the kernel leaves them at 0)
-    bnnk::DevBuf lin_x4;   // e2m1 images of a TMA-fed lin4 stage (expand_act4_kernel)
+    bnnk::DevBuf lin_x4[2];  // e2m1 images of TMA-fed lin4 stages (ping-pong: a lin4 stage writes the next one's)
     bnnk::DevBuf fcols;  // float im2col matrix (control-group engine)
 };
 
@@ -776,6 +776,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         bool lin4 = false;
         LinGeom lg{};
         CUtensorMap tmx;  // the e2m1 images of a TMA-fed lin4 stage
+        bool in4_ready = false;  // ... written by the previous lin4 stage's epilogue
     };
     std::vector<Plan> plans;
     size_t ws_need = 0, sem_need = 0;  // the largest split-K workspace of any stage
@@ -842,17 +843,27 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         BNN_CUDA(cudaMemsetAsync(net->lin_sem.p, 0, lin_sem_need, s));
         ++net->arena_epoch;
     }
-    if (net->lin_x4.bytes < lin_x4_need) {
-        BNN_TRY(net->lin_x4.alloc(lin_x4_need));
-        ++net->arena_epoch;
-    }
+    for (auto& b4 : net->lin_x4)
+        if (b4.bytes < lin_x4_need) {
+            BNN_TRY(b4.alloc(lin_x4_need));
+            ++net->arena_epoch;
+        }
     for (auto& pl : plans) {
         if (pl.g.ksplit > 1) pl.g.ws = net->ws.as<int>(), pl.g.sem = net->sem.as<unsigned>();
         if (pl.lin4) pl.lg.ws = net->lin_ws.as<int>(), pl.lg.sem = net->lin_sem.as<unsigned>();
-        if (pl.lin4 && pl.lg.tmab) {
-            pl.lg.in4 = net->lin_x4.as<uint8_t>();
-            const size_t lb = size_t(pl.lg.Kw) * 16;
-            BNN_TRY(make_tmap_2d_s8(&pl.tmx, pl.lg.in4, size_t(pl.lg.B), lb, lb, uint32_t(pl.lg.NB)));
+    }
+    // TMA-fed lin4 stages read e2m1 images from lin_x4[k]; a preceding lin4 stage with a bits
+    // epilogue writes them there directly (no expand_act4 launch), the buffers alternating
+    for (size_t i = 0, k = 0; i < plans.size(); ++i) {
+        Plan& pl = plans[i];
+        if (!(pl.lin4 && pl.lg.tmab)) continue;
+        pl.lg.in4 = net->lin_x4[k].as<uint8_t>();
+        k ^= 1;
+        const size_t lb = size_t(pl.lg.Kw) * 16;
+        BNN_TRY(make_tmap_2d_s8(&pl.tmx, pl.lg.in4, size_t(pl.lg.B), lb, lb, uint32_t(pl.lg.NB)));
+        if (i > 0 && plans[i - 1].lin4 && plans[i - 1].lg.epi == FEPI_BITS && plans[i - 1].lg.Dw == pl.lg.Kw) {
+            plans[i - 1].lg.out4 = pl.lg.in4;
+            pl.in4_ready = true;
         }
     }
     size_t launches = 0;
@@ -898,7 +909,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
             BNN_TRY(launch_pix_popc(gp, st.pix, pix_f32, s));
         }
         else if (plans[i].lin4) {
-            if (plans[i].lg.tmab && !pre4) {
+            if (plans[i].lg.tmab && !pre4 && !plans[i].in4_ready) {
                 BNN_TRY(launch_expand_act4(plans[i].lg, s));
                 ++launches;
             }
