@@ -70,6 +70,66 @@ __global__ void __launch_bounds__(256)
     if (j0 + line < lines && k0 + kq < wpl) words[(j0 + line) * ld + k0 + kq] = tile[line][kq];
 }
 
+// Phase 2 of the row-bits im2col (shared by the per-group and the pipelined kernels): from the
+// group's sign-packed input rows `rows` [C][nrow], word q of every output position of its ry
+// rows into `tile` [ry * ow][wpl]; lane = patch row r = 32 q + lane.
+__device__ __forceinline__ void rowbits_words(const uint32_t* __restrict__ rows, uint32_t* __restrict__ tile, int W,
+                                              int kH, int kW, int sH, int sW, int pW, int ow, int K, int wpl, int ry,
+                                              int nrow, int warp, int nwarps, int lane) {
+    // 2. word q of every position of every row of the group: lane = patch row r
+    const int kk = kH * kW;
+    const uint64_t pad = ~(((1ull << W) - 1ull) << 16);  // row at bits [16, 16 + W), the rest 1
+    // per-lane transpose constants (see transpose32 in umma.cuh): round j keeps the half of the
+    // word selected by k_j (~k_j in lanes with bit j set) and rotates the partner's word by j
+    uint32_t keep[5];
+    int rot[5];
+#pragma unroll
+    for (int jj = 0; jj < 5; ++jj) {
+        const int j = 16 >> jj;
+        const uint32_t k = jj == 0 ? 0x0000FFFFu : jj == 1 ? 0x00FF00FFu : jj == 2 ? 0x0F0F0F0Fu : jj == 3 ? 0x33333333u
+                                                                                                     : 0x55555555u;
+        const bool up = (lane & j) != 0;
+        keep[jj] = up ? ~k : k;
+        rot[jj] = up ? 32 - j : j;
+    }
+    // word q outer (the lane's patch row decode once), the group's rows inner
+    for (int q = warp; q < wpl; q += nwarps) {
+        const int r = q * 32 + lane;
+        const bool rv = r < K;  // bits past K are 0
+        const int c = r / kk, t = r - c * kk, kh = t / kW, kw = t - kh * kW;
+        const int sh0 = 16 - pW + kw;  // window bit of position ox: sh0 + ox * sW
+        const uint32_t* rowp = rows + c * nrow + kh;
+        for (int yy = 0; yy < ry; ++yy) {
+            const uint64_t win = rv ? ((uint64_t(rowp[yy * sH]) << 16) | pad) : 0ull;
+            for (int ox0 = 0; ox0 < ow; ox0 += 32) {
+                uint32_t mine = 0;
+                if (sW == 1) {
+                    // lane r holds its bits for 32 consecutive positions; a 32 x 32 bit transpose
+                    // across the warp gives lane ox its word: per round a shuffle, a funnel-shift
+                    // rotate and one LOP3 with the lane's loop-invariant keep mask and rotation
+                    uint32_t v = uint32_t(win >> (sh0 + ox0));
+#pragma unroll
+                    for (int jj = 0; jj < 5; ++jj) {
+                        const int j = 16 >> jj;
+                        const uint32_t p = __shfl_xor_sync(0xffffffffu, v, j);
+                        const uint32_t qv = __funnelshift_l(p, p, rot[jj]);
+                        v = (v & keep[jj]) | (qv & ~keep[jj]);
+                    }
+                    mine = v;
+                } else {
+#pragma unroll 8
+                    for (int j = 0; j < 32; ++j) {
+                        const int ox = ox0 + j;
+                        const uint32_t wbits = __ballot_sync(0xffffffffu, (win >> (sh0 + ox * sW)) & 1ull);
+                        if (lane == j) mine = wbits;
+                    }
+                }
+                if (ox0 + lane < ow) tile[(yy * ow + ox0 + lane) * wpl + q] = mine;
+            }
+        }
+    }
+}
+
 // Row-bits kernel (W <= 32, the CIFAR-class shapes): one block per (image, group of R output
 // rows).
 //  1. Sign-pack every input row the group needs — rows (oy0*sH - pH) .. of all C channels, each
@@ -136,58 +196,7 @@ __global__ void __launch_bounds__(256, 5)
         }
     }
     __syncthreads();
-    // 2. word q of every position of every row of the group: lane = patch row r
-    const int kk = kH * kW;
-    const uint64_t pad = ~(((1ull << W) - 1ull) << 16);  // row at bits [16, 16 + W), the rest 1
-    // per-lane transpose constants (see transpose32 in umma.cuh): round j keeps the half of the
-    // word selected by k_j (~k_j in lanes with bit j set) and rotates the partner's word by j
-    uint32_t keep[5];
-    int rot[5];
-#pragma unroll
-    for (int jj = 0; jj < 5; ++jj) {
-        const int j = 16 >> jj;
-        const uint32_t k = jj == 0 ? 0x0000FFFFu : jj == 1 ? 0x00FF00FFu : jj == 2 ? 0x0F0F0F0Fu : jj == 3 ? 0x33333333u
-                                                                                                     : 0x55555555u;
-        const bool up = (lane & j) != 0;
-        keep[jj] = up ? ~k : k;
-        rot[jj] = up ? 32 - j : j;
-    }
-    // word q outer (the lane's patch row decode once), the group's rows inner
-    for (int q = warp; q < wpl; q += nwarps) {
-        const int r = q * 32 + lane;
-        const bool rv = r < K;  // bits past K are 0
-        const int c = r / kk, t = r - c * kk, kh = t / kW, kw = t - kh * kW;
-        const int sh0 = 16 - pW + kw;  // window bit of position ox: sh0 + ox * sW
-        const uint32_t* rowp = rows + c * nrow + kh;
-        for (int yy = 0; yy < ry; ++yy) {
-            const uint64_t win = rv ? ((uint64_t(rowp[yy * sH]) << 16) | pad) : 0ull;
-            for (int ox0 = 0; ox0 < ow; ox0 += 32) {
-                uint32_t mine = 0;
-                if (sW == 1) {
-                    // lane r holds its bits for 32 consecutive positions; a 32 x 32 bit transpose
-                    // across the warp gives lane ox its word: per round a shuffle, a funnel-shift
-                    // rotate and one LOP3 with the lane's loop-invariant keep mask and rotation
-                    uint32_t v = uint32_t(win >> (sh0 + ox0));
-#pragma unroll
-                    for (int jj = 0; jj < 5; ++jj) {
-                        const int j = 16 >> jj;
-                        const uint32_t p = __shfl_xor_sync(0xffffffffu, v, j);
-                        const uint32_t qv = __funnelshift_l(p, p, rot[jj]);
-                        v = (v & keep[jj]) | (qv & ~keep[jj]);
-                    }
-                    mine = v;
-                } else {
-#pragma unroll 8
-                    for (int j = 0; j < 32; ++j) {
-                        const int ox = ox0 + j;
-                        const uint32_t wbits = __ballot_sync(0xffffffffu, (win >> (sh0 + ox * sW)) & 1ull);
-                        if (lane == j) mine = wbits;
-                    }
-                }
-                if (ox0 + lane < ow) tile[(yy * ow + ox0 + lane) * wpl + q] = mine;
-            }
-        }
-    }
+    rowbits_words(rows, tile, W, kH, kW, sH, sW, pW, ow, K, wpl, ry, nrow, warp, nwarps, lane);
     __syncthreads();
     if (y) {
         // Fused conv_forward_binary (network.cpp:65-79) for small layers: the xnor-popcount GEMM
@@ -228,6 +237,7 @@ __global__ void __launch_bounds__(256, 5)
         }
     }
 }
+
 
 }  // namespace
 

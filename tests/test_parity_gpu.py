@@ -109,7 +109,11 @@ GEOMS = [((2, 3, 6, 6), (3, 3, 1, 1, 1, 1, 3, 5)), ((1, 64, 32, 32), (3, 3, 1, 1
          # stride 2, 5x5 / pad 2, a partial last word and rectangular kernels
          ((6, 64, 32, 32), (3, 3, 1, 1, 1, 1, 64, 64)), ((40, 3, 8, 8), (5, 5, 1, 1, 2, 2, 3, 4)),
          ((80, 5, 9, 7), (3, 2, 2, 1, 1, 0, 5, 7)), ((160, 33, 4, 4), (1, 1, 1, 1, 0, 0, 33, 2)),
-         ((150, 7, 5, 11), (2, 3, 1, 2, 0, 1, 7, 2)), ((3, 16, 64, 20), (3, 3, 1, 1, 1, 1, 16, 8))]
+         ((150, 7, 5, 11), (2, 3, 1, 2, 0, 1, 7, 2)), ((3, 16, 64, 20), (3, 3, 1, 1, 1, 1, 16, 8)),
+         # many row groups per SM (a pipelined bulk-copy variant was measured slower and removed):
+         # 32 / 16 / 20 / 4 wide, stride 2, 5x5 pad 2 with a ragged last row group, a partial word
+         ((160, 8, 32, 32), (3, 3, 1, 1, 1, 1, 8, 8)), ((600, 8, 16, 16), (4, 4, 2, 2, 1, 1, 8, 4)),
+         ((300, 4, 20, 20), (5, 5, 1, 1, 2, 2, 4, 3)), ((650, 36, 4, 4), (1, 1, 1, 1, 0, 0, 36, 2))]
 
 
 @pytest.mark.parametrize("shape,g", GEOMS)
