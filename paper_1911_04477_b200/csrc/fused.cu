@@ -1173,7 +1173,7 @@ int launch_swap_t(const CUtensorMap& tm, const FusedGeom& g, cudaStream_t s) {
 // kernel parameter (PixParams): with the channel loops unrolled, every w_d / P_d is a
 // constant-bank operand of the XOR / compare, so a channel costs XOR, POPC, compare, select.
 template <int DW, bool F32, bool POOL>
-__global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 2 : 4) : (DW > 6 ? 4 : 6)) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
+__global__ void __launch_bounds__(256, F32 ? (DW > 6 ? 1 : 4) : (DW > 6 ? 1 : 6)) pix_popc_kernel(const FusedGeom g, const PixParams pp) {
     // PDL: the next layer may start its prologue (it waits for this grid before reading);
     // this grid waits for the pixel packer's words
     asm volatile("griddepcontrol.launch_dependents;");

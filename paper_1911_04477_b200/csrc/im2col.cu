@@ -13,6 +13,7 @@
 // every output word from kW-bit fields of those row words; im2col_sign_pack_kernel is the
 // general one (a load and compare per bit).
 #include <algorithm>
+#include <cstdlib>
 
 #include "bnn_common.cuh"
 
@@ -264,6 +265,7 @@ int launch_im2col_sign_pack(const float* x, size_t B, size_t C, size_t H, size_t
         while (R < 16 && R * 2 <= oh && smem_of(R * 2) <= 48 * 1024 &&
                B * ceil_div(oh, R * 2) >= 2 * size_t(num_sms()))
             R *= 2;
+        if (const char* e = getenv("BNN_IM2COL_R")) R = std::max(1, atoi(e));  // experiments
         if (smem_of(R) <= 48 * 1024) {
             im2col_rowbits_kernel<<<dim3(unsigned(ceil_div(oh, R)), unsigned(B)), 256, smem_of(R), s>>>(
                 x, int(C), int(H), int(W), int(kH), int(kW), int(sH), int(g->stride_w), int(g->pad_h), int(pW),
