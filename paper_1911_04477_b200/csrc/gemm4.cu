@@ -15,6 +15,7 @@
 // columns chosen so the tiles fill the SMs), persistent over tiles when there are more.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "bnn_common.cuh"
 #include "umma.cuh"
@@ -317,6 +318,30 @@ __global__ void __launch_bounds__(256) expand4_kernel(const Expand4Op a, const E
     }
 }
 
+// CL = 2: a CTA pair (cluster of two) computes a 256-row x NB tile with cta_group::2 M = 256
+// instructions issued by the even CTA: each CTA TMA-loads its own 128 A rows and half of the
+// B tile (NB / 2 rows), completing bytes on the leader's full barrier; D rows 0-127 land in the
+// leader's TMEM, 128-255 in the peer's; each CTA's epilogue reads its own TMEM and releases the
+// accumulator on the leader's barrier. Per CTA and K block the shared memory then takes 16 KB +
+// NB x 64 B of TMA writes and the same again of MMA reads: the single-CTA kernel moved 16 KB +
+// NB x 128 B each way per 4 MMAs, more than the ~128 B/cycle an SM's shared memory sustains at
+// the FP4 MMA rate (measured: 0.61 of the FP4 peak single-CTA).
+__device__ __forceinline__ void mma_mxf4_cg2_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t sf, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf)
+        : "memory");
+}
+
+__host__ __device__ constexpr uint32_t idesc_mxf4_mn(int M, int N) {
+    return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(M >> 4) << 24);
+}
+
+template <int CL>
 __global__ void __launch_bounds__(kTThreads, 1)
     xnor4t_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                   const __grid_constant__ G4 g) {
@@ -324,9 +349,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     const int nst = g.nst;
+    const int BH = g.NB / CL;                // B rows per CTA
     uint8_t* sA = smem_raw + (base - raw);   // [nst][128 x 128 B]
-    uint8_t* sB = sA + size_t(nst) * 16384;  // [nst][NB x 128 B]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(nst) * g.NB * 128);
+    uint8_t* sB = sA + size_t(nst) * 16384;  // [nst][BH x 128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + size_t(nst) * BH * 128);
     uint64_t* full = bars;
     uint64_t* empty = bars + kGMaxStages;
     uint64_t* tfull = bars + 2 * kGMaxStages;  // [2]
@@ -334,16 +360,20 @@ __global__ void __launch_bounds__(kTThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
-    const int units = g.m_tiles * g.n_tiles;
-    const uint32_t stage_tx = 16384u + uint32_t(g.NB) * 128u;
+    const int rank = CL == 2 ? int(cluster_ctarank()) : 0;
+    const int mp_tiles = (g.m_tiles + CL - 1) / CL;  // row-tile groups (one per cluster)
+    const int units = mp_tiles * g.n_tiles;
+    const int u0 = int(blockIdx.x) / CL, ustep = int(gridDim.x) / CL;
+    const uint32_t stage_tx = 16384u + uint32_t(BH) * 128u;  // this CTA's bytes per stage
+    auto leader = [&](uint64_t* bar) { return CL == 2 ? mapa(smem_u32(bar), 0) : smem_u32(bar); };
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], CL);  // (the leader's) one expect_tx arrive per CTA
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * CL);  // (the leader's) four epilogue warps per CTA
         }
         fence_mbar_init();
     }
@@ -351,7 +381,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
         tma_prefetch(&tA);
         tma_prefetch(&tB);
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) {
+        if (CL == 2)
+            tmem_alloc_cg2<512>(tmem_slot);
+        else
+            tmem_alloc<512>(tmem_slot);
+    }
     __syncwarp();
     tc_fence_before();
     __syncthreads();
@@ -369,72 +404,111 @@ __global__ void __launch_bounds__(kTThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (CL == 2) cluster_sync();  // the peer's barriers and scale factors are ready
     tc_fence_after();
 
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+            for (int u = u0; u < units; u += ustep) {
+                const int mt = (u % mp_tiles) * CL + rank, nt = u / mp_tiles;
                 for (int kb = 0; kb < g.KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], stage_tx);
-                    tma_load_2d(&tA, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
-                    tma_load_2d(&tB, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
+                    uint8_t* da = sA + size_t(stage) * 16384;
+                    uint8_t* db = sB + size_t(stage) * BH * 128;
+                    if (CL == 2) {
+                        const uint32_t fb = leader(&full[stage]);
+                        mbar_arrive_expect_tx_cluster(fb, stage_tx);
+                        tma_load_2d_cg2(&tA, fb, da, kb * 128, mt * 128);
+                        tma_load_2d_cg2(&tB, fb, db, kb * 128, nt * g.NB + rank * BH);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], stage_tx);
+                        tma_load_2d(&tA, &full[stage], da, kb * 128, mt * 128);
+                        tma_load_2d(&tB, &full[stage], db, kb * 128, nt * g.NB);
+                    }
+                    if (++stage == nst) stage = 0, phase ^= 1;
+                }
+            }
+            if (CL == 2) {  // every stage's last release (the pair MMA's multicast commit) has landed
+                for (int k = 0; k < nst; ++k) {
+                    mbar_wait(&empty[stage], phase ^ 1);
                     if (++stage == nst) stage = 0, phase ^= 1;
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
-        const uint32_t idesc = idesc_mxf4_m128(g.NB);
-        int stage = 0, i = 0;
-        uint32_t phase = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-            const int acc = g.accs == 2 ? (i & 1) : 0, use = g.accs == 2 ? (i >> 1) : i;
-            const uint32_t d = tmem_base + uint32_t(acc * 256);
-            mbar_wait(&tempty[acc], (use & 1) ^ 1);
-            tc_fence_after();
-            for (int kb = 0; kb < g.KB; ++kb) {
-                mbar_wait(&full[stage], phase);
+        if (CL == 1 || rank == 0) {
+            const uint32_t idesc = idesc_mxf4_mn(128 * CL, g.NB);
+            int stage = 0, i = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < units; u += ustep, ++i) {
+                const int acc = i & 1, use = i >> 1;
+                const uint32_t d = tmem_base + uint32_t(acc * 256);
+                mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(sA + size_t(stage) * 16384);
-                const uint32_t b0 = smem_u32(sB + size_t(stage) * g.NB * 128);
-                const int nk = min(4, (g.L - 256 * kb + 63) / 64);  // 64-element steps with data
+                for (int kb = 0; kb < g.KB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + size_t(stage) * 16384);
+                    const uint32_t b0 = smem_u32(sB + size_t(stage) * BH * 128);
+                    const int nk = min(4, (g.L - 256 * kb + 63) / 64);  // 64-element steps with data
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (k >= nk) break;
-                    mma_mxf4_w(d, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc, tmem_base + kGSfCol,
-                               (kb != 0 || k != 0));
+                    for (int k = 0; k < 4; ++k) {
+                        if (k >= nk) break;
+                        if (CL == 2)
+                            mma_mxf4_cg2_w(d, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                           tmem_base + kGSfCol, (kb != 0 || k != 0));
+                        else
+                            mma_mxf4_w(d, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
+                                       tmem_base + kGSfCol, (kb != 0 || k != 0));
+                    }
+                    if (CL == 2) {
+                        mma_commit_cg2_mc_w(&empty[stage], uint16_t(3));  // both CTAs' slots free
+                        if (kb == g.KB - 1) mma_commit_cg2_mc_w(&tfull[acc], uint16_t(3));
+                    } else {
+                        mma_commit_w(&empty[stage]);
+                        if (kb == g.KB - 1) mma_commit_w(&tfull[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == nst) stage = 0, phase ^= 1;
                 }
-                mma_commit_w(&empty[stage]);
-                if (kb == g.KB - 1) mma_commit_w(&tfull[acc]);
-                __syncwarp();
-                if (++stage == nst) stage = 0, phase ^= 1;
             }
+            // the epilogues have released the last accumulators (CL = 2: the peer's remote
+            // arrives have then all landed here)
+            for (int k = 0; k < 2; ++k, ++i) mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);
         }
     } else {
         const int q = warp & 3;
         int i = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-            const int acc = g.accs == 2 ? (i & 1) : 0, use = g.accs == 2 ? (i >> 1) : i;
-            const int mt = u % g.m_tiles, nt = u / g.m_tiles;
+        for (int u = u0; u < units; u += ustep, ++i) {
+            const int acc = i & 1, use = i >> 1;
+            const int mt = (u % mp_tiles) * CL + rank, nt = u / mp_tiles;
             mbar_wait(&tfull[acc], use & 1);
             tc_fence_after();
             store_tile(g, tmem_base + uint32_t(acc * 256) + (uint32_t(q * 32) << 16), mt * 128 + q * 32 + lane,
                        nt * g.NB);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (CL == 2)
+                    mbar_arrive_cluster(leader(&tempty[acc]));
+                else
+                    mbar_arrive(&tempty[acc]);
+            }
         }
     }
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (CL == 2) cluster_sync_relaxed();  // every cross-CTA operation has landed (drains above)
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if (CL == 2)
+            tmem_dealloc_cg2<512>(tmem_base);
+        else
+            tmem_dealloc<512>(tmem_base);
     }
 }
 
@@ -456,7 +530,8 @@ int pick_nb_t(int m_tiles, int N, int sms) {
 int launch_xnor4t(G4 g, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(xnor4t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGSmemMax)));
+        BNN_CUDA(cudaFuncSetAttribute(xnor4t_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGSmemMax)));
+        BNN_CUDA(cudaFuncSetAttribute(xnor4t_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kGSmemMax)));
         attr_set = true;
     }
     g.Lw = (g.L + 31) / 32;
@@ -466,7 +541,6 @@ int launch_xnor4t(G4 g, cudaStream_t s) {
     g.NB = pick_nb_t(g.m_tiles, g.N, sms);
     g.accs = 2;
     g.n_tiles = (g.N + g.NB - 1) / g.NB;
-    g.nst = int(std::min<size_t>(kGMaxStages, (kGSmemMax - 1024 - 256) / (16384 + size_t(g.NB) * 128)));
     // operands expanded once to e2m1 in stream-ordered scratch, 16 B per packed word
     const size_t lb = size_t(g.Lw) * 16;
     Scratch ea, eb;
@@ -477,14 +551,37 @@ int launch_xnor4t(G4 g, cudaStream_t s) {
     BNN_TRY(launch_check("expand4_kernel"));
     CUtensorMap ta, tb;
     BNN_TRY(make_tmap_2d_s8(&ta, ea.p, size_t(g.M), lb, lb, 128));
-    BNN_TRY(make_tmap_2d_s8(&tb, eb.p, size_t(g.N), lb, lb, uint32_t(g.NB)));
-    const int units = g.m_tiles * g.n_tiles;
+    // CTA pairs (cta_group::2, 256 rows per pair) when there are at least two row tiles
+    static const int cl_env = getenv("BNN_XNOR4T_CLUSTER") ? atoi(getenv("BNN_XNOR4T_CLUSTER")) : 2;
+    const int CL = (cl_env == 2 && g.m_tiles >= 2) ? 2 : 1;
+    const size_t stage_bytes = 16384 + size_t(g.NB / CL) * 128;
+    g.nst = int(std::min<size_t>(kGMaxStages, (kGSmemMax - 1024 - 256) / stage_bytes));
+    BNN_TRY(make_tmap_2d_s8(&tb, eb.p, size_t(g.N), lb, lb, uint32_t(g.NB / CL)));
+    const int units = (g.m_tiles + CL - 1) / CL * g.n_tiles;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(std::min(units, sms)));
+    cfg.gridDim = dim3(unsigned(CL * std::min(units, sms / CL)));
     cfg.blockDim = dim3(unsigned(kTThreads));
-    cfg.dynamicSmemBytes = 1024 + size_t(g.nst) * (16384 + size_t(g.NB) * 128) + 256;
+    cfg.dynamicSmemBytes = 1024 + size_t(g.nst) * stage_bytes + 256;
     cfg.stream = s;
-    BNN_CUDA(cudaLaunchKernelEx(&cfg, xnor4t_kernel, ta, tb, g));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(CL);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (CL == 2) {  // persistent: no more clusters than can be co-resident
+        static int max_clusters = -1;
+        if (max_clusters < 0) {
+            int n = 0;
+            max_clusters = cudaOccupancyMaxActiveClusters(&n, xnor4t_kernel<2>, &cfg) == cudaSuccess && n > 0 ? n : sms / 2;
+        }
+        cfg.gridDim = dim3(unsigned(2 * std::min(units, max_clusters)));
+    }
+    if (CL == 2)
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, xnor4t_kernel<2>, ta, tb, g));
+    else
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, xnor4t_kernel<1>, ta, tb, g));
     set_last_gemm("xnor4t_kernel");
     return launch_check("xnor4t_kernel");
 }

@@ -49,6 +49,27 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.iters
+            dev_ms = None
+            try:  # device-only: the calls captured into one CUDA graph (host overhead excluded)
+                st = torch.cuda.Stream()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(st):
+                    run_s = lambda: bnn._lib.check(lib.bnn_xnor_gemm_s32(w.data_ptr(), wpl, x.data_ptr(), wpl, M, N, L,
+                                                                         out.data_ptr(), N, st.cuda_stream))
+                    run_s()
+                    st.synchronize()
+                    with torch.cuda.graph(g, stream=st):
+                        for _ in range(5):
+                            run_s()
+                    g.replay()
+                    st.synchronize()
+                    e0.record(st)
+                    g.replay()
+                    e1.record(st)
+                    st.synchronize()
+                dev_ms = e0.elapsed_time(e1) / 5
+            except Exception as e:  # noqa: BLE001
+                dev_ms = f"not capturable: {e}"
             same = None
             if ref is None:
                 ref = out.clone()
@@ -56,6 +77,8 @@ def main():
                 same = bool(torch.equal(ref, out))
             print(json.dumps({"M": M, "N": N, "L": L, "kernel": lib.bnn_last_gemm_kernel().decode(),
                               "ms": round(ms, 4), "Tbops": round(2 * M * N * L / ms / 1e9, 1),
+                              "device_ms": dev_ms if not isinstance(dev_ms, float) else round(dev_ms, 4),
+                              "device_Tbops": round(2 * M * N * L / dev_ms / 1e9, 1) if isinstance(dev_ms, float) else None,
                               "matches_first": same}), flush=True)
     lib.bnn_set_gemm_policy(0)
 
