@@ -113,8 +113,6 @@ struct LinGeom {
     int tmab;                 // 1: images TMA-loaded from in4 (expanded once by expand_act4), no producers
     uint8_t* in4;             // [B, Kw * 16] e2m1 images when tmab
     uint8_t* out4;            // FEPI_BITS: write [B, Dw * 16] e2m1 (the next layer's in4) instead of out_bits
-    int cl;                   // 2: clusters of two feature tiles multicasting the image tile (tmab, no split)
-    int pf;                   // 1: prefetch the CTA's weight slice into L2 at entry
 };
 bool lin4_plan(const FusedGeom& g, int epi, LinGeom& l);
 // Images [B, Kw] packed bits -> e2m1 {0, 1.0} lines [B, Kw * 16 bytes] in put_word4's order.

@@ -87,11 +87,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 
 }  // namespace
 
-// CL = 2 (TMA-loaded images, no split): clusters of two CTAs on adjacent feature tiles of the
-// same image tile; each loads its own weight tile and half of the image tile, multicast into
-// both (the image tile is the bigger operand: NB x 128 B per K block against 16 KB of weights),
-// and each MMA commit frees the stage in both CTAs.
-template <int CL>
 __global__ void __launch_bounds__(kLThreads, 1)
     lin4_kernel(const __grid_constant__ CUtensorMap tmW4, const __grid_constant__ CUtensorMap tmX4,
                 const __grid_constant__ LinGeom g) {
@@ -110,10 +105,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
 
     const int warp = warp_uniform(int(threadIdx.x >> 5)), lane = threadIdx.x & 31;
     asm volatile("griddepcontrol.launch_dependents;");
-    const int rank = CL == 2 ? int(cluster_ctarank()) : 0;
-    const int mp_tiles = (g.m_tiles + CL - 1) / CL;
-    const int units = mp_tiles * g.n_tiles * g.ksplit;
-    const int u0 = int(blockIdx.x) / CL, ustep = int(gridDim.x) / CL;
+    const int units = g.m_tiles * g.n_tiles * g.ksplit;
     const unsigned long long t_start = (g.dbg || g.tl) ? lgtimer() : 0;
     if (g.tl && threadIdx.x == 0) g.tl[blockIdx.x * 4 + 0] = t_start;
     // BNN_LIN4_PROFILE: per-phase times (ns since the CTA started, summed over CTAs)
@@ -125,7 +117,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         if (g.tmab) tma_prefetch(&tmX4);
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], g.tmab ? 1 : 1 + 8);  // TMA arrive (expect_tx) [+ 8 producer warps]
-            mbar_init(&empty[s], CL);
+            mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
         mbar_init(tempty, 4);
@@ -135,7 +127,6 @@ __global__ void __launch_bounds__(kLThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
-    if (CL == 2) cluster_sync();  // both CTAs' barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem_base = warp_uniform(*tmem_slot);
     if (warp >= 2 && warp < 6) {  // block scales: every byte of columns [496, 512) = 2^0
@@ -156,8 +147,8 @@ __global__ void __launch_bounds__(kLThreads, 1)
     auto decode = [&](int u, int& mt, int& nt, int& ks) {
         ks = u % g.ksplit;
         const int t = u / g.ksplit;
-        mt = (t % mp_tiles) * CL + rank;
-        nt = t / mp_tiles;
+        mt = t % g.m_tiles;
+        nt = t / g.m_tiles;
     };
     auto kb_range = [&](int ks, int& kb0, int& kb1) {
         kb0 = ks * g.kbs;
@@ -171,16 +162,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
             int stage = 0, issued = 0;
             uint32_t phase = 0;
             const uint32_t btx = g.tmab ? uint32_t(g.NB) * 128u : 0u;
-            if (g.pf) {  // the CTA's whole weight slice on its way from HBM into L2 up front: the
-                         // ring's TMA loads then wait on L2, not on HBM latency
-                for (int u = u0; u < units; u += ustep) {
-                    int mt, nt, ks, kb0, kb1;
-                    decode(u, mt, nt, ks);
-                    kb_range(ks, kb0, kb1);
-                    for (int kb = kb0 + nst; kb < kb1; ++kb) tma_prefetch_l2_2d(&tmW4, kb * 128, mt * 128);
-                }
-            }
-            for (int u = u0; u < units; u += ustep) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int mt, nt, ks, kb0, kb1;
                 decode(u, mt, nt, ks);
                 kb_range(ks, kb0, kb1);
@@ -190,11 +172,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     tma_load_2d(&tmW4, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
                     if (g.tmab) {
                         if (issued == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-                        if (CL == 2)
-                            tma_load_2d_mc(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128 + size_t(rank) * g.NB * 64,
-                                           kb * 128, nt * g.NB + rank * (g.NB / 2), uint16_t(3));
-                        else
-                            tma_load_2d(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
+                        tma_load_2d(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
                     }
                     if (++stage == nst) stage = 0, phase ^= 1;
                 }
@@ -204,7 +182,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         const uint32_t idesc = idesc_mxf4_m128(g.NB);
         int stage = 0, i = 0;
         uint32_t phase = 0;
-        for (int u = u0; u < units; u += ustep, ++i) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
             int mt, nt, ks, kb0, kb1;
             decode(u, mt, nt, ks);
             kb_range(ks, kb0, kb1);
@@ -222,10 +200,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
                     mma_mxf4_w(tmem_base, sdesc_k_sw128(a0 + 32 * k), sdesc_k_sw128(b0 + 32 * k), idesc,
                                tmem_base + kLSfCol, (kb != kb0 || k != 0));
                 }
-                if (CL == 2)
-                    mma_commit_mc_w(&empty[stage], uint16_t(3));
-                else
-                    mma_commit_w(&empty[stage]);
+                mma_commit_w(&empty[stage]);
                 if (kb == kb1 - 1) mma_commit_w(tfull);
                 __syncwarp();
                 if (++stage == nst) stage = 0, phase ^= 1;
@@ -241,7 +216,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         if (g.tl && warp == 2 && lane == 0) g.tl[blockIdx.x * 4 + 2] = lgtimer();
         const int q = warp & 3;
         int i = 0;
-        for (int u = u0; u < units; u += ustep, ++i) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
             int mt, nt, ks;
             decode(u, mt, nt, ks);
             const int d0 = mt * 128 + q * 32, d = d0 + lane, b0 = nt * g.NB;
@@ -303,7 +278,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         const int r = int(threadIdx.x) - 6 * 32;  // 0..255
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = u0; u < units; u += ustep) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
             int mt, nt, ks, kb0, kb1;
             decode(u, mt, nt, ks);
             kb_range(ks, kb0, kb1);
@@ -354,7 +329,6 @@ __global__ void __launch_bounds__(kLThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
-    if (CL == 2) cluster_sync();  // the peer's multicasts into / commits onto this CTA are done
     if (g.ksplit > 1) {
         // Split-K completion in the same launch (one unit per CTA when split: lin4_plan). Once
         // every slice of this (feature, image) tile has written its partial sums, slice ks
@@ -516,14 +490,8 @@ bool lin4_plan(const FusedGeom& fg, int epi, LinGeom& l) {
     // expanded by many feature tiles (BNN_LIN4_TMA=0/1 forces it off/on).
     if (g_lin4_tma == -2) g_lin4_tma = getenv("BNN_LIN4_TMA") ? atoi(getenv("BNN_LIN4_TMA")) : -1;
     l.tmab = g_lin4_tma >= 0 ? (g_lin4_tma != 0) : (l.m_tiles >= 4 && fg.B >= 512);
-    // TMA-loaded images without a K split: pairs of feature tiles share (multicast) the image
-    // tile (BNN_LIN4_CLUSTER=1 turns it off)
-    static const int cl_env = getenv("BNN_LIN4_CLUSTER") ? atoi(getenv("BNN_LIN4_CLUSTER")) : 1;
-    l.cl = (cl_env == 2 && l.tmab && l.ksplit == 1 && l.m_tiles >= 2 && l.NB % 16 == 0) ? 2 : 1;
     l.in4 = nullptr;
     l.out4 = nullptr;
-    static const int pf_env = getenv("BNN_LIN4_PREFETCH") ? atoi(getenv("BNN_LIN4_PREFETCH")) : 1;
-    l.pf = pf_env;
     return true;
 }
 
@@ -534,41 +502,27 @@ size_t lin4_ws_bytes(const LinGeom& l) { return l.ksplit > 1 ? size_t(l.ksplit) 
 int launch_lin4(const CUtensorMap& tm4, const CUtensorMap& tmx, const LinGeom& l, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        BNN_CUDA(cudaFuncSetAttribute(lin4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLSmem)));
-        BNN_CUDA(cudaFuncSetAttribute(lin4_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLSmem)));
+        BNN_CUDA(cudaFuncSetAttribute(lin4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kLSmem)));
         attr_set = true;
     }
-    const int units = (l.m_tiles + l.cl - 1) / l.cl * l.n_tiles * l.ksplit;
+    const int units = l.m_tiles * l.n_tiles * l.ksplit;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(l.cl * std::min(units, num_sms() / l.cl)));
+    cfg.gridDim = dim3(unsigned(std::min(units, num_sms())));
     cfg.blockDim = dim3(unsigned(kLThreads));
     cfg.dynamicSmemBytes = 1024 + size_t(l.nst) * (16384 + size_t(l.NB) * 128) + 256;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = unsigned(l.cl);
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = l.cl == 2 ? 2 : 1;
-    if (l.cl == 2) {  // no more clusters than can be co-resident
-        static int max_clusters = -1;
-        if (max_clusters < 0) {
-            int n = 0;
-            max_clusters = cudaOccupancyMaxActiveClusters(&n, lin4_kernel<2>, &cfg) == cudaSuccess && n > 0 ? n : num_sms() / 2;
-        }
-        cfg.gridDim = dim3(unsigned(2 * std::min(units, max_clusters)));
-    }
-    auto kern = l.cl == 2 ? lin4_kernel<2> : lin4_kernel<1>;
+    cfg.numAttrs = 1;
     static const bool prof = getenv("BNN_LIN4_PROFILE") != nullptr;
     LinGeom lt = l;
     lt.tl = fused_timeline_slot(1);
     if (lt.tl) fused_timeline_name(("lin4 D=" + std::to_string(l.D) + " K=" + std::to_string(l.K) + " split=" +
                                     std::to_string(l.ksplit)).c_str());
     if (!prof) {
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm4, tmx, lt));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, tmx, lt));
         BNN_TRY(launch_check("lin4_kernel"));
     } else {  // synchronous, not capturable: tools only
         LinGeom lp = l;
@@ -578,7 +532,7 @@ int launch_lin4(const CUtensorMap& tm4, const CUtensorMap& tmx, const LinGeom& l
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
-        BNN_CUDA(cudaLaunchKernelEx(&cfg, kern, tm4, tmx, lp));
+        BNN_CUDA(cudaLaunchKernelEx(&cfg, lin4_kernel, tm4, tmx, lp));
         cudaEventRecord(e1, s);
         BNN_TRY(launch_check("lin4_kernel"));
         BNN_CUDA(cudaStreamSynchronize(s));

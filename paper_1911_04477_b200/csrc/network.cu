@@ -860,7 +860,7 @@ int forward_fused(bnn_net* net, const float* x, size_t B, float* logits, cudaStr
         pl.lg.in4 = net->lin_x4[k].as<uint8_t>();
         k ^= 1;
         const size_t lb = size_t(pl.lg.Kw) * 16;
-        BNN_TRY(make_tmap_2d_s8(&pl.tmx, pl.lg.in4, size_t(pl.lg.B), lb, lb, uint32_t(pl.lg.NB / pl.lg.cl)));
+        BNN_TRY(make_tmap_2d_s8(&pl.tmx, pl.lg.in4, size_t(pl.lg.B), lb, lb, uint32_t(pl.lg.NB)));
         if (i > 0 && plans[i - 1].lin4 && plans[i - 1].lg.epi == FEPI_BITS && plans[i - 1].lg.Dw == pl.lg.Kw) {
             plans[i - 1].lg.out4 = pl.lg.in4;
             pl.in4_ready = true;
