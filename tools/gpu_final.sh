@@ -10,3 +10,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"fused|pix_tile|pix_popc|halo4|lin4|logits" -c 9 -o gpurun_out/prof_b256 -f python tools/prof_net.py 256 > gpurun_out/prof.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/prof.log
 tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/prof.log
+timeout 300 python tools/gemm_bench.py --kernels umma,tma --shapes 1024,1024,1024 4096,1024,9216 1000,1024,4096 4096,4096,4096 128,262144,1152 8192,8192,8192 16384,16384,16384 > gpurun_out/gemm_crossover.jsonl 2>&1
+timeout 120 python tools/timeline.py 256 > gpurun_out/timeline_b256.log 2>&1
+timeout 120 python tools/timeline.py 1024 fc4 > gpurun_out/timeline_fc4.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"xnor4t" -c 1 -o gpurun_out/prof_xnor4t -f python tools/gemm_bench.py --kernels tma --iters 1 --shapes 8192,8192,8192 > gpurun_out/prof_xnor4t.log 2>&1; echo "ncu xnor4t rc=$?" >> gpurun_out/prof_xnor4t.log
