@@ -2,6 +2,7 @@
 each checked against the oracle (run under `compute-sanitizer --tool memcheck|racecheck|synccheck`).
 
     python tools/sanitize.py [quick]   # quick: the default setting at batches 1 and 5 only
+    python tools/sanitize.py tma       # the TMA-fed kernels: xnor4t CTA pairs, lin4 TMA-loaded images
 """
 import sys
 
@@ -22,6 +23,29 @@ QUICK = len(sys.argv) > 1 and sys.argv[1] == "quick"
 if QUICK:
     SETTINGS = {"default": {}}
 bad = 0
+if len(sys.argv) > 1 and sys.argv[1] == "tma":
+    SETTINGS = {}
+    lib.bnn_set_gemm_policy(3)  # xnor4t: CTA pairs when there are >= 2 row tiles
+    for (m, n, L) in ((300, 481, 257), (129, 241, 2050), (1024, 600, 1030)):
+        w = orc.pack(orc.fill_random((m, L), m), "rows", True)
+        xx = orc.pack(orc.fill_random((L, n), n), "cols", True)
+        got = bnn.xnor_gemm(bnn.PackedBitMatrix(m, L, "rows", w), bnn.PackedBitMatrix(L, n, "cols", xx), L)
+        ok = np.array_equal(got, orc.xnor_gemm(w, xx, L)) and lib.bnn_last_gemm_kernel().decode() == "xnor4t_kernel"
+        bad += not ok
+        print("xnor4t", m, n, L, ok, flush=True)
+    lib.bnn_set_gemm_policy(0)
+    G = [{"kind": "affine_norm"}, {"kind": "htanh"}, {"kind": "sign"}]
+    layers = [{"kind": "linear", "out_features": 992}] + G + [{"kind": "linear", "out_features": 544}] + G + \
+             [{"kind": "linear", "out_features": 10}]
+    for mode, b in ((2, 5), (1, 600)):  # forced TMA-loaded images / auto (e2m1 epilogue hand-off)
+        lib.bnn_set_fused_lin4(mode)
+        net = bnn.Network(layers, (2336, 1, 1), 41)
+        net.set_engine("fused")
+        x = orc.fill_random((b, 2336, 1, 1), 7)
+        ok = np.array_equal(net.forward(x), orc.net(layers, (2336, 1, 1), 41).forward(x))
+        bad += not ok
+        print("lin4 tma", mode, b, ok, flush=True)
+    lib.bnn_set_fused_lin4(1)
 for name, st in SETTINGS.items():
     lib.bnn_set_fused_split(st.get("split", 0))
     lib.bnn_set_fused_halo(st.get("halo", 1))
