@@ -1,6 +1,8 @@
 // K3 on the FP4 tensor cores for the standalone operator API: xnor_gemm (kernels.cpp:53-88),
 // its float epilogue (to_float + bias_add, kernels.cpp:90-107) and the conv_forward_binary
-// scatter (reshape_output, lowering.cpp:87-95), in ONE launch straight from the packed bits.
+// scatter (reshape_output, lowering.cpp:87-95), in ONE launch straight from the packed bits
+// (xnor4_kernel); for large products (>= 2^32 bit-MACs, M, N >= 512) the operands are expanded
+// once into HBM and streamed by TMA into CTA pairs (expand4_kernel + xnor4t_kernel, below).
 //
 // Both operands are the reference's packed lines (W row-packed [M x ldw], X col-packed
 // [N x ldx], bit j of word q = element 32q + j, 1 = +1) expanded in shared memory to e2m1
@@ -48,7 +50,6 @@ struct G4 {
     float* out_f32;      // [N / P][M][P] (f32 epilogue: float(acc) + bias[m])
     const float* bias;
     int P;
-    int accs;  // TMEM accumulators (xnor4t_kernel)
 };
 
 __host__ __device__ constexpr uint32_t idesc_mxf4_m128(int N) {
@@ -539,7 +540,6 @@ int launch_xnor4t(G4 g, cudaStream_t s) {
     g.m_tiles = (g.M + 127) / 128;
     const int sms = num_sms();
     g.NB = pick_nb_t(g.m_tiles, g.N, sms);
-    g.accs = 2;
     g.n_tiles = (g.N + g.NB - 1) / g.NB;
     // operands expanded once to e2m1 in stream-ordered scratch, 16 B per packed word
     const size_t lb = size_t(g.Lw) * 16;
