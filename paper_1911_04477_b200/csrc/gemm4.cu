@@ -84,10 +84,18 @@ __device__ __forceinline__ void put_pm1(uint32_t tile, int r, int chunk, uint32_
 __device__ __forceinline__ void load_block(const uint32_t* base, size_t ld, int line, bool live, int kb, int Lw, int L,
                                            uint32_t (&w)[8], uint32_t (&m)[8]) {
     const uint32_t* src = base + size_t(live ? line : 0) * ld;
+    // the block's 8 words are one 32-byte sector: two 16-byte loads when the line is 16-byte
+    // aligned (a warp's scalar loads touch 32 lines each: L1 wavefronts bounded the kernel)
+    const bool vec = live && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && 8 * kb + 8 <= Lw;
+    if (vec) {
+        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src + 8 * kb));
+        const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src + 8 * kb + 4));
+        w[0] = lo.x, w[1] = lo.y, w[2] = lo.z, w[3] = lo.w, w[4] = hi.x, w[5] = hi.y, w[6] = hi.z, w[7] = hi.w;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const int q = 8 * kb + k;
-        w[k] = (live && q < Lw) ? __ldg(src + q) : 0u;
+        if (!vec) w[k] = (live && q < Lw) ? __ldg(src + q) : 0u;
         const int nv = L - 32 * q;  // valid elements in word q
         m[k] = !live || nv <= 0 ? 0u : nv >= 32 ? 0xffffffffu : ((1u << nv) - 1u);
     }

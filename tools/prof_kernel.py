@@ -1,6 +1,6 @@
 """Run one K1/K2/K3 launch at the bench shapes (for ncu captures).
 
-    python tools/prof_kernel.py im2col|pack_cols|pack_rows|gemm_popc|gemm_xnor4|conv_b1|probes
+    python tools/prof_kernel.py im2col|pack_cols|pack_rows|gemm_popc|gemm_xnor4|gemm_xnor4_conv|conv_b1|probes
 """
 import ctypes as C
 import os
@@ -23,7 +23,8 @@ if what == "im2col":
     for _ in range(2):
         _lib.check(lib.bnn_im2col_sign_pack_f32(x.data_ptr(), 256, 128, 32, 32, C.byref(g), out.data_ptr(), 36, S))
 elif what.startswith("gemm"):
-    M = N = L = 1024
+    # gemm_xnor4_conv: the conv-shaped product of VGG conv1 at batch 256 (M = 128, N = 262144)
+    M, N, L = (128, 262144, 1152) if what.endswith("_conv") else (1024, 1024, 1024)
     w = torch.randint(-2**31, 2**31 - 1, (M, L // 32), dtype=torch.int32, device="cuda")
     x = torch.randint(-2**31, 2**31 - 1, (N, L // 32), dtype=torch.int32, device="cuda")
     out = torch.empty((M, N), dtype=torch.int32, device="cuda")
