@@ -29,6 +29,9 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict_
                                                         size_t L, uint32_t* __restrict__ words,
                                                         size_t ld, size_t wpl,
                                                         unsigned long long* first_bad) {
+    // E2M1 (the fused engine's first layer): the dependent TMA-fed linear launch may start its
+    // prologue and weight loads now; it waits for this grid before reading the images
+    if (E2M1) asm volatile("griddepcontrol.launch_dependents;");
     const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const size_t chunks = (wpl + 31) / 32;

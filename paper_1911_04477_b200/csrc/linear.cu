@@ -159,21 +159,35 @@ __global__ void __launch_bounds__(kLThreads, 1)
         // weights: build-time constants, loaded ahead of the grid dependency (with TMA-loaded
         // images: the first ring's weights, then the wait, then both operands)
         if (lane == 0) {
-            int stage = 0, issued = 0;
+            int stage = 0;
             uint32_t phase = 0;
             const uint32_t btx = g.tmab ? uint32_t(g.NB) * 128u : 0u;
+            int pre = 0;  // K blocks of the first unit whose weights went out before the wait
+            if (g.tmab && int(blockIdx.x) < units) {
+                // the whole first ring of weights ahead of the grid dependency, their images after
+                int mt, nt, ks, kb0, kb1;
+                decode(int(blockIdx.x), mt, nt, ks);
+                kb_range(ks, kb0, kb1);
+                pre = min(nst, kb1 - kb0);
+                for (int j = 0; j < pre; ++j) {
+                    mbar_arrive_expect_tx(&full[j], 16384 + btx);
+                    tma_load_2d(&tmW4, &full[j], sA + size_t(j) * 16384, (kb0 + j) * 128, mt * 128);
+                }
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                for (int j = 0; j < pre; ++j)
+                    tma_load_2d(&tmX4, &full[j], sB + size_t(j) * g.NB * 128, (kb0 + j) * 128, nt * g.NB);
+                stage = pre == nst ? 0 : pre;
+                phase = pre == nst ? 1u : 0u;
+            }
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int mt, nt, ks, kb0, kb1;
                 decode(u, mt, nt, ks);
                 kb_range(ks, kb0, kb1);
-                for (int kb = kb0; kb < kb1; ++kb, ++issued) {
+                for (int kb = kb0 + (u == int(blockIdx.x) ? pre : 0); kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], 16384 + btx);
                     tma_load_2d(&tmW4, &full[stage], sA + size_t(stage) * 16384, kb * 128, mt * 128);
-                    if (g.tmab) {
-                        if (issued == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-                        tma_load_2d(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
-                    }
+                    if (g.tmab) tma_load_2d(&tmX4, &full[stage], sB + size_t(stage) * g.NB * 128, kb * 128, nt * g.NB);
                     if (++stage == nst) stage = 0, phase ^= 1;
                 }
             }
