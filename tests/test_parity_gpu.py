@@ -166,10 +166,15 @@ def test_gemm_all_agree_all_disagree(bnn, L):
     assert (bnn.xnor_gemm(ones, minus, L) == -L).all()
 
 
-def test_gemm_device_api_strides_and_bias(bnn, orc):
+@pytest.mark.parametrize("kernel", ["auto", "popc", "umma", "tma"])
+@pytest.mark.parametrize("M", [70, 300])
+def test_gemm_device_api_strides_and_bias(bnn, orc, policy, kernel, M):
+    """Padded leading dimensions (garbage past each line), an output stride and the bias epilogue
+    on every K3 kernel (tma with M = 300: a CTA pair whose second half is out of range)."""
     torch = torch_cuda()
     lib = bnn.load()
-    M, N, L = 70, 90, 200
+    policy(kernel)
+    N, L = 90, 200
     wpl, ldw, ldx, ldo = 7, 9, 12, 100
     w = orc.pack(orc.fill_random((M, L), 1), "rows", True)
     x = orc.pack(orc.fill_random((L, N), 2), "cols", True)
