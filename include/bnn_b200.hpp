@@ -168,7 +168,10 @@ inline int word_dot(std::uint32_t w, std::uint32_t x) noexcept { return 2 * popc
 FloatMatrix float_gemm(const FloatMatrix& w, const FloatMatrix& x, unsigned threads = 1);
 // Direct convolution of one batch slice (kernels.hpp:63-64), bit-identical.
 FloatTensor naive_conv(const FloatTensor& x, std::size_t batch_index, const FloatTensor& w, const ConvGeometry& geom);
-// `threads` is accepted for source compatibility; the device grid replaces it.
+// `threads` is accepted for source compatibility; the device grid replaces it. The kernel
+// follows the product size (bnn_set_gemm_policy, include/bnn_cuda.h): LOP3 + POPC below 2^26
+// bit-MACs, FP4 tensor cores with in-CTA operand expansion up to 2^32, TMA-fed FP4 CTA pairs
+// over operands expanded once in HBM above; every choice is bit-exact.
 IntMatrix xnor_gemm(const PackedBitMatrix& w, const PackedBitMatrix& x, std::size_t inner_len,
                     unsigned threads = 1);
 FloatMatrix to_float(const IntMatrix& m);
