@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
     } else if (warp >= 6) {
         // producers: thread t expands W line mt*128 + t (t < 128) and X line nt*NB + t (t < NB)
         const int t = int(threadIdx.x) - 6 * 32;
-        int stage = 0;
+        int stage = 0, pending = -1;  // pending: a filled stage whose fence + release waits for the next
         uint32_t phase = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
             const int mt = u % g.m_tiles, nt = u / g.m_tiles;
@@ -257,11 +257,25 @@ __global__ void __launch_bounds__(kGThreads, 1) xnor4_kernel(const __grid_consta
 #pragma unroll
                     for (int k = 0; k < 8; ++k) put_pm1(tbb, t, k, bw[k], bm8[k]);
                 }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[stage]);
+                // one proxy fence per two filled stages (released together)
+                if (pending >= 0) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&full[pending]);
+                        mbar_arrive(&full[stage]);
+                    }
+                    pending = -1;
+                } else {
+                    pending = stage;
+                }
                 if (++stage == nst) stage = 0, phase ^= 1;
             }
+        }
+        if (pending >= 0) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[pending]);
         }
     }
     __syncwarp();
